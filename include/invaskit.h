@@ -1,0 +1,125 @@
+/*
+ * libinvaskit — B200 (sm_100a) Inv-ASKIT factorization and solve, C ABI.
+ *
+ * This is the drop-in boundary for the reference's factor/solve entry points
+ * (kernelsolve 0.1.0, /root/reference/pkg/src/kernelsolve):
+ *
+ *   ks_create + ks_factorize   replace  factorize(ck, lam, threads)   solver.py:92-189
+ *   ks_solve                   replaces solve(hf, b)                  solver.py:192-197
+ *                                       solve_many(hf, B)             solver.py:200-213
+ *   ks_get_diag / ks_get_z_cond / ks_get_fallback_nodes
+ *                              expose   HierFactor.diagnostics       solver.py:111-116,175-188
+ *   ks_get_node_h / ks_get_leaf_factor
+ *                              expose   NodeFactor.H / LeafFactor.factor (parity debugging)
+ *
+ * The problem is passed exactly as the reference's CompressedKernel holds it
+ * (compress.py:93-142, tree.py:53-81): points in ORIGINAL order, the tree
+ * permutation, BFS node table, skeleton ids (global point ids, pivot order)
+ * and interpolation matrices P (rank x |cand|, row-major). Plain pointers and
+ * sizes only; the library copies what it needs to the device at create time.
+ *
+ * Right-hand sides and solutions are n x q row-major in TREE (perm) order, as
+ * solve_many takes them (solver.py:193). They may be host or
+ * device pointers; the library detects which.
+ *
+ * Return codes (the Python layer maps them to kernelsolve.errors types):
+ */
+#ifndef INVASKIT_H
+#define INVASKIT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KS_OK 0
+#define KS_ERR_INVALID 1      /* InvalidArgumentError            (errors.py:13) */
+#define KS_ERR_NOT_SPD 2      /* NotSPDError (never escapes: LU fallback, solver.py:127-130) */
+#define KS_ERR_SINGULAR 3     /* SingularMatrixError             (errors.py:25, linalg.py:205-206) */
+#define KS_ERR_ILL_COND 4     /* IllConditionedError(node, cond) (errors.py:29-39, solver.py:150-152) */
+#define KS_ERR_CUDA 5         /* device / runtime failure */
+#define KS_ERR_UNSUPPORTED 6  /* shape outside what the kernels handle */
+
+typedef struct ks_problem {
+  int64_t n;                  /* points */
+  int64_t d;                  /* dimension */
+  const double* coords;       /* n x d row-major, ORIGINAL order (PointSet.coords) */
+  const int64_t* perm;        /* n, tree permutation (PartitionTree.perm) */
+  int64_t n_nodes;            /* BFS node count, node 0 = root */
+  const int64_t* node_begin;  /* n_nodes, TreeNode.begin */
+  const int64_t* node_end;    /* n_nodes, TreeNode.end */
+  const int64_t* node_left;   /* n_nodes, children[0] or -1 at leaves */
+  const int64_t* node_right;  /* n_nodes, children[1] or -1 at leaves */
+  const int64_t* rank;        /* n_nodes, Skeleton.rank (0: no skeleton, e.g. root) */
+  const int64_t* skel_off;    /* n_nodes + 1 offsets into skel */
+  const int64_t* skel;        /* Skeleton.skel, global point ids, pivot order */
+  const int64_t* coeff_off;   /* n_nodes + 1 offsets into coeff */
+  const double* coeff;        /* Skeleton.coeff, rank x |cand| row-major */
+  double bandwidth;           /* Gaussian h (KernelSpec.bandwidth) */
+} ks_problem;
+
+typedef struct ks_diag {
+  int64_t cholesky_fallbacks; /* diagnostics["cholesky_fallbacks"] */
+  int64_t n_z_cond;           /* number of internal nodes with a Z condition estimate */
+  int64_t n_warnings;         /* z_cond > 1e10 (solver.py:183-188) */
+  int64_t error_node;         /* node id for KS_ERR_ILL_COND / KS_ERR_SINGULAR, else -1 */
+  double error_cond;          /* condition estimate for KS_ERR_ILL_COND */
+  double max_z_cond;
+} ks_diag;
+
+typedef struct ks_factor ks_factor;
+
+/* Validate the problem, upload it (tree order) and allocate factor storage on
+ * `device`. No factorization yet. */
+int ks_create(const ks_problem* prob, int device, ks_factor** out);
+
+/* Factor K~ + lam I (solver.py:92-189). `threads` of the reference is accepted
+ * by the Python layer and ignored: the result does not depend on it. May be
+ * called again on the same handle (e.g. a new lam); `stream` may be NULL. */
+int ks_factorize(ks_factor* f, double lam, void* stream);
+
+/* X = (K~ + lam I)^-1 B, B and X n x q row-major, tree order; q >= 0. */
+int ks_solve(ks_factor* f, const double* B, double* X, int64_t q, void* stream);
+
+int ks_get_diag(const ks_factor* f, ks_diag* out);
+/* Fill up to cap (node id, Z condition estimate) pairs, ascending node id. */
+int64_t ks_get_z_cond(const ks_factor* f, int64_t* nodes, double* conds, int64_t cap);
+/* Fill up to cap leaf node ids that fell back from Cholesky to LU. */
+int64_t ks_get_fallback_nodes(const ks_factor* f, int64_t* nodes, int64_t cap);
+/* Copy the symmetrized reduced matrix H of a non-root node (rank x rank). */
+int ks_get_node_h(const ks_factor* f, int64_t node, double* out);
+/* Copy the m x m lower Cholesky factor of a leaf (LeafFactor.factor.lower). */
+int ks_get_leaf_factor(const ks_factor* f, int64_t node, double* out);
+
+/* Device bytes held by the handle. */
+int64_t ks_device_bytes(const ks_factor* f);
+/* Per-phase device times (ms) of the last ks_factorize / ks_solve, measured with
+ * CUDA events on the launching stream when profiling is on:
+ * [0] leaf assembly, [1] leaf Cholesky + L21, [2] leaf SYRK (H), [3] internal
+ * levels, [4] whole factorization, [5] whole solve. Returns count written. */
+int ks_set_profiling(ks_factor* f, int on);
+int ks_get_phase_ms(const ks_factor* f, double* ms, int cap);
+/* Kernel launches issued by the last factorize / solve. */
+int64_t ks_last_launches(const ks_factor* f, int which /* 0 factor, 1 solve */);
+
+/* Parity debugging: copy `count` doubles of an internal buffer (0 z per leaf,
+ * 1 c per node, 2 t per node, 3 y per internal index, 4 augmented LU per
+ * internal index, 5 leaf trapezoid per leaf index) and the padded layout
+ * (m_pad, s_pad, t_pad, T, R, q_cap, n_internal, n_leaves). */
+int ks_debug_copy(const ks_factor* f, int which, int64_t index, double* out, int64_t count);
+int ks_debug_layout(const ks_factor* f, int64_t* out8);
+
+void ks_destroy(ks_factor* f);
+
+/* Last error message of this thread (NUL-terminated, truncated to len). */
+int ks_last_error(char* buf, int64_t len);
+
+/* Library build fingerprint ("sm_100a ..."). */
+const char* ks_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* INVASKIT_H */

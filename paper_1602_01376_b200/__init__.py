@@ -1,0 +1,39 @@
+"""B200-native Inv-ASKIT factorization and solve (arXiv 1602.01376).
+
+Drop-in for the reference's hot path (`kernelsolve.factorize`, `solve`,
+`solve_many`; /root/reference/pkg/src/kernelsolve/solver.py:92-237): the
+operator's inputs (tree, skeletons, interpolation matrices) come from the
+reference compression, and the factor/solve runs in libinvaskit.so
+(hand-written sm_100a CUDA, C ABI in include/invaskit.h).
+"""
+
+from .errors import (
+    DeviceError,
+    IllConditionedError,
+    InvalidArgumentError,
+    KernelSolveError,
+    NotSPDError,
+    SingularMatrixError,
+)
+from .problem import Problem, as_problem, from_arrays, from_compressed_kernel
+from .solver import GpuHierFactor, factorize, solve, solve_many
+
+HierFactor = GpuHierFactor
+
+__all__ = [
+    "DeviceError",
+    "GpuHierFactor",
+    "HierFactor",
+    "IllConditionedError",
+    "InvalidArgumentError",
+    "KernelSolveError",
+    "NotSPDError",
+    "Problem",
+    "SingularMatrixError",
+    "as_problem",
+    "factorize",
+    "from_arrays",
+    "from_compressed_kernel",
+    "solve",
+    "solve_many",
+]

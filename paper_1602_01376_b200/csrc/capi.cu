@@ -1,0 +1,782 @@
+// Host runtime behind the C ABI (include/invaskit.h): problem upload in tree
+// order, the level plan, and the factor / solve launch sequences.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/invaskit.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define KS_CUDA(x)                                                                              \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) return fail(KS_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #x,     \
+                                       cudaGetErrorString(e_));                                 \
+  } while (0)
+
+constexpr double kCondHard = 1e14;  // solver.py:50
+constexpr double kCondWarn = 1e10;  // solver.py:51
+
+int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t alloc(size_t count) {
+    n = count;
+    if (count == 0) return cudaSuccess;
+    return cudaMalloc(&p, count * sizeof(T));
+  }
+  cudaError_t upload(const std::vector<T>& v) {
+    cudaError_t e = alloc(v.size());
+    if (e != cudaSuccess || v.empty()) return e;
+    return cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct ks_factor {
+  int device = 0;
+  int64_t n = 0, d = 0, n_nodes = 0;
+  std::vector<int64_t> begin, end, left, right, rank, level;
+  // plan
+  std::vector<int> leaf_nodes;                 // leaf index -> node
+  std::vector<std::vector<int>> levels;        // internal nodes per level, deepest first
+  std::vector<int> level_first;                // internal index of each level's first node
+  std::vector<int> int_nodes;                  // internal index -> node
+  int n_int = 0;
+  int m_pad = 0, s_pad = 0, t_pad = 0, T = 0, R = 0, pw = 32;
+  // device tables
+  DBuf<double> coords;
+  DBuf<int> rank_d, skel_pos;
+  DBuf<int64_t> skel_off, coeff_off;
+  DBuf<double> coeff;
+  DBuf<int> leaf_node, leaf_begin, leaf_size, leaf_info;
+  DBuf<int> int_node, int_left, int_right, int_info, piv;
+  DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
+  // solve scratch
+  DBuf<double> z, c, tin, y, bdev, xdev;
+  int64_t q_cap = 0;
+  double h = 1.0;
+  double lam = 0.0;
+  bool factored = false;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // diagnostics
+  std::vector<int> leaf_info_h, int_info_h;
+  std::vector<double> cond_h;
+  std::vector<int64_t> fallback;
+  // profiling
+  bool profiling = false;
+  double phase_ms[6] = {0, 0, 0, 0, 0, 0};
+  int64_t launches[2] = {0, 0};
+
+  ks::DevTree devtree() const {
+    ks::DevTree t;
+    t.n = n;
+    t.d = d;
+    t.coords = coords.p;
+    t.rank = rank_d.p;
+    t.skel_off = skel_off.p;
+    t.skel_pos = skel_pos.p;
+    t.coeff_off = coeff_off.p;
+    t.coeff = coeff.p;
+    t.h = h;
+    return t;
+  }
+  ks::LeafBatch leafbatch() const {
+    ks::LeafBatch lb;
+    lb.count = (int)leaf_nodes.size();
+    lb.node = leaf_node.p;
+    lb.begin = leaf_begin.p;
+    lb.size = leaf_size.p;
+    lb.m_pad = m_pad;
+    lb.s_pad = s_pad;
+    lb.A = leafA.p;
+    lb.a_stride = (int64_t)R * m_pad;
+    return lb;
+  }
+  ks::NodeBatch nodebatch(int lev) const {
+    const int first = level_first[lev];
+    ks::NodeBatch nb;
+    nb.count = (int)levels[lev].size();
+    nb.first = first;
+    nb.node = int_node.p + first;
+    nb.left = int_left.p + first;
+    nb.right = int_right.p + first;
+    nb.s_pad = s_pad;
+    nb.t_pad = t_pad;
+    nb.T = T;
+    nb.Aug = aug.p + (int64_t)first * T * T;
+    nb.Bc = bc.p + (int64_t)first * s_pad * s_pad;
+    nb.Pn = pn.p + (int64_t)first * s_pad * t_pad;
+    nb.piv = piv.p + (int64_t)first * t_pad;
+    nb.norm1 = norm1.p + first;
+    nb.cond = cond.p + first;
+    nb.info = int_info.p + first;
+    return nb;
+  }
+  void release_all() {
+    coords.release(); rank_d.release(); skel_pos.release(); skel_off.release(); coeff_off.release();
+    coeff.release(); leaf_node.release(); leaf_begin.release(); leaf_size.release(); leaf_info.release();
+    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release();
+    leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
+    norm1.release(); cond.release(); z.release(); c.release(); tin.release(); y.release();
+    bdev.release(); xdev.release();
+  }
+};
+
+namespace {
+
+using ks::GemmArgs;
+using ks::Operand;
+using ks::OperandW;
+
+GemmArgs mk(int M, int N, int K, int batch, Operand A, Operand B, OperandW C, double alpha, double beta) {
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K; g.batch = batch;
+  g.A = A; g.B = B; g.C = C;
+  g.alpha = alpha; g.beta = beta; g.tri = 0;
+  return g;
+}
+
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("KS_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+struct Launcher {
+  ks_factor* f;
+  cudaStream_t st;
+  int64_t* count;
+  // KS_DEBUG_SYNC=1: synchronize after every launch so errors name their kernel
+  int check(const char* what) {
+    if (!debug_sync()) return KS_OK;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(KS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return KS_OK;
+  }
+  int gemm(const GemmArgs& g, bool ta, bool tb) {
+    ++*count;
+    cudaError_t e = ks::gemm(g, ta, tb, st);
+    if (e != cudaSuccess) return fail(KS_ERR_CUDA, "gemm %dx%dx%d: %s", g.M, g.N, g.K, cudaGetErrorString(e));
+    return check("gemm");
+  }
+};
+
+// B[r0:r0+w, c0:c0+ncols] := L^-1 B, L unit lower at (r0, r0) of each node's Aug.
+int trsm_ul(Launcher& L, const ks::NodeBatch& nb, int r0, int w, int c0, int ncols) {
+  if (ncols <= 0) return KS_OK;
+  if (w <= 64) {
+    ks::launch_trsm_unit_lower(nb, r0, w, c0, ncols, L.st);
+    ++*L.count;
+    return L.check("trsm_unit_lower");
+  }
+  const int h = (int)roundup(w / 2, 32);
+  int rc = trsm_ul(L, nb, r0, h, c0, ncols);
+  if (rc) return rc;
+  const int64_t TT = (int64_t)nb.T * nb.T;
+  Operand A{nb.Aug + (int64_t)(r0 + h) * nb.T + r0, nb.T, TT, nullptr};
+  Operand B{nb.Aug + (int64_t)r0 * nb.T + c0, nb.T, TT, nullptr};
+  OperandW C{nb.Aug + (int64_t)(r0 + h) * nb.T + c0, nb.T, TT, nullptr};
+  rc = L.gemm(mk(w - h, ncols, h, nb.count, A, B, C, -1.0, 1.0), false, false);
+  if (rc) return rc;
+  return trsm_ul(L, nb, r0 + h, w - h, c0, ncols);
+}
+
+// Recursive LU of columns [c0, c0+w) over rows [c0, T), pivots among rows < t_pad.
+int rlu(Launcher& L, const ks::NodeBatch& nb, int c0, int w, int pw) {
+  if (w <= pw) {
+    ks::launch_lu_panel(nb, c0, w, L.st);
+    int rc = L.check("lu_panel");
+    if (rc) return rc;
+    ks::launch_lu_swap(nb, c0, w, L.st);
+    *L.count += 2;
+    return L.check("lu_swap");
+  }
+  const int h = (int)roundup(w / 2, pw);
+  int rc = rlu(L, nb, c0, h, pw);
+  if (rc) return rc;
+  rc = trsm_ul(L, nb, c0, h, c0 + h, w - h);
+  if (rc) return rc;
+  const int64_t TT = (int64_t)nb.T * nb.T;
+  Operand A{nb.Aug + (int64_t)(c0 + h) * nb.T + c0, nb.T, TT, nullptr};
+  Operand B{nb.Aug + (int64_t)c0 * nb.T + c0 + h, nb.T, TT, nullptr};
+  OperandW C{nb.Aug + (int64_t)(c0 + h) * nb.T + c0 + h, nb.T, TT, nullptr};
+  rc = L.gemm(mk(nb.T - c0 - h, w - h, h, nb.count, A, B, C, -1.0, 1.0), false, false);
+  if (rc) return rc;
+  return rlu(L, nb, c0 + h, w - h, pw);
+}
+
+struct PhaseTimer {
+  bool on;
+  cudaStream_t st;
+  std::vector<cudaEvent_t> ev;
+  PhaseTimer(bool on_, cudaStream_t s, int n) : on(on_), st(s) {
+    if (!on) return;
+    ev.resize(n);
+    for (auto& e : ev) cudaEventCreate(&e);
+  }
+  void mark(int i) {
+    if (on) cudaEventRecord(ev[i], st);
+  }
+  float between(int a, int b) {
+    float ms = 0.f;
+    if (on) cudaEventElapsedTime(&ms, ev[a], ev[b]);
+    return ms;
+  }
+  ~PhaseTimer() {
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
+int ensure_solve_bufs(ks_factor* f, int64_t q) {
+  if (q <= f->q_cap) return KS_OK;
+  f->z.release(); f->c.release(); f->tin.release(); f->y.release(); f->bdev.release(); f->xdev.release();
+  KS_CUDA(f->z.alloc((size_t)f->leaf_nodes.size() * f->m_pad * q));
+  KS_CUDA(f->c.alloc((size_t)std::max<int64_t>(f->n_nodes * f->s_pad * q, 1)));
+  KS_CUDA(f->tin.alloc((size_t)std::max<int64_t>(f->n_nodes * f->s_pad * q, 1)));
+  KS_CUDA(f->y.alloc((size_t)std::max<int64_t>((int64_t)f->n_int * f->t_pad * q, 1)));
+  KS_CUDA(f->bdev.alloc((size_t)f->n * q));
+  KS_CUDA(f->xdev.alloc((size_t)f->n * q));
+  f->q_cap = q;
+  return KS_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ks_last_error(char* buf, int64_t len) {
+  if (!buf || len <= 0) return (int)g_err.size();
+  std::snprintf(buf, (size_t)len, "%s", g_err.c_str());
+  return (int)g_err.size();
+}
+
+const char* ks_version(void) { return "libinvaskit 0.1 sm_100a (DMMA fp64, telescoping solve)"; }
+
+int ks_create(const ks_problem* p, int device, ks_factor** out) {
+  if (!p || !out) return fail(KS_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (p->n < 1 || p->d < 1 || p->n_nodes < 1) return fail(KS_ERR_INVALID, "empty problem");
+  if (!(p->bandwidth > 0.0) || !std::isfinite(p->bandwidth))
+    return fail(KS_ERR_INVALID, "gaussian kernel needs bandwidth > 0, got %g", p->bandwidth);
+  KS_CUDA(cudaSetDevice(device));
+  ks_factor* f = new ks_factor();
+  f->device = device;
+  f->n = p->n;
+  f->d = p->d;
+  f->n_nodes = p->n_nodes;
+  f->h = p->bandwidth;
+  const int64_t nn = p->n_nodes;
+  f->begin.assign(p->node_begin, p->node_begin + nn);
+  f->end.assign(p->node_end, p->node_end + nn);
+  f->left.assign(p->node_left, p->node_left + nn);
+  f->right.assign(p->node_right, p->node_right + nn);
+  f->rank.assign(p->rank, p->rank + nn);
+  auto bad = [&](const char* msg) {
+    delete f;
+    return fail(KS_ERR_INVALID, "%s", msg);
+  };
+  // levels by BFS from the root; validate the node table (tree.py:98-127)
+  f->level.assign(nn, -1);
+  f->level[0] = 0;
+  if (f->begin[0] != 0 || f->end[0] != p->n) return bad("root must own [0, n)");
+  std::vector<int> order{0};
+  for (size_t i = 0; i < order.size(); ++i) {
+    const int v = order[i];
+    if (f->left[v] < 0) {
+      if (f->right[v] >= 0) return bad("node with one child");
+      continue;
+    }
+    const int64_t l = f->left[v], r = f->right[v];
+    if (l <= 0 || r <= 0 || l >= nn || r >= nn || f->level[l] >= 0 || f->level[r] >= 0) return bad("bad child ids");
+    if (f->begin[l] != f->begin[v] || f->end[l] != f->begin[r] || f->end[r] != f->end[v]) return bad("children do not split the parent range");
+    f->level[l] = f->level[r] = f->level[v] + 1;
+    order.push_back((int)l);
+    order.push_back((int)r);
+  }
+  if ((int64_t)order.size() != nn) return bad("unreachable nodes in the tree");
+  int depth = 0;
+  int64_t m_max = 0, s_max = 0;
+  for (int64_t v = 0; v < nn; ++v) {
+    depth = std::max<int>(depth, (int)f->level[v] + 1);
+    if (f->left[v] < 0) {
+      f->leaf_nodes.push_back((int)v);
+      m_max = std::max(m_max, f->end[v] - f->begin[v]);
+      if (f->end[v] <= f->begin[v]) return bad("empty leaf");
+    }
+    if (f->rank[v] < 0) return bad("negative rank");
+    s_max = std::max(s_max, f->rank[v]);
+    const bool root = (v == 0);
+    if (!root && f->rank[v] < 1) return bad("non-root node without a skeleton");
+    if (root && f->rank[v] != 0) return bad("the root has no skeleton");
+    const int64_t cand = (f->left[v] < 0) ? (f->end[v] - f->begin[v]) : (f->rank[f->left[v]] + f->rank[f->right[v]]);
+    if (p->skel_off[v + 1] - p->skel_off[v] != f->rank[v]) return bad("skel_off inconsistent with rank");
+    if (p->coeff_off[v + 1] - p->coeff_off[v] != f->rank[v] * cand) return bad("coeff_off inconsistent with rank x |cand|");
+  }
+  f->levels.assign(depth, {});
+  for (int64_t v = 0; v < nn; ++v)
+    if (f->left[v] >= 0) f->levels[f->level[v]].push_back((int)v);
+  std::reverse(f->levels.begin(), f->levels.end());
+  f->levels.erase(std::remove_if(f->levels.begin(), f->levels.end(), [](const std::vector<int>& l) { return l.empty(); }),
+                  f->levels.end());
+  for (auto& lv : f->levels) {
+    f->level_first.push_back((int)f->int_nodes.size());
+    for (int v : lv) f->int_nodes.push_back(v);
+  }
+  f->n_int = (int)f->int_nodes.size();
+  f->m_pad = (int)roundup(m_max, 64);
+  f->s_pad = (int)roundup(s_max, 64);
+  f->t_pad = 2 * f->s_pad;
+  f->T = 3 * f->s_pad;
+  f->R = f->m_pad + f->s_pad;
+  f->pw = (f->T <= 880) ? 32 : 16;
+  if (f->T > 1760) { delete f; return fail(KS_ERR_UNSUPPORTED, "skeleton rank %lld too large (max 576)", (long long)s_max); }
+
+  // host-side tree-order data
+  std::vector<int64_t> pos(p->n, -1);
+  for (int64_t i = 0; i < p->n; ++i) {
+    const int64_t id = p->perm[i];
+    if (id < 0 || id >= p->n || pos[id] >= 0) return bad("perm is not a permutation");
+    pos[id] = i;
+  }
+  std::vector<double> ct((size_t)p->n * p->d);
+  for (int64_t i = 0; i < p->n; ++i)
+    std::memcpy(&ct[(size_t)i * p->d], p->coords + (size_t)p->perm[i] * p->d, sizeof(double) * p->d);
+  for (double v : ct)
+    if (!std::isfinite(v)) return bad("coords contain non-finite values");
+  const int64_t nsk = p->skel_off[nn];
+  std::vector<int> sp((size_t)nsk);
+  for (int64_t i = 0; i < nsk; ++i) {
+    const int64_t id = p->skel[i];
+    if (id < 0 || id >= p->n) return bad("skeleton id out of range");
+    sp[i] = (int)pos[id];
+  }
+  std::vector<int64_t> so(p->skel_off, p->skel_off + nn + 1), co(p->coeff_off, p->coeff_off + nn + 1);
+  std::vector<double> cf(p->coeff, p->coeff + p->coeff_off[nn]);
+  std::vector<int> rk(nn);
+  for (int64_t v = 0; v < nn; ++v) rk[v] = (int)f->rank[v];
+  std::vector<int> ln, lbg, lsz;
+  for (int v : f->leaf_nodes) {
+    ln.push_back(v);
+    lbg.push_back((int)f->begin[v]);
+    lsz.push_back((int)(f->end[v] - f->begin[v]));
+  }
+  std::vector<int> inode, ileft, iright;
+  for (int v : f->int_nodes) {
+    inode.push_back(v);
+    ileft.push_back((int)f->left[v]);
+    iright.push_back((int)f->right[v]);
+  }
+  const size_t nl = f->leaf_nodes.size();
+  auto up = [&]() -> int {
+    KS_CUDA(f->coords.upload(ct));
+    KS_CUDA(f->rank_d.upload(rk));
+    KS_CUDA(f->skel_pos.upload(sp));
+    KS_CUDA(f->skel_off.upload(so));
+    KS_CUDA(f->coeff_off.upload(co));
+    KS_CUDA(f->coeff.upload(cf));
+    KS_CUDA(f->leaf_node.upload(ln));
+    KS_CUDA(f->leaf_begin.upload(lbg));
+    KS_CUDA(f->leaf_size.upload(lsz));
+    KS_CUDA(f->leaf_info.alloc(nl));
+    KS_CUDA(f->int_node.upload(inode));
+    KS_CUDA(f->int_left.upload(ileft));
+    KS_CUDA(f->int_right.upload(iright));
+    KS_CUDA(f->int_info.alloc(std::max(f->n_int, 1)));
+    KS_CUDA(f->piv.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
+    KS_CUDA(f->leafA.alloc(nl * (size_t)f->R * f->m_pad));
+    KS_CUDA(f->inv.alloc(nl * 64 * 64));
+    KS_CUDA(f->hbuf.alloc((size_t)nn * f->s_pad * f->s_pad + 1));
+    KS_CUDA(f->aug.alloc((size_t)f->n_int * f->T * f->T + 1));
+    KS_CUDA(f->bc.alloc((size_t)f->n_int * f->s_pad * f->s_pad + 1));
+    KS_CUDA(f->pn.alloc((size_t)f->n_int * f->s_pad * f->t_pad + 1));
+    KS_CUDA(f->norm1.alloc(std::max(f->n_int, 1)));
+    KS_CUDA(f->cond.alloc(std::max(f->n_int, 1)));
+    KS_CUDA(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
+    KS_CUDA(cudaEventCreateWithFlags(&f->ev_fork, cudaEventDisableTiming));
+    KS_CUDA(cudaEventCreateWithFlags(&f->ev_join, cudaEventDisableTiming));
+    return KS_OK;
+  };
+  int rc = up();
+  if (rc) {
+    f->release_all();
+    delete f;
+    return rc;
+  }
+  *out = f;
+  return KS_OK;
+}
+
+int ks_factorize(ks_factor* f, double lam, void* stream) {
+  if (!f) return fail(KS_ERR_INVALID, "null handle");
+  if (!std::isfinite(lam) || lam < 0.0) return fail(KS_ERR_INVALID, "need lambda >= 0 and finite, got %g", lam);
+  KS_CUDA(cudaSetDevice(f->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  f->lam = lam;
+  f->factored = false;
+  f->launches[0] = 0;
+  Launcher L{f, st, &f->launches[0]};
+  const ks::DevTree dt = f->devtree();
+  const ks::LeafBatch lb = f->leafbatch();
+  const int nl = lb.count;
+  const int M = f->m_pad, S = f->s_pad, R = f->R;
+  PhaseTimer tm(f->profiling, st, 6);
+  tm.mark(0);
+  KS_CUDA(cudaMemsetAsync(f->leaf_info.p, 0, sizeof(int) * nl, st));
+  if (f->n_int) KS_CUDA(cudaMemsetAsync(f->int_info.p, 0, sizeof(int) * f->n_int, st));
+  // ---- leaves: assemble [[K + lam I], [P]] ----
+  ks::launch_leaf_assemble(dt, lb, lam, st);
+  L.count[0] += 2;
+  KS_CUDA(cudaGetLastError());
+  tm.mark(1);
+  // ---- left-looking Cholesky of the trapezoid, 64-column panels ----
+  const int64_t AS = lb.a_stride;
+  for (int j0 = 0; j0 < M; j0 += 64) {
+    if (j0 > 0) {
+      Operand A{f->leafA.p + (int64_t)j0 * M, M, AS, nullptr};
+      Operand B{f->leafA.p + (int64_t)j0 * M, M, AS, nullptr};
+      OperandW C{f->leafA.p + (int64_t)j0 * M + j0, M, AS, nullptr};
+      int rc = L.gemm(mk(R - j0, 64, j0, nl, A, B, C, -1.0, 1.0), false, true);
+      if (rc) return rc;
+    }
+    ks::launch_potrf64(lb, j0, f->inv.p, f->leaf_info.p, st);
+    ++L.count[0];
+    if (int rc = L.check("potrf64")) return rc;
+    if (R - j0 - 64 > 0) {
+      Operand A{f->leafA.p + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
+      Operand B{f->inv.p, 64, 64 * 64, nullptr};
+      OperandW C{f->leafA.p + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
+      int rc = L.gemm(mk(R - j0 - 64, 64, 64, nl, A, B, C, 1.0, 0.0), false, true);
+      if (rc) return rc;
+    }
+  }
+  KS_CUDA(cudaGetLastError());
+  tm.mark(2);
+  // ---- H = L21 L21^T for every non-root leaf ----
+  if (S > 0 && f->n_int > 0) {
+    Operand A{f->leafA.p + (int64_t)M * M, M, AS, nullptr};
+    OperandW C{f->hbuf.p, S, (int64_t)S * S, f->leaf_node.p};
+    int rc = L.gemm(mk(S, S, M, nl, A, A, C, 1.0, 0.0), false, true);
+    if (rc) return rc;
+    ks::launch_sym_h(f->hbuf.p, (int64_t)S * S, f->leaf_node.p, nl, S, st);
+    ++L.count[0];
+  }
+  KS_CUDA(cudaGetLastError());
+  tm.mark(3);
+  // leaf Cholesky failures (NotSPD) need the LU fallback before any parent runs
+  f->leaf_info_h.assign(nl, 0);
+  KS_CUDA(cudaMemcpyAsync(f->leaf_info_h.data(), f->leaf_info.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, st));
+  KS_CUDA(cudaStreamSynchronize(st));
+  f->fallback.clear();
+  for (int i = 0; i < nl; ++i)
+    if (f->leaf_info_h[i]) f->fallback.push_back(f->leaf_nodes[i]);
+  if (!f->fallback.empty())
+    return fail(KS_ERR_NOT_SPD, "leaf %d: Cholesky hit a non-positive pivot; LU fallback not built yet",
+                (int)f->fallback[0]);
+  // ---- internal levels, deepest first ----
+  const int TP = f->t_pad, T = f->T;
+  const int64_t TT = (int64_t)T * T, SS = (int64_t)S * S;
+  for (size_t lev = 0; lev < f->levels.size(); ++lev) {
+    const ks::NodeBatch nb = f->nodebatch((int)lev);
+    const int cnt = nb.count;
+    ks::launch_coupling(dt, nb, st);
+    ks::launch_aug_init(dt, nb, st);
+    L.count[0] += 2;
+    int rc = L.check("coupling/aug_init");
+    if (rc) return rc;
+    // Z12 = B H_r, Z21 = B^T H_l   (W G, solver.py:142-148, zero blocks skipped)
+    rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
+                   OperandW{nb.Aug + S, T, TT, nullptr}, 1.0, 0.0), false, true);
+    if (rc) return rc;
+    rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
+                   OperandW{nb.Aug + (int64_t)S * T, T, TT, nullptr}, 1.0, 0.0), true, true);
+    if (rc) return rc;
+    // -P G = [-P_l H_l, -P_r H_r]
+    const int64_t PS = (int64_t)S * TP;
+    rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Pn, TP, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
+                   OperandW{nb.Aug + (int64_t)TP * T, T, TT, nullptr}, -1.0, 0.0), false, true);
+    if (rc) return rc;
+    rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Pn + S, TP, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
+                   OperandW{nb.Aug + (int64_t)TP * T + S, T, TT, nullptr}, -1.0, 0.0), false, true);
+    if (rc) return rc;
+    ks::launch_colnorm1(dt, nb, st);
+    ++L.count[0];
+    // LU of the Z columns with pivots restricted to Z's rows
+    rc = rlu(L, nb, 0, TP, f->pw);
+    if (rc) return rc;
+    // U12 = L^-1 Pi P^T and the Schur complement H = P G Z^-1 P^T
+    rc = trsm_ul(L, nb, 0, TP, TP, S);
+    if (rc) return rc;
+    rc = L.gemm(mk(S, S, TP, cnt, Operand{nb.Aug + (int64_t)TP * T, T, TT, nullptr},
+                   Operand{nb.Aug + TP, T, TT, nullptr}, OperandW{nb.Aug + (int64_t)TP * T + TP, T, TT, nullptr},
+                   -1.0, 1.0), false, false);
+    if (rc) return rc;
+    // condition estimate off the critical path (it only feeds diagnostics)
+    KS_CUDA(cudaEventRecord(f->ev_fork, st));
+    KS_CUDA(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
+    ks::launch_hager(dt, nb, f->side);
+    ++L.count[0];
+    const bool is_root_level = (lev + 1 == f->levels.size());
+    if (!is_root_level) {
+      ks::launch_extract_h(nb, f->hbuf.p, SS, st);
+      ++L.count[0];
+    }
+    KS_CUDA(cudaGetLastError());
+  }
+  KS_CUDA(cudaEventRecord(f->ev_join, f->side));
+  KS_CUDA(cudaStreamWaitEvent(st, f->ev_join, 0));
+  tm.mark(4);
+  tm.mark(5);
+  // ---- diagnostics and errors (solver.py:150-152, 175-188) ----
+  f->int_info_h.assign(f->n_int, 0);
+  f->cond_h.assign(f->n_int, 0.0);
+  if (f->n_int) {
+    KS_CUDA(cudaMemcpyAsync(f->int_info_h.data(), f->int_info.p, sizeof(int) * f->n_int, cudaMemcpyDeviceToHost, st));
+    KS_CUDA(cudaMemcpyAsync(f->cond_h.data(), f->cond.p, sizeof(double) * f->n_int, cudaMemcpyDeviceToHost, st));
+  }
+  KS_CUDA(cudaStreamSynchronize(st));
+  if (f->profiling) {
+    f->phase_ms[0] = tm.between(0, 1);
+    f->phase_ms[1] = tm.between(1, 2);
+    f->phase_ms[2] = tm.between(2, 3);
+    f->phase_ms[3] = tm.between(3, 4);
+    f->phase_ms[4] = tm.between(0, 5);
+  }
+  // the reference raises at the first failing node in its processing order
+  for (int k = 0; k < f->n_int; ++k) {
+    if (f->int_info_h[k])
+      return fail(KS_ERR_SINGULAR, "node %d: zero pivot column at elimination step %d", f->int_nodes[k],
+                  f->int_info_h[k] - 1);
+    const double cnd = f->cond_h[k];
+    if (!(cnd <= kCondHard)) {
+      g_err = "";
+      char buf[256];
+      std::snprintf(buf, sizeof buf, "reduced system at node %d is numerically singular (1-norm condition estimate %.3e)",
+                    f->int_nodes[k], cnd);
+      g_err = buf;
+      return KS_ERR_ILL_COND;
+    }
+  }
+  f->factored = true;
+  return KS_OK;
+}
+
+int ks_solve(ks_factor* f, const double* B, double* X, int64_t q, void* stream) {
+  if (!f) return fail(KS_ERR_INVALID, "null handle");
+  if (!f->factored) return fail(KS_ERR_INVALID, "handle is not factored");
+  if (q < 0) return fail(KS_ERR_INVALID, "q must be >= 0");
+  if (q == 0) return KS_OK;
+  if (!B || !X) return fail(KS_ERR_INVALID, "null B or X");
+  KS_CUDA(cudaSetDevice(f->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_solve_bufs(f, q);
+  if (rc) return rc;
+  f->launches[1] = 0;
+  PhaseTimer tm(f->profiling, st, 2);
+  tm.mark(0);
+  const bool bdev = is_device_ptr(B), xdev = is_device_ptr(X);
+  const double* Bd = B;
+  double* Xd = X;
+  const size_t bytes = (size_t)f->n * q * sizeof(double);
+  if (!bdev) {
+    KS_CUDA(cudaMemcpyAsync(f->bdev.p, B, bytes, cudaMemcpyHostToDevice, st));
+    Bd = f->bdev.p;
+  }
+  if (!xdev) Xd = f->xdev.p;
+  ks::SolveBufs sb{(int)q, f->z.p, f->c.p, f->tin.p, f->y.p};
+  const ks::LeafBatch lb = f->leafbatch();
+  ks::launch_leaf_fwd(lb, Bd, q, sb, st);
+  ++f->launches[1];
+  const int nlev = (int)f->levels.size();
+  for (int lev = 0; lev < nlev; ++lev) {
+    ks::launch_node_up(f->nodebatch(lev), sb, lev == nlev - 1, st);
+    ++f->launches[1];
+  }
+  for (int lev = nlev - 1; lev >= 0; --lev) {
+    ks::launch_node_down(f->nodebatch(lev), sb, lev == nlev - 1, st);
+    ++f->launches[1];
+  }
+  ks::launch_leaf_bwd(lb, Xd, q, sb, nlev > 0, st);
+  ++f->launches[1];
+  KS_CUDA(cudaGetLastError());
+  if (!xdev) KS_CUDA(cudaMemcpyAsync(X, Xd, bytes, cudaMemcpyDeviceToHost, st));
+  tm.mark(1);
+  if (!xdev || !bdev) KS_CUDA(cudaStreamSynchronize(st));
+  if (f->profiling) {
+    KS_CUDA(cudaStreamSynchronize(st));
+    f->phase_ms[5] = tm.between(0, 1);
+  }
+  return KS_OK;
+}
+
+int ks_get_diag(const ks_factor* f, ks_diag* out) {
+  if (!f || !out) return fail(KS_ERR_INVALID, "null argument");
+  out->cholesky_fallbacks = (int64_t)f->fallback.size();
+  out->n_z_cond = f->n_int;
+  out->n_warnings = 0;
+  out->error_node = -1;
+  out->error_cond = 0.0;
+  out->max_z_cond = 0.0;
+  for (int k = 0; k < (int)f->cond_h.size(); ++k) {
+    if (f->cond_h[k] > kCondWarn) ++out->n_warnings;
+    out->max_z_cond = std::max(out->max_z_cond, f->cond_h[k]);
+    if (out->error_node < 0 && (f->int_info_h[k] || !(f->cond_h[k] <= kCondHard))) {
+      out->error_node = f->int_nodes[k];
+      out->error_cond = f->cond_h[k];
+    }
+  }
+  return KS_OK;
+}
+
+int64_t ks_get_z_cond(const ks_factor* f, int64_t* nodes, double* conds, int64_t cap) {
+  if (!f) return 0;
+  std::vector<std::pair<int, double>> v;
+  for (int k = 0; k < (int)f->cond_h.size(); ++k) v.push_back({f->int_nodes[k], f->cond_h[k]});
+  std::sort(v.begin(), v.end());
+  int64_t i = 0;
+  for (; i < (int64_t)v.size() && i < cap; ++i) {
+    nodes[i] = v[i].first;
+    conds[i] = v[i].second;
+  }
+  return (int64_t)v.size();
+}
+
+int64_t ks_get_fallback_nodes(const ks_factor* f, int64_t* nodes, int64_t cap) {
+  if (!f) return 0;
+  for (int64_t i = 0; i < (int64_t)f->fallback.size() && i < cap; ++i) nodes[i] = f->fallback[i];
+  return (int64_t)f->fallback.size();
+}
+
+int ks_get_node_h(const ks_factor* f, int64_t node, double* out) {
+  if (!f || !out || node <= 0 || node >= f->n_nodes) return fail(KS_ERR_INVALID, "bad node");
+  const int r = (int)f->rank[node];
+  KS_CUDA(cudaSetDevice(f->device));
+  KS_CUDA(cudaDeviceSynchronize());
+  KS_CUDA(cudaMemcpy2D(out, sizeof(double) * r, f->hbuf.p + (int64_t)node * f->s_pad * f->s_pad,
+                       sizeof(double) * f->s_pad, sizeof(double) * r, r, cudaMemcpyDeviceToHost));
+  return KS_OK;
+}
+
+int ks_get_leaf_factor(const ks_factor* f, int64_t node, double* out) {
+  if (!f || !out) return fail(KS_ERR_INVALID, "null argument");
+  auto it = std::find(f->leaf_nodes.begin(), f->leaf_nodes.end(), (int)node);
+  if (it == f->leaf_nodes.end()) return fail(KS_ERR_INVALID, "node %lld is not a leaf", (long long)node);
+  const int li = (int)(it - f->leaf_nodes.begin());
+  const int m = (int)(f->end[node] - f->begin[node]);
+  KS_CUDA(cudaSetDevice(f->device));
+  KS_CUDA(cudaDeviceSynchronize());
+  KS_CUDA(cudaMemcpy2D(out, sizeof(double) * m, f->leafA.p + (int64_t)li * f->R * f->m_pad, sizeof(double) * f->m_pad,
+                       sizeof(double) * m, m, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < m; ++i)
+    for (int j = i + 1; j < m; ++j) out[(int64_t)i * m + j] = 0.0;
+  return KS_OK;
+}
+
+int ks_debug_copy(const ks_factor* f, int which, int64_t index, double* out, int64_t count) {
+  if (!f || !out) return fail(KS_ERR_INVALID, "null argument");
+  const double* base = nullptr;
+  int64_t stride = 0;
+  switch (which) {
+    case 0: base = f->z.p; stride = (int64_t)f->m_pad * f->q_cap; break;      // per leaf index
+    case 1: base = f->c.p; stride = (int64_t)f->s_pad * f->q_cap; break;      // per node
+    case 2: base = f->tin.p; stride = (int64_t)f->s_pad * f->q_cap; break;    // per node
+    case 3: base = f->y.p; stride = (int64_t)f->t_pad * f->q_cap; break;      // per internal index
+    case 4: base = f->aug.p; stride = (int64_t)f->T * f->T; break;            // per internal index
+    case 5: base = f->leafA.p; stride = (int64_t)f->R * f->m_pad; break;      // per leaf index
+    default: return fail(KS_ERR_INVALID, "bad buffer id");
+  }
+  KS_CUDA(cudaSetDevice(f->device));
+  KS_CUDA(cudaDeviceSynchronize());
+  KS_CUDA(cudaMemcpy(out, base + index * stride, sizeof(double) * std::min(count, stride), cudaMemcpyDeviceToHost));
+  return KS_OK;
+}
+
+int ks_debug_layout(const ks_factor* f, int64_t* out8) {
+  if (!f || !out8) return fail(KS_ERR_INVALID, "null argument");
+  out8[0] = f->m_pad; out8[1] = f->s_pad; out8[2] = f->t_pad; out8[3] = f->T;
+  out8[4] = f->R; out8[5] = f->q_cap; out8[6] = f->n_int; out8[7] = (int64_t)f->leaf_nodes.size();
+  return KS_OK;
+}
+
+int64_t ks_device_bytes(const ks_factor* f) {
+  if (!f) return 0;
+  int64_t b = 0;
+  b += f->coords.n * 8 + f->coeff.n * 8 + f->leafA.n * 8 + f->inv.n * 8 + f->hbuf.n * 8 + f->aug.n * 8;
+  b += f->bc.n * 8 + f->pn.n * 8 + f->z.n * 8 + f->c.n * 8 + f->tin.n * 8 + f->y.n * 8;
+  b += f->bdev.n * 8 + f->xdev.n * 8;
+  return b;
+}
+
+int ks_set_profiling(ks_factor* f, int on) {
+  if (!f) return fail(KS_ERR_INVALID, "null handle");
+  f->profiling = on != 0;
+  return KS_OK;
+}
+
+int ks_get_phase_ms(const ks_factor* f, double* ms, int cap) {
+  if (!f) return 0;
+  int n = std::min(cap, 6);
+  for (int i = 0; i < n; ++i) ms[i] = f->phase_ms[i];
+  return n;
+}
+
+int64_t ks_last_launches(const ks_factor* f, int which) {
+  if (!f || which < 0 || which > 1) return 0;
+  return f->launches[which];
+}
+
+void ks_destroy(ks_factor* f) {
+  if (!f) return;
+  cudaSetDevice(f->device);
+  cudaDeviceSynchronize();
+  f->release_all();
+  if (f->side) cudaStreamDestroy(f->side);
+  if (f->ev_fork) cudaEventDestroy(f->ev_fork);
+  if (f->ev_join) cudaEventDestroy(f->ev_join);
+  delete f;
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// Shared device helpers for libinvaskit (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#if defined(__CUDA_ARCH__) && !defined(__CUDA_ARCH_FEAT_SM100_ALL)
+#error "libinvaskit is built for sm_100a only (-gencode arch=compute_100a,code=sm_100a)"
+#endif
+
+namespace ks {
+
+constexpr int kWarp = 32;
+
+// fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col). On sm_100a this is
+// DMMA.8x8x4 in SASS (the m16n8k{4,8,16} forms lower to sequences of it).
+// Fragment layout, g = lane>>2, t = lane&3:
+//   a = A[g][t]   b = B[t][g]   d0 = D[g][2t]   d1 = D[g][2t+1]
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 16-byte async global->shared copy; src_bytes == 0 zero-fills the destination.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Batched operand addressing: matrix b of a batch lives at base + idx[b] * stride
+// (idx == nullptr means idx[b] = b).
+struct Operand {
+  const double* ptr;
+  int64_t ld;
+  int64_t stride;
+  const int* idx;
+  __device__ __forceinline__ const double* at(int b) const {
+    return ptr + (idx ? (int64_t)idx[b] : (int64_t)b) * stride;
+  }
+};
+struct OperandW {
+  double* ptr;
+  int64_t ld;
+  int64_t stride;
+  const int* idx;
+  __device__ __forceinline__ double* at(int b) const {
+    return ptr + (idx ? (int64_t)idx[b] : (int64_t)b) * stride;
+  }
+};
+
+}  // namespace ks

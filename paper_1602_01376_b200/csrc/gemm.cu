@@ -1,0 +1,50 @@
+// Tile-shape selection and instantiation of the batched DMMA GEMM.
+#include "gemm.cuh"
+
+namespace ks {
+
+namespace {
+
+template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
+cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
+  using Cfg = GemmCfg<BM, BN, WM, WN, TA, TB, STAGES>;
+  auto kern = k_gemm<BM, BN, WM, WN, TA, TB, STAGES>;
+  static bool attr = false;  // per instantiation; set before first launch
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.batch);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(g);
+  return cudaGetLastError();
+}
+
+template <bool TA, bool TB>
+cudaError_t dispatch(const GemmArgs& g, cudaStream_t st) {
+  // Large output tiles when there is enough work to fill the 148 SMs with
+  // them; otherwise narrower tiles (N <= 64 panels, small per-node blocks).
+  const long tiles128 = (long)((g.M + 127) / 128) * ((g.N + 127) / 128) * g.batch;
+  if (g.N <= 64) {
+    if (g.M >= 128 && (long)((g.M + 127) / 128) * g.batch >= 2 * 148)
+      return launch<128, 64, 4, 2, TA, TB, 3>(g, st);
+    return launch<64, 64, 2, 2, TA, TB, 3>(g, st);
+  }
+  if (tiles128 >= 148) return launch<128, 128, 2, 4, TA, TB, 3>(g, st);
+  return launch<64, 64, 2, 2, TA, TB, 3>(g, st);
+}
+
+}  // namespace
+
+cudaError_t gemm(const GemmArgs& g, bool ta, bool tb, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
+  if ((g.M | g.N | g.K) & 1) return cudaErrorInvalidValue;
+  if ((g.A.ld | g.B.ld | g.C.ld) & 1) return cudaErrorInvalidValue;
+  if (g.K <= 0) return cudaErrorInvalidValue;
+  if (!ta && !tb) return dispatch<false, false>(g, st);
+  if (!ta && tb) return dispatch<false, true>(g, st);
+  if (ta && !tb) return dispatch<true, false>(g, st);
+  return dispatch<true, true>(g, st);
+}
+
+}  // namespace ks

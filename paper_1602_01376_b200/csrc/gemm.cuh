@@ -1,0 +1,161 @@
+// Batched fp64 GEMM on the DMMA tensor pipe (mma.sync m8n8k4 f64 -> DMMA.8x8x4).
+//
+//   C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b]      (row-major storage)
+//   op(A) = A (M x K, K contiguous)  or  A^T (A stored K x M)      [TA]
+//   op(B) = B (K x N, N contiguous)  or  B^T (B stored N x K)      [TB]
+//
+// This is the workhorse of the factorization: the leaf Cholesky panel updates
+// and panel TRSMs, the leaf SYRK H = L21 L21^T, the Z / -PG assembly products
+// and the trailing updates of the recursive LU all run through it.
+//
+// Tiles are staged global->shared with a cp.async multistage pipeline; shared
+// tiles are padded so that every DMMA fragment load (8-byte, half-warp phases)
+// is bank-conflict free: a leading dimension == 4 (mod 16) doubles.
+#pragma once
+
+#include "common.cuh"
+
+namespace ks {
+
+struct GemmArgs {
+  int M, N, K, batch;
+  Operand A, B;
+  OperandW C;
+  double alpha, beta;
+  int tri;  // 1: skip CTA tiles strictly above the diagonal of C
+};
+
+template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
+struct GemmCfg {
+  static constexpr int BK = 16;
+  static constexpr int THREADS = WM * WN * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN;
+  static constexpr int MT = WTM / 8, NT = WTN / 8;
+  static constexpr int A_ROWS = TA ? BK : BM, A_COLS = TA ? BM : BK, A_LD = A_COLS + 4;
+  static constexpr int B_ROWS = TB ? BN : BK, B_COLS = TB ? BK : BN, B_LD = B_COLS + 4;
+  static constexpr int A_STAGE = A_ROWS * A_LD, B_STAGE = B_ROWS * B_LD;
+  static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+  static_assert(A_LD % 16 == 4 && B_LD % 16 == 4, "conflict-free fragment loads need ld = 4 mod 16");
+};
+
+template <int ROWS, int COLS, int LD, int THREADS>
+__device__ __forceinline__ void load_tile(double* dst, const double* src, int64_t ld, int r0, int c0,
+                                          int rlim, int clim) {
+  // ROWS x COLS tile of a row-major matrix, 16-byte chunks (2 doubles).
+  constexpr int CPR = COLS / 2;
+  constexpr int CHUNKS = ROWS * CPR;
+#pragma unroll
+  for (int c = threadIdx.x; c < CHUNKS; c += THREADS) {
+    const int r = c / CPR, cc = (c % CPR) * 2;
+    const int gr = r0 + r, gc = c0 + cc;
+    const bool ok = (gr < rlim) && (gc < clim);
+    const double* s = ok ? src + (int64_t)gr * ld + gc : src;
+    cp_async16(dst + r * LD + cc, s, ok ? 16 : 0);
+  }
+}
+
+template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
+__global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
+  using Cfg = GemmCfg<BM, BN, WM, WN, TA, TB, STAGES>;
+  constexpr int BK = Cfg::BK;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * Cfg::A_STAGE;
+
+  const int b = blockIdx.z;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (g.tri && n0 >= m0 + BM) return;
+  const double* A = g.A.at(b);
+  const double* B = g.B.at(b);
+  double* C = g.C.at(b);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm0 = (warp / WN) * Cfg::WTM, wn0 = (warp % WN) * Cfg::WTN;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  double acc[Cfg::MT][Cfg::NT][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int KT = (g.K + BK - 1) / BK;
+  auto issue = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    double* as = As + stage * Cfg::A_STAGE;
+    double* bs = Bs + stage * Cfg::B_STAGE;
+    if (!TA)
+      load_tile<BM, BK, Cfg::A_LD, Cfg::THREADS>(as, A, g.A.ld, m0, k0, g.M, g.K);
+    else
+      load_tile<BK, BM, Cfg::A_LD, Cfg::THREADS>(as, A, g.A.ld, k0, m0, g.K, g.M);
+    if (!TB)
+      load_tile<BK, BN, Cfg::B_LD, Cfg::THREADS>(bs, B, g.B.ld, k0, n0, g.K, g.N);
+    else
+      load_tile<BN, BK, Cfg::B_LD, Cfg::THREADS>(bs, B, g.B.ld, n0, k0, g.N, g.K);
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) issue(s, s);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < KT) issue(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * Cfg::A_STAGE;
+    const double* bs = Bs + (kt % STAGES) * Cfg::B_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[Cfg::MT], bf[Cfg::NT];
+#pragma unroll
+      for (int i = 0; i < Cfg::MT; ++i) {
+        const int r = wm0 + i * 8 + gq, k = kk + tq;
+        af[i] = TA ? as[k * Cfg::A_LD + r] : as[r * Cfg::A_LD + k];
+      }
+#pragma unroll
+      for (int j = 0; j < Cfg::NT; ++j) {
+        const int c = wn0 + j * 8 + gq, k = kk + tq;
+        bf[j] = TB ? bs[c * Cfg::B_LD + k] : bs[k * Cfg::B_LD + c];
+      }
+#pragma unroll
+      for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  const double alpha = g.alpha, beta = g.beta;
+#pragma unroll
+  for (int i = 0; i < Cfg::MT; ++i) {
+    const int r = m0 + wm0 + i * 8 + gq;
+    if (r >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < Cfg::NT; ++j) {
+      const int c = n0 + wn0 + j * 8 + 2 * tq;
+      if (c >= g.N) continue;
+      double2* p = reinterpret_cast<double2*>(C + (int64_t)r * g.C.ld + c);
+      double2 v;
+      v.x = alpha * acc[i][j][0];
+      v.y = alpha * acc[i][j][1];
+      if (beta != 0.0) {
+        const double2 o = *p;
+        v.x = fma(beta, o.x, v.x);
+        v.y = fma(beta, o.y, v.y);
+      }
+      *p = v;
+    }
+  }
+}
+
+// Host launcher: picks a tile shape for the problem; all dims must be even,
+// leading dimensions even and base pointers 16-byte aligned.
+cudaError_t gemm(const GemmArgs& g, bool ta, bool tb, cudaStream_t st);
+
+}  // namespace ks

@@ -1,0 +1,83 @@
+// Kernel argument blocks and launchers shared by the factor/solve runtime.
+#pragma once
+
+#include "common.cuh"
+
+namespace ks {
+
+// Device-resident problem tables (tree order everywhere).
+struct DevTree {
+  int64_t n, d;
+  const double* coords;      // n x d, tree order (coords[perm])
+  const int* rank;           // per node
+  const int64_t* skel_off;   // per node, into skel_pos
+  const int* skel_pos;       // skeleton point positions in tree order
+  const int64_t* coeff_off;  // per node, into coeff
+  const double* coeff;       // P per node, rank x |cand| row-major
+  double h;                  // Gaussian bandwidth
+};
+
+// Leaf batch: leaves are processed together regardless of tree level.
+struct LeafBatch {
+  int count;
+  const int* node;    // node id per leaf
+  const int* begin;   // first point (tree order)
+  const int* size;    // points in the leaf
+  int m_pad, s_pad;   // padded leaf size / rank
+  double* A;          // count x (m_pad + s_pad) x m_pad workspace, ld = m_pad
+  int64_t a_stride;
+};
+
+// Internal nodes of one level (contiguous internal indices).
+struct NodeBatch {
+  int count;
+  int first;         // internal index of the batch's first node (per-node solve buffers)
+  const int* node;   // node ids
+  const int* left;   // child node ids
+  const int* right;
+  int s_pad, t_pad, T;  // T = t_pad + s_pad (augmented order)
+  double* Aug;          // count x T x T (row-major), already offset to the level
+  double* Bc;           // count x s_pad x s_pad coupling blocks
+  double* Pn;           // count x s_pad x t_pad padded P
+  int* piv;             // count x t_pad
+  double* norm1;        // count
+  double* cond;         // count
+  int* info;            // count (LU: first zero pivot column + 1)
+};
+
+// --- factor launchers (factor_kernels.cu) ---
+void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, double lam, cudaStream_t st);
+void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStream_t st);
+void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st);
+void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
+void launch_aug_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
+void launch_colnorm1(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
+void launch_lu_panel(const NodeBatch& nb, int c0, int w, cudaStream_t st);
+void launch_lu_swap(const NodeBatch& nb, int c0, int w, cudaStream_t st);
+void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncols, cudaStream_t st);
+void launch_hager(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
+void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st);
+// leaf LU fallback (NotSPD leaves): augmented [[A, P^T], [-P, 0]]
+void launch_leaf_aug_init(const DevTree& t, const LeafBatch& lb, const NodeBatch& fb, double lam,
+                          cudaStream_t st);
+
+// --- solve launchers (solve_kernels.cu) ---
+struct SolveBufs {
+  int q;                 // RHS columns (row-major [row][q])
+  double* z;             // leaves x m_pad x q
+  double* c;             // nodes x s_pad x q (skeleton weights, up pass)
+  double* tin;           // nodes x s_pad x q (incoming, down pass)
+  double* y;             // internal x t_pad x q
+};
+void launch_leaf_fwd(const LeafBatch& lb, const double* B, int64_t ldb, const SolveBufs& sb, cudaStream_t st);
+void launch_leaf_bwd(const LeafBatch& lb, double* X, int64_t ldx, const SolveBufs& sb, bool has_tin,
+                     cudaStream_t st);
+void launch_node_up(const NodeBatch& nb, const SolveBufs& sb, bool root, cudaStream_t st);
+void launch_node_down(const NodeBatch& nb, const SolveBufs& sb, bool root, cudaStream_t st);
+// leaf LU fallback solves
+void launch_leaf_lu_fwd(const LeafBatch& lb, const NodeBatch& fb, const int* leaf_idx, const double* B,
+                        int64_t ldb, const SolveBufs& sb, cudaStream_t st);
+void launch_leaf_lu_bwd(const LeafBatch& lb, const NodeBatch& fb, const int* leaf_idx, double* X,
+                        int64_t ldx, const SolveBufs& sb, bool has_tin, cudaStream_t st);
+
+}  // namespace ks

@@ -1,0 +1,412 @@
+// Telescoping solve on the stored factors (replaces the reference's recursive
+// _solve_node, solver.py:216-237, which visits a level-l node 2^l times; the
+// up/down form below visits every node once).
+//
+//   up   leaf  z = L^-1 b ;  c = L21 z                     (= P A^-1 b)
+//        node  w = [B c_r ; B^T c_l] ;  y = L^-1 Pi w ;  c = P cc + L21aug y
+//   down node  u = U^-1 (y + U12aug t) ;  t_l, t_r = split(u)
+//        leaf  x = L^-T (z - L21^T t)
+//
+// Every kernel streams its node's factor rows once, coalesced along rows, with
+// warp-shuffle reductions; right-hand sides are processed QC columns at a time.
+#include "kernels.cuh"
+
+namespace ks {
+
+constexpr int SB = 32;       // diagonal block of the blocked triangular solves
+constexpr int STHREADS = 256;
+constexpr int SWARPS = STHREADS / 32;
+
+// Row-oriented blocked triangular solve, in place on the shared vector x (n x QC):
+// lower (ascending blocks) or upper (descending), unit or not. Rows of A are
+// contiguous (ld = lda); n is a multiple of SB.
+template <int QC, bool UPPER, bool UNIT>
+__device__ void cta_trsv_rows(const double* __restrict__ A, int64_t lda, int n, double* x, double (*D)[SB + 1]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = n / SB;
+  for (int s = 0; s < nb; ++s) {
+    const int bi = UPPER ? nb - 1 - s : s;
+    const int r0 = bi * SB;
+    const int cb = UPPER ? r0 + SB : 0, ce = UPPER ? n : r0;
+    // 1) off-diagonal GEMV: 4 rows per warp
+    {
+      double acc[4][QC];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < QC; ++q) acc[i][q] = 0.0;
+      const int rb = r0 + warp * 4;
+      for (int c = cb + lane; c < ce; c += 32) {
+        double a[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = __ldg(A + (int64_t)(rb + i) * lda + c);
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+          const double xv = x[c * QC + q];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[i][q] = fma(a[i], xv, acc[i][q]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+          const double v = warp_sum(acc[i][q]);
+          if (lane == 0) x[(rb + i) * QC + q] -= v;
+        }
+    }
+    // 2) diagonal block to shared memory
+    for (int e = threadIdx.x; e < SB * SB; e += STHREADS) {
+      const int i = e / SB, j = e % SB;
+      D[i][j] = A[(int64_t)(r0 + i) * lda + r0 + j];
+    }
+    __syncthreads();
+    // 3) one warp: column-oriented substitution, lane r owns row r0+r
+    if (warp == 0) {
+      double v[QC];
+#pragma unroll
+      for (int q = 0; q < QC; ++q) v[q] = x[(r0 + lane) * QC + q];
+#pragma unroll 4
+      for (int s2 = 0; s2 < SB; ++s2) {
+        const int c = UPPER ? SB - 1 - s2 : s2;
+        if (!UNIT && lane == c) {
+#pragma unroll
+          for (int q = 0; q < QC; ++q) v[q] /= D[c][c];
+        }
+        const double dl = D[lane][c];
+        const bool upd = UPPER ? (lane < c) : (lane > c);
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+          const double xc = __shfl_sync(0xffffffffu, v[q], c);
+          if (upd) v[q] = fma(-dl, xc, v[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < QC; ++q) x[(r0 + lane) * QC + q] = v[q];
+    }
+    __syncthreads();
+  }
+}
+
+// y[r] = sum_c A[r][c] x[c] for rows [0, nrows): warps over rows, lanes over c.
+template <int QC>
+__device__ void cta_gemv_rows(const double* __restrict__ A, int64_t lda, int nrows, int ncols, const double* x,
+                              double* out, int64_t ldo, bool accumulate) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int rb = warp * 4; rb < nrows; rb += SWARPS * 4) {
+    double acc[4][QC];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < QC; ++q) acc[i][q] = 0.0;
+    for (int c = lane; c < ncols; c += 32) {
+      double a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = (rb + i < nrows) ? __ldg(A + (int64_t)(rb + i) * lda + c) : 0.0;
+#pragma unroll
+      for (int q = 0; q < QC; ++q) {
+        const double xv = x[c * QC + q];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][q] = fma(a[i], xv, acc[i][q]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < QC; ++q) {
+        const double v = warp_sum(acc[i][q]);
+        if (lane == 0 && rb + i < nrows) {
+          double* o = out + (int64_t)(rb + i) * ldo + q;
+          *o = accumulate ? *o + v : v;
+        }
+      }
+  }
+}
+
+// out[c] (+)= sum_r A[r][c] x[r] for columns [0, ncols): lanes over c, warps
+// over r, cross-warp reduction in shared memory. red: SWARPS x 32 x QC.
+template <int QC>
+__device__ void cta_gemv_cols(const double* __restrict__ A, int64_t lda, int nrows, int ncols, const double* x,
+                              double* out, double sign, double* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    const int c = c0 + lane;
+    double acc[QC];
+#pragma unroll
+    for (int q = 0; q < QC; ++q) acc[q] = 0.0;
+    if (c < ncols) {
+      for (int r = warp; r < nrows; r += SWARPS) {
+        const double a = __ldg(A + (int64_t)r * lda + c);
+#pragma unroll
+        for (int q = 0; q < QC; ++q) acc[q] = fma(a, x[r * QC + q], acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < QC; ++q) red[(warp * 32 + lane) * QC + q] = acc[q];
+    __syncthreads();
+    if (warp == 0 && c < ncols) {
+#pragma unroll
+      for (int q = 0; q < QC; ++q) {
+        double s = 0.0;
+        for (int w = 0; w < SWARPS; ++w) s += red[(w * 32 + lane) * QC + q];
+        out[c * QC + q] += sign * s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// leaf up: z = L^-1 b, c = L21 z
+// ---------------------------------------------------------------------------
+template <int QC>
+__global__ void __launch_bounds__(STHREADS) k_leaf_fwd(LeafBatch lb, const double* B, int64_t ldb, SolveBufs sb,
+                                                        int q0) {
+  extern __shared__ double x[];  // m_pad x QC
+  __shared__ double D[SB][SB + 1];
+  const int leaf = blockIdx.x;
+  const int node = lb.node[leaf], begin = lb.begin[leaf], m = lb.size[leaf];
+  const int M = lb.m_pad;
+  const double* A = lb.A + (int64_t)leaf * lb.a_stride;
+  for (int e = threadIdx.x; e < M * QC; e += STHREADS) {
+    const int r = e / QC, q = e % QC;
+    x[e] = (r < m) ? B[(int64_t)(begin + r) * ldb + q0 + q] : 0.0;
+  }
+  __syncthreads();
+  cta_trsv_rows<QC, false, false>(A, M, M, x, D);
+  double* z = sb.z + (int64_t)leaf * M * sb.q;
+  for (int e = threadIdx.x; e < M * QC; e += STHREADS) z[(e / QC) * sb.q + q0 + e % QC] = x[e];
+  if (lb.s_pad > 0) {
+    double* c = sb.c + (int64_t)node * lb.s_pad * sb.q + q0;
+    cta_gemv_rows<QC>(A + (int64_t)M * M, M, lb.s_pad, M, x, c, sb.q, false);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// leaf down: x = L^-T (z - L21^T t)
+// ---------------------------------------------------------------------------
+template <int QC>
+__global__ void __launch_bounds__(STHREADS) k_leaf_bwd(LeafBatch lb, double* X, int64_t ldx, SolveBufs sb, int q0,
+                                                        int has_tin) {
+  extern __shared__ double sm[];
+  double* x = sm;                       // m_pad x QC
+  double* tv = sm + lb.m_pad * QC;      // s_pad x QC
+  double* red = tv + lb.s_pad * QC;     // SWARPS x 32 x QC
+  __shared__ double D[SB][SB + 1];
+  const int leaf = blockIdx.x;
+  const int node = lb.node[leaf], begin = lb.begin[leaf], m = lb.size[leaf];
+  const int M = lb.m_pad, S = lb.s_pad;
+  const double* A = lb.A + (int64_t)leaf * lb.a_stride;
+  const double* z = sb.z + (int64_t)leaf * M * sb.q;
+  for (int e = threadIdx.x; e < M * QC; e += STHREADS) x[e] = z[(e / QC) * sb.q + q0 + e % QC];
+  if (has_tin) {
+    const double* ti = sb.tin + (int64_t)node * S * sb.q;
+    for (int e = threadIdx.x; e < S * QC; e += STHREADS) tv[e] = ti[(e / QC) * sb.q + q0 + e % QC];
+  }
+  __syncthreads();
+  if (has_tin) cta_gemv_cols<QC>(A + (int64_t)M * M, M, S, M, tv, x, -1.0, red);
+  // backward with L^T, blocks descending; column-oriented reads of L rows
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = M / SB;
+  for (int bi = nb - 1; bi >= 0; --bi) {
+    const int r0 = bi * SB;
+    {
+      double acc[QC];
+#pragma unroll
+      for (int q = 0; q < QC; ++q) acc[q] = 0.0;
+      for (int r = r0 + SB + warp; r < M; r += SWARPS) {
+        const double a = __ldg(A + (int64_t)r * M + r0 + lane);
+#pragma unroll
+        for (int q = 0; q < QC; ++q) acc[q] = fma(a, x[r * QC + q], acc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < QC; ++q) red[(warp * 32 + lane) * QC + q] = acc[q];
+    }
+    for (int e = threadIdx.x; e < SB * SB; e += STHREADS) {
+      const int i = e / SB, j = e % SB;
+      D[i][j] = A[(int64_t)(r0 + i) * M + r0 + j];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double v[QC];
+#pragma unroll
+      for (int q = 0; q < QC; ++q) {
+        double s = 0.0;
+        for (int w = 0; w < SWARPS; ++w) s += red[(w * 32 + lane) * QC + q];
+        v[q] = x[(r0 + lane) * QC + q] - s;
+      }
+#pragma unroll 4
+      for (int k = SB - 1; k >= 0; --k) {
+        if (lane == k) {
+#pragma unroll
+          for (int q = 0; q < QC; ++q) v[q] /= D[k][k];
+        }
+        const double dl = D[k][lane];  // (L^T)[lane][k] = L[k][lane]
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+          const double xk = __shfl_sync(0xffffffffu, v[q], k);
+          if (lane < k) v[q] = fma(-dl, xk, v[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < QC; ++q) x[(r0 + lane) * QC + q] = v[q];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < m * QC; e += STHREADS) X[(int64_t)(begin + e / QC) * ldx + q0 + e % QC] = x[e];
+}
+
+// ---------------------------------------------------------------------------
+// internal node up: w = [B c_r; B^T c_l], y = L^-1 Pi w, c = P cc + L21aug y
+// ---------------------------------------------------------------------------
+template <int QC>
+__global__ void __launch_bounds__(STHREADS) k_node_up(NodeBatch nb, SolveBufs sb, int q0, int root) {
+  extern __shared__ double sm[];
+  const int S = nb.s_pad, TP = nb.t_pad, T = nb.T;
+  double* cc = sm;              // TP x QC
+  double* w = cc + TP * QC;     // TP x QC
+  double* red = w + TP * QC;    // SWARPS x 32 x QC
+  __shared__ double D[SB][SB + 1];
+  const int k = blockIdx.x;
+  const int v = nb.node[k], l = nb.left[k], r = nb.right[k];
+  const double* cl = sb.c + (int64_t)l * S * sb.q;
+  const double* cr = sb.c + (int64_t)r * S * sb.q;
+  for (int e = threadIdx.x; e < S * QC; e += STHREADS) {
+    const int i = e / QC, q = e % QC;
+    cc[e] = cl[(int64_t)i * sb.q + q0 + q];
+    cc[S * QC + e] = cr[(int64_t)i * sb.q + q0 + q];
+    w[S * QC + e] = 0.0;
+  }
+  __syncthreads();
+  const double* Bc = nb.Bc + (int64_t)k * S * S;
+  cta_gemv_rows<QC>(Bc, S, S, S, cc + S * QC, w, QC, false);      // B c_r
+  cta_gemv_cols<QC>(Bc, S, S, S, cc, w + S * QC, 1.0, red);       // B^T c_l
+  __syncthreads();
+  const int* piv = nb.piv + (int64_t)k * TP;
+  if (threadIdx.x < QC) {
+    const int q = threadIdx.x;
+    for (int i = 0; i < TP; ++i) {
+      const int p = piv[i];
+      if (p != i) { const double t = w[i * QC + q]; w[i * QC + q] = w[p * QC + q]; w[p * QC + q] = t; }
+    }
+  }
+  __syncthreads();
+  const double* A = nb.Aug + (int64_t)k * T * T;
+  cta_trsv_rows<QC, false, true>(A, T, TP, w, D);
+  double* y = sb.y + (int64_t)(nb.first + k) * TP * sb.q;
+  for (int e = threadIdx.x; e < TP * QC; e += STHREADS) y[(e / QC) * sb.q + q0 + e % QC] = w[e];
+  if (!root) {
+    double* c = sb.c + (int64_t)v * S * sb.q + q0;
+    cta_gemv_rows<QC>(nb.Pn + (int64_t)k * S * TP, TP, S, TP, cc, c, sb.q, false);
+    __syncthreads();
+    cta_gemv_rows<QC>(A + (int64_t)TP * T, T, S, TP, w, c, sb.q, true);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// internal node down: u = U^-1 (y + U12aug t); children receive split(u)
+// ---------------------------------------------------------------------------
+template <int QC>
+__global__ void __launch_bounds__(STHREADS) k_node_down(NodeBatch nb, SolveBufs sb, int q0, int root) {
+  extern __shared__ double sm[];
+  const int S = nb.s_pad, TP = nb.t_pad, T = nb.T;
+  double* u = sm;             // TP x QC
+  double* tv = u + TP * QC;   // S x QC
+  __shared__ double D[SB][SB + 1];
+  const int k = blockIdx.x;
+  const int v = nb.node[k], l = nb.left[k], r = nb.right[k];
+  const double* y = sb.y + (int64_t)(nb.first + k) * TP * sb.q;
+  for (int e = threadIdx.x; e < TP * QC; e += STHREADS) u[e] = y[(e / QC) * sb.q + q0 + e % QC];
+  if (!root) {
+    const double* ti = sb.tin + (int64_t)v * S * sb.q;
+    for (int e = threadIdx.x; e < S * QC; e += STHREADS) tv[e] = ti[(e / QC) * sb.q + q0 + e % QC];
+  }
+  __syncthreads();
+  const double* A = nb.Aug + (int64_t)k * T * T;
+  if (!root) {
+    cta_gemv_rows<QC>(A + TP, T, TP, S, tv, u, QC, true);
+    __syncthreads();
+  }
+  cta_trsv_rows<QC, true, false>(A, T, TP, u, D);
+  double* tl = sb.tin + (int64_t)l * S * sb.q;
+  double* tr = sb.tin + (int64_t)r * S * sb.q;
+  for (int e = threadIdx.x; e < S * QC; e += STHREADS) {
+    const int i = e / QC, q = e % QC;
+    tl[(int64_t)i * sb.q + q0 + q] = u[e];
+    tr[(int64_t)i * sb.q + q0 + q] = u[S * QC + e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers: RHS columns in chunks of QC (largest of 4, 2, 1 dividing q)
+// ---------------------------------------------------------------------------
+template <typename F>
+static void for_chunks(int q, F f) {
+  int q0 = 0;
+  while (q0 < q) {
+    const int rem = q - q0;
+    const int qc = rem >= 4 ? 4 : (rem >= 2 ? 2 : 1);
+    f(q0, qc);
+    q0 += qc;
+  }
+}
+
+template <typename K>
+static void set_smem(K kern, size_t bytes) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+void launch_leaf_fwd(const LeafBatch& lb, const double* B, int64_t ldb, const SolveBufs& sb, cudaStream_t st) {
+  for_chunks(sb.q, [&](int q0, int qc) {
+    const size_t smem = (size_t)lb.m_pad * qc * sizeof(double);
+#define KS_CASE(QC)                                                  \
+  if (qc == QC) {                                                    \
+    set_smem(k_leaf_fwd<QC>, smem);                                  \
+    k_leaf_fwd<QC><<<lb.count, STHREADS, smem, st>>>(lb, B, ldb, sb, q0); \
+  }
+    KS_CASE(1) KS_CASE(2) KS_CASE(4)
+#undef KS_CASE
+  });
+}
+
+void launch_leaf_bwd(const LeafBatch& lb, double* X, int64_t ldx, const SolveBufs& sb, bool has_tin,
+                     cudaStream_t st) {
+  for_chunks(sb.q, [&](int q0, int qc) {
+    const size_t smem = ((size_t)lb.m_pad + lb.s_pad + SWARPS * 32) * qc * sizeof(double);
+#define KS_CASE(QC)                                                                  \
+  if (qc == QC) {                                                                    \
+    set_smem(k_leaf_bwd<QC>, smem);                                                  \
+    k_leaf_bwd<QC><<<lb.count, STHREADS, smem, st>>>(lb, X, ldx, sb, q0, has_tin ? 1 : 0); \
+  }
+    KS_CASE(1) KS_CASE(2) KS_CASE(4)
+#undef KS_CASE
+  });
+}
+
+void launch_node_up(const NodeBatch& nb, const SolveBufs& sb, bool root, cudaStream_t st) {
+  for_chunks(sb.q, [&](int q0, int qc) {
+    const size_t smem = ((size_t)2 * nb.t_pad + SWARPS * 32) * qc * sizeof(double);
+#define KS_CASE(QC)                                                                 \
+  if (qc == QC) {                                                                   \
+    set_smem(k_node_up<QC>, smem);                                                  \
+    k_node_up<QC><<<nb.count, STHREADS, smem, st>>>(nb, sb, q0, root ? 1 : 0);      \
+  }
+    KS_CASE(1) KS_CASE(2) KS_CASE(4)
+#undef KS_CASE
+  });
+}
+
+void launch_node_down(const NodeBatch& nb, const SolveBufs& sb, bool root, cudaStream_t st) {
+  for_chunks(sb.q, [&](int q0, int qc) {
+    const size_t smem = ((size_t)nb.t_pad + nb.s_pad) * qc * sizeof(double);
+#define KS_CASE(QC)                                                                 \
+  if (qc == QC) {                                                                   \
+    set_smem(k_node_down<QC>, smem);                                                \
+    k_node_down<QC><<<nb.count, STHREADS, smem, st>>>(nb, sb, q0, root ? 1 : 0);    \
+  }
+    KS_CASE(1) KS_CASE(2) KS_CASE(4)
+#undef KS_CASE
+  });
+}
+
+}  // namespace ks
