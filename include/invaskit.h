@@ -100,6 +100,11 @@ int64_t ks_device_bytes(const ks_factor* f);
  * levels, [4] whole factorization, [5] whole solve. Returns count written. */
 int ks_set_profiling(ks_factor* f, int on);
 int ks_get_phase_ms(const ks_factor* f, double* ms, int cap);
+/* Per internal level (deepest first) main-stream time of the last factorization. */
+int ks_get_level_ms(const ks_factor* f, double* ms, int cap);
+/* With KS_TRACE=1 in the environment: per-kernel device time table of the last
+ * factorization (events after every launch on the launching stream). */
+int ks_trace_report(const ks_factor* f, char* buf, int64_t len);
 /* Kernel launches issued by the last factorize / solve. */
 int64_t ks_last_launches(const ks_factor* f, int which /* 0 factor, 1 solve */);
 
@@ -109,6 +114,11 @@ int64_t ks_last_launches(const ks_factor* f, int which /* 0 factor, 1 solve */);
  * (m_pad, s_pad, t_pad, T, R, q_cap, n_internal, n_leaves). */
 int ks_debug_copy(const ks_factor* f, int which, int64_t index, double* out, int64_t count);
 int ks_debug_layout(const ks_factor* f, int64_t* out8);
+
+/* Test hook: the library's batched DMMA GEMM on strided device batches. */
+int ks_test_gemm(int M, int N, int K, int batch, int tri, const double* A, const double* B, double* C,
+                 int64_t lda, int64_t sa, int64_t ldb, int64_t sb, int64_t ldc, int64_t sc, double alpha, double beta,
+                 int ta, int tb, void* stream);
 
 void ks_destroy(ks_factor* f);
 

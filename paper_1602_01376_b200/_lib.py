@@ -63,9 +63,13 @@ SIGNATURES = {
     "ks_device_bytes": (C.c_int64, [C.c_void_p]),
     "ks_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "ks_get_phase_ms": (C.c_int, [C.c_void_p, _f64p, C.c_int]),
+    "ks_get_level_ms": (C.c_int, [C.c_void_p, _f64p, C.c_int]),
+    "ks_trace_report": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
     "ks_last_launches": (C.c_int64, [C.c_void_p, C.c_int]),
     "ks_debug_copy": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, _f64p, C.c_int64]),
     "ks_debug_layout": (C.c_int, [C.c_void_p, _i64p]),
+    "ks_test_gemm": (C.c_int, [C.c_int] * 5 + [C.c_void_p] * 3 + [C.c_int64] * 6
+                     + [C.c_double, C.c_double, C.c_int, C.c_int, C.c_void_p]),
     "ks_destroy": (None, [C.c_void_p]),
     "ks_last_error": (C.c_int, [C.c_char_p, C.c_int64]),
     "ks_version": (C.c_char_p, []),

@@ -79,7 +79,7 @@ struct ks_factor {
   DBuf<int64_t> skel_off, coeff_off;
   DBuf<double> coeff;
   DBuf<int> leaf_node, leaf_begin, leaf_size, leaf_info;
-  DBuf<int> int_node, int_left, int_right, int_info, piv;
+  DBuf<int> int_node, int_left, int_right, int_info, piv, moves;
   DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
   // solve scratch
   DBuf<double> z, c, tin, y, bdev, xdev;
@@ -87,7 +87,14 @@ struct ks_factor {
   double h = 1.0;
   double lam = 0.0;
   bool factored = false;
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr, cap = nullptr;
+  cudaEvent_t ev_phase[5] = {};
+  std::vector<cudaEvent_t> ev_level;
+  cudaGraphExec_t graph_exec = nullptr;
+  bool graph_profiling = false;
+  int64_t graph_launches = 0;
+  int64_t n_factorizations = 0;
+  DBuf<double> lam_dev;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // diagnostics
   std::vector<int> leaf_info_h, int_info_h;
@@ -96,6 +103,15 @@ struct ks_factor {
   // profiling
   bool profiling = false;
   double phase_ms[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<double> level_ms;
+  // KS_TRACE=1: an event after every launch on the main stream; consecutive
+  // deltas are per-kernel device times (including launch gaps)
+  std::vector<cudaEvent_t> trace_ev;
+  std::vector<const char*> trace_name;
+  std::vector<int> trace_tag;
+  int cur_tag = -1;  // -1 leaves, else internal level index
+  int trace_n = 0;
+  std::string trace_report;
   int64_t launches[2] = {0, 0};
 
   ks::DevTree devtree() const {
@@ -141,12 +157,13 @@ struct ks_factor {
     nb.norm1 = norm1.p + first;
     nb.cond = cond.p + first;
     nb.info = int_info.p + first;
+    nb.moves = moves.p + (int64_t)first * (2 * 64 + 1);
     return nb;
   }
   void release_all() {
     coords.release(); rank_d.release(); skel_pos.release(); skel_off.release(); coeff_off.release();
     coeff.release(); leaf_node.release(); leaf_begin.release(); leaf_size.release(); leaf_info.release();
-    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release();
+    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
     norm1.release(); cond.release(); z.release(); c.release(); tin.release(); y.release();
     bdev.release(); xdev.release();
@@ -167,6 +184,15 @@ GemmArgs mk(int M, int N, int K, int batch, Operand A, Operand B, OperandW C, do
   return g;
 }
 
+bool trace_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("KS_TRACE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 bool debug_sync() {
   static int v = -1;
   if (v < 0) {
@@ -182,6 +208,18 @@ struct Launcher {
   int64_t* count;
   // KS_DEBUG_SYNC=1: synchronize after every launch so errors name their kernel
   int check(const char* what) {
+    if (trace_on() && f) {
+      if (f->trace_n >= (int)f->trace_ev.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        f->trace_ev.push_back(e);
+        f->trace_name.push_back(what);
+        f->trace_tag.push_back(-1);
+      }
+      f->trace_name[f->trace_n] = what;
+      f->trace_tag[f->trace_n] = f->cur_tag;
+      cudaEventRecord(f->trace_ev[f->trace_n++], st);
+    }
     if (!debug_sync()) return KS_OK;
     cudaError_t e = cudaStreamSynchronize(st);
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -199,12 +237,13 @@ struct Launcher {
 // B[r0:r0+w, c0:c0+ncols] := L^-1 B, L unit lower at (r0, r0) of each node's Aug.
 int trsm_ul(Launcher& L, const ks::NodeBatch& nb, int r0, int w, int c0, int ncols) {
   if (ncols <= 0) return KS_OK;
-  if (w <= 64) {
+  if (w == 8 || w == 16 || w == 32 || w == 64) {
     ks::launch_trsm_unit_lower(nb, r0, w, c0, ncols, L.st);
     ++*L.count;
     return L.check("trsm_unit_lower");
   }
-  const int h = (int)roundup(w / 2, 32);
+  // w is a multiple of 8; split into base sizes
+  const int h = (w > 64) ? (int)roundup(w / 2, 8) : (w > 32 ? 32 : (w > 16 ? 16 : 8));
   int rc = trsm_ul(L, nb, r0, h, c0, ncols);
   if (rc) return rc;
   const int64_t TT = (int64_t)nb.T * nb.T;
@@ -372,21 +411,20 @@ int ks_create(const ks_problem* p, int device, ks_factor** out) {
   f->t_pad = 2 * f->s_pad;
   f->T = 3 * f->s_pad;
   f->R = f->m_pad + f->s_pad;
-  f->pw = (f->T <= 880) ? 32 : 16;
-  if (f->T > 1760) { delete f; return fail(KS_ERR_UNSUPPORTED, "skeleton rank %lld too large (max 576)", (long long)s_max); }
+  // LU panel width: the panel rows live in registers (16 columns up to 1024
+  // rows, 8 columns up to 2048)
+  f->pw = (f->T <= 1024) ? 16 : 8;
+  if (f->T > 2048) { delete f; return fail(KS_ERR_UNSUPPORTED, "skeleton rank %lld too large (max 682)", (long long)s_max); }
 
-  // host-side tree-order data
+  // host-side checks and small tables (large arrays go to the device directly)
   std::vector<int64_t> pos(p->n, -1);
   for (int64_t i = 0; i < p->n; ++i) {
     const int64_t id = p->perm[i];
     if (id < 0 || id >= p->n || pos[id] >= 0) return bad("perm is not a permutation");
     pos[id] = i;
   }
-  std::vector<double> ct((size_t)p->n * p->d);
-  for (int64_t i = 0; i < p->n; ++i)
-    std::memcpy(&ct[(size_t)i * p->d], p->coords + (size_t)p->perm[i] * p->d, sizeof(double) * p->d);
-  for (double v : ct)
-    if (!std::isfinite(v)) return bad("coords contain non-finite values");
+  for (int64_t i = 0, e = p->n * p->d; i < e; ++i)
+    if (!std::isfinite(p->coords[i])) return bad("coords contain non-finite values");
   const int64_t nsk = p->skel_off[nn];
   std::vector<int> sp((size_t)nsk);
   for (int64_t i = 0; i < nsk; ++i) {
@@ -395,7 +433,6 @@ int ks_create(const ks_problem* p, int device, ks_factor** out) {
     sp[i] = (int)pos[id];
   }
   std::vector<int64_t> so(p->skel_off, p->skel_off + nn + 1), co(p->coeff_off, p->coeff_off + nn + 1);
-  std::vector<double> cf(p->coeff, p->coeff + p->coeff_off[nn]);
   std::vector<int> rk(nn);
   for (int64_t v = 0; v < nn; ++v) rk[v] = (int)f->rank[v];
   std::vector<int> ln, lbg, lsz;
@@ -412,12 +449,26 @@ int ks_create(const ks_problem* p, int device, ks_factor** out) {
   }
   const size_t nl = f->leaf_nodes.size();
   auto up = [&]() -> int {
-    KS_CUDA(f->coords.upload(ct));
+    {  // points to tree order on the device: coords_tree[i] = coords[perm[i]]
+      DBuf<double> orig;
+      DBuf<int64_t> pm;
+      KS_CUDA(orig.alloc((size_t)p->n * p->d));
+      KS_CUDA(pm.alloc((size_t)p->n));
+      KS_CUDA(f->coords.alloc((size_t)p->n * p->d));
+      KS_CUDA(cudaMemcpy(orig.p, p->coords, sizeof(double) * p->n * p->d, cudaMemcpyHostToDevice));
+      KS_CUDA(cudaMemcpy(pm.p, p->perm, sizeof(int64_t) * p->n, cudaMemcpyHostToDevice));
+      ks::launch_gather_rows(orig.p, pm.p, p->n, p->d, f->coords.p, nullptr);
+      KS_CUDA(cudaDeviceSynchronize());
+      orig.release();
+      pm.release();
+    }
     KS_CUDA(f->rank_d.upload(rk));
     KS_CUDA(f->skel_pos.upload(sp));
     KS_CUDA(f->skel_off.upload(so));
     KS_CUDA(f->coeff_off.upload(co));
-    KS_CUDA(f->coeff.upload(cf));
+    KS_CUDA(f->coeff.alloc((size_t)p->coeff_off[nn]));
+    if (p->coeff_off[nn] > 0)
+      KS_CUDA(cudaMemcpy(f->coeff.p, p->coeff, sizeof(double) * p->coeff_off[nn], cudaMemcpyHostToDevice));
     KS_CUDA(f->leaf_node.upload(ln));
     KS_CUDA(f->leaf_begin.upload(lbg));
     KS_CUDA(f->leaf_size.upload(lsz));
@@ -427,6 +478,7 @@ int ks_create(const ks_problem* p, int device, ks_factor** out) {
     KS_CUDA(f->int_right.upload(iright));
     KS_CUDA(f->int_info.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->piv.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
+    KS_CUDA(f->moves.alloc((size_t)std::max(f->n_int, 1) * (2 * 64 + 1)));
     KS_CUDA(f->leafA.alloc(nl * (size_t)f->R * f->m_pad));
     KS_CUDA(f->inv.alloc(nl * 64 * 64));
     KS_CUDA(f->hbuf.alloc((size_t)nn * f->s_pad * f->s_pad + 1));
@@ -436,6 +488,11 @@ int ks_create(const ks_problem* p, int device, ks_factor** out) {
     KS_CUDA(f->norm1.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->cond.alloc(std::max(f->n_int, 1)));
     KS_CUDA(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
+    KS_CUDA(cudaStreamCreateWithFlags(&f->cap, cudaStreamNonBlocking));
+    for (auto& e : f->ev_phase) KS_CUDA(cudaEventCreate(&e));
+    f->ev_level.resize(f->levels.size());
+    for (auto& e : f->ev_level) KS_CUDA(cudaEventCreate(&e));
+    KS_CUDA(f->lam_dev.alloc(1));
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_fork, cudaEventDisableTiming));
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_join, cudaEventDisableTiming));
     return KS_OK;
@@ -450,28 +507,30 @@ int ks_create(const ks_problem* p, int device, ks_factor** out) {
   return KS_OK;
 }
 
-int ks_factorize(ks_factor* f, double lam, void* stream) {
-  if (!f) return fail(KS_ERR_INVALID, "null handle");
-  if (!std::isfinite(lam) || lam < 0.0) return fail(KS_ERR_INVALID, "need lambda >= 0 and finite, got %g", lam);
-  KS_CUDA(cudaSetDevice(f->device));
-  cudaStream_t st = (cudaStream_t)stream;
-  f->lam = lam;
-  f->factored = false;
-  f->launches[0] = 0;
+// Enqueue the whole factorization on `st` (no host synchronization inside, so
+// the sequence can be captured into a CUDA graph). Leaf Cholesky failures are
+// recorded on the device and handled by the caller afterwards.
+static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   Launcher L{f, st, &f->launches[0]};
   const ks::DevTree dt = f->devtree();
   const ks::LeafBatch lb = f->leafbatch();
   const int nl = lb.count;
   const int M = f->m_pad, S = f->s_pad, R = f->R;
-  PhaseTimer tm(f->profiling, st, 6);
-  tm.mark(0);
+  auto mark = [&](cudaEvent_t e) -> int {
+    if (f->profiling) KS_CUDA(cudaEventRecord(e, st));
+    return KS_OK;
+  };
+  f->cur_tag = -1;
+  if (int rc = mark(f->ev_phase[0])) return rc;
   KS_CUDA(cudaMemsetAsync(f->leaf_info.p, 0, sizeof(int) * nl, st));
   if (f->n_int) KS_CUDA(cudaMemsetAsync(f->int_info.p, 0, sizeof(int) * f->n_int, st));
   // ---- leaves: assemble [[K + lam I], [P]] ----
-  ks::launch_leaf_assemble(dt, lb, lam, st);
+  if (int rc = L.check("start")) return rc;
+  ks::launch_leaf_assemble(dt, lb, f->lam_dev.p, st);
   L.count[0] += 2;
+  if (int rc = L.check("leaf_assemble")) return rc;
   KS_CUDA(cudaGetLastError());
-  tm.mark(1);
+  if (int rc = mark(f->ev_phase[1])) return rc;
   // ---- left-looking Cholesky of the trapezoid, 64-column panels ----
   const int64_t AS = lb.a_stride;
   for (int j0 = 0; j0 < M; j0 += 64) {
@@ -494,7 +553,7 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
     }
   }
   KS_CUDA(cudaGetLastError());
-  tm.mark(2);
+  if (int rc = mark(f->ev_phase[2])) return rc;
   // ---- H = L21 L21^T for every non-root leaf ----
   if (S > 0 && f->n_int > 0) {
     Operand A{f->leafA.p + (int64_t)M * M, M, AS, nullptr};
@@ -503,23 +562,15 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
     if (rc) return rc;
     ks::launch_sym_h(f->hbuf.p, (int64_t)S * S, f->leaf_node.p, nl, S, st);
     ++L.count[0];
+    if (int rc = L.check("sym_h")) return rc;
   }
   KS_CUDA(cudaGetLastError());
-  tm.mark(3);
-  // leaf Cholesky failures (NotSPD) need the LU fallback before any parent runs
-  f->leaf_info_h.assign(nl, 0);
-  KS_CUDA(cudaMemcpyAsync(f->leaf_info_h.data(), f->leaf_info.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, st));
-  KS_CUDA(cudaStreamSynchronize(st));
-  f->fallback.clear();
-  for (int i = 0; i < nl; ++i)
-    if (f->leaf_info_h[i]) f->fallback.push_back(f->leaf_nodes[i]);
-  if (!f->fallback.empty())
-    return fail(KS_ERR_NOT_SPD, "leaf %d: Cholesky hit a non-positive pivot; LU fallback not built yet",
-                (int)f->fallback[0]);
+  if (int rc = mark(f->ev_phase[3])) return rc;
   // ---- internal levels, deepest first ----
   const int TP = f->t_pad, T = f->T;
   const int64_t TT = (int64_t)T * T, SS = (int64_t)S * S;
   for (size_t lev = 0; lev < f->levels.size(); ++lev) {
+    f->cur_tag = (int)lev;
     const ks::NodeBatch nb = f->nodebatch((int)lev);
     const int cnt = nb.count;
     ks::launch_coupling(dt, nb, st);
@@ -544,6 +595,7 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
     if (rc) return rc;
     ks::launch_colnorm1(dt, nb, st);
     ++L.count[0];
+    if (int rc2 = L.check("colnorm1")) return rc2;
     // LU of the Z columns with pivots restricted to Z's rows
     rc = rlu(L, nb, 0, TP, f->pw);
     if (rc) return rc;
@@ -563,13 +615,72 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
     if (!is_root_level) {
       ks::launch_extract_h(nb, f->hbuf.p, SS, st);
       ++L.count[0];
+      if (int rc2 = L.check("extract_h")) return rc2;
     }
     KS_CUDA(cudaGetLastError());
+    if (int rc2 = mark(f->ev_level[lev])) return rc2;
   }
   KS_CUDA(cudaEventRecord(f->ev_join, f->side));
   KS_CUDA(cudaStreamWaitEvent(st, f->ev_join, 0));
-  tm.mark(4);
-  tm.mark(5);
+  if (int rc = mark(f->ev_phase[4])) return rc;
+  return KS_OK;
+}
+
+static int graph_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("KS_GRAPH");
+    v = e ? std::atoi(e) : 1;
+  }
+  return v;
+}
+
+int ks_factorize(ks_factor* f, double lam, void* stream) {
+  if (!f) return fail(KS_ERR_INVALID, "null handle");
+  if (!std::isfinite(lam) || lam < 0.0) return fail(KS_ERR_INVALID, "need lambda >= 0 and finite, got %g", lam);
+  KS_CUDA(cudaSetDevice(f->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  f->lam = lam;
+  f->factored = false;
+  f->launches[0] = 0;
+  f->trace_n = 0;
+  const int nl = (int)f->leaf_nodes.size();
+  KS_CUDA(cudaMemcpyAsync(f->lam_dev.p, &f->lam, sizeof(double), cudaMemcpyHostToDevice, st));
+  // CUDA graph of the ~1000-launch sequence: from the second factorization on
+  // (KS_GRAPH=1, default), always (2) or never (0); tracing runs eagerly.
+  const int gm = (trace_on() || debug_sync() || f->profiling) ? 0 : graph_mode();
+  const bool use_graph = gm == 2 || (gm == 1 && f->n_factorizations > 0);
+  if (use_graph) {
+    if (!f->graph_exec || f->graph_profiling != f->profiling) {
+      if (f->graph_exec) { cudaGraphExecDestroy(f->graph_exec); f->graph_exec = nullptr; }
+      cudaGraph_t g = nullptr;
+      KS_CUDA(cudaStreamBeginCapture(f->cap, cudaStreamCaptureModeThreadLocal));
+      int rc = enqueue_factorization(f, f->cap);
+      cudaError_t ce = cudaStreamEndCapture(f->cap, &g);
+      if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+      KS_CUDA(ce);
+      KS_CUDA(cudaGraphInstantiate(&f->graph_exec, g, 0));
+      cudaGraphDestroy(g);
+      f->graph_profiling = f->profiling;
+      f->graph_launches = f->launches[0];
+    }
+    KS_CUDA(cudaGraphLaunch(f->graph_exec, st));
+    f->launches[0] = f->graph_launches;
+  } else {
+    int rc = enqueue_factorization(f, st);
+    if (rc) return rc;
+  }
+  ++f->n_factorizations;
+  // leaf Cholesky failures (NotSPD) -> LU fallback for those leaves (solver.py:125-131)
+  f->leaf_info_h.assign(nl, 0);
+  KS_CUDA(cudaMemcpyAsync(f->leaf_info_h.data(), f->leaf_info.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, st));
+  KS_CUDA(cudaStreamSynchronize(st));
+  f->fallback.clear();
+  for (int i = 0; i < nl; ++i)
+    if (f->leaf_info_h[i]) f->fallback.push_back(f->leaf_nodes[i]);
+  if (!f->fallback.empty())
+    return fail(KS_ERR_NOT_SPD, "leaf %d: Cholesky hit a non-positive pivot; LU fallback not built yet",
+                (int)f->fallback[0]);
   // ---- diagnostics and errors (solver.py:150-152, 175-188) ----
   f->int_info_h.assign(f->n_int, 0);
   f->cond_h.assign(f->n_int, 0.0);
@@ -579,11 +690,46 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
   }
   KS_CUDA(cudaStreamSynchronize(st));
   if (f->profiling) {
-    f->phase_ms[0] = tm.between(0, 1);
-    f->phase_ms[1] = tm.between(1, 2);
-    f->phase_ms[2] = tm.between(2, 3);
-    f->phase_ms[3] = tm.between(3, 4);
-    f->phase_ms[4] = tm.between(0, 5);
+    auto el = [](cudaEvent_t a, cudaEvent_t b) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, a, b);
+      return (double)ms;
+    };
+    f->phase_ms[0] = el(f->ev_phase[0], f->ev_phase[1]);
+    f->phase_ms[1] = el(f->ev_phase[1], f->ev_phase[2]);
+    f->phase_ms[2] = el(f->ev_phase[2], f->ev_phase[3]);
+    f->phase_ms[3] = el(f->ev_phase[3], f->ev_phase[4]);
+    f->phase_ms[4] = el(f->ev_phase[0], f->ev_phase[4]);
+    f->level_ms.assign(f->levels.size(), 0.0);
+    for (size_t i = 0; i < f->levels.size(); ++i)
+      f->level_ms[i] = el(i == 0 ? f->ev_phase[3] : f->ev_level[i - 1], f->ev_level[i]);
+  }
+  if (trace_on() && f->trace_n > 1) {
+    std::vector<std::pair<std::string, std::pair<int, double>>> agg;
+    for (int i = 1; i < f->trace_n; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, f->trace_ev[i - 1], f->trace_ev[i]);
+      std::string nm = (f->trace_tag[i] < 0 ? std::string("leaf ") : "L" + std::to_string(f->trace_tag[i]) + " ") +
+                       f->trace_name[i];
+      bool found = false;
+      for (auto& a : agg)
+        if (a.first == nm) { a.second.first++; a.second.second += ms; found = true; }
+      if (!found) agg.push_back({nm, {1, (double)ms}});
+    }
+    std::string rep;
+    char line[160];
+    for (auto& a : agg) {
+      std::snprintf(line, sizeof line, "%-24s %5d x %10.3f ms\n", a.first.c_str(), a.second.first, a.second.second);
+      rep += line;
+    }
+    rep += "-- last 120 launches --\n";
+    for (int i = std::max(1, f->trace_n - 120); i < f->trace_n; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, f->trace_ev[i - 1], f->trace_ev[i]);
+      std::snprintf(line, sizeof line, "%-18s %8.1f us\n", f->trace_name[i], ms * 1e3);
+      rep += line;
+    }
+    f->trace_report = rep;
   }
   // the reference raises at the first failing node in its processing order
   for (int k = 0; k < f->n_int; ++k) {
@@ -763,6 +909,32 @@ int ks_get_phase_ms(const ks_factor* f, double* ms, int cap) {
   return n;
 }
 
+int ks_get_level_ms(const ks_factor* f, double* ms, int cap) {
+  if (!f) return 0;
+  const int n = std::min<int>(cap, (int)f->level_ms.size());
+  for (int i = 0; i < n; ++i) ms[i] = f->level_ms[i];
+  return n;
+}
+
+// Test hook for the batched DMMA GEMM (tools/gemm_probe.py, tests): strided
+// batches, C = alpha op(A) op(B) + beta C.
+int ks_test_gemm(int M, int N, int K, int batch, int tri, const double* A, const double* B, double* C,
+                 int64_t lda, int64_t sa, int64_t ldb, int64_t sb, int64_t ldc, int64_t sc, double alpha, double beta,
+                 int ta, int tb, void* stream) {
+  ks::GemmArgs g = mk(M, N, K, batch, Operand{A, lda, sa, nullptr}, Operand{B, ldb, sb, nullptr},
+                      OperandW{C, ldc, sc, nullptr}, alpha, beta);
+  g.tri = tri;
+  cudaError_t e = ks::gemm(g, ta != 0, tb != 0, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(KS_ERR_CUDA, "gemm: %s", cudaGetErrorString(e));
+  return KS_OK;
+}
+
+int ks_trace_report(const ks_factor* f, char* buf, int64_t len) {
+  if (!f || !buf || len <= 0) return 0;
+  std::snprintf(buf, (size_t)len, "%s", f->trace_report.c_str());
+  return (int)f->trace_report.size();
+}
+
 int64_t ks_last_launches(const ks_factor* f, int which) {
   if (!f || which < 0 || which > 1) return 0;
   return f->launches[which];
@@ -773,7 +945,14 @@ void ks_destroy(ks_factor* f) {
   cudaSetDevice(f->device);
   cudaDeviceSynchronize();
   f->release_all();
+  if (f->graph_exec) cudaGraphExecDestroy(f->graph_exec);
   if (f->side) cudaStreamDestroy(f->side);
+  if (f->cap) cudaStreamDestroy(f->cap);
+  for (auto e : f->ev_phase)
+    if (e) cudaEventDestroy(e);
+  for (auto e : f->ev_level) cudaEventDestroy(e);
+  for (auto e : f->trace_ev) cudaEventDestroy(e);
+  f->lam_dev.release();
   if (f->ev_fork) cudaEventDestroy(f->ev_fork);
   if (f->ev_join) cudaEventDestroy(f->ev_join);
   delete f;

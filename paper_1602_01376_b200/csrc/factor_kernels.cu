@@ -14,6 +14,7 @@
 #include <cfloat>
 
 #include "kernels.cuh"
+#include "trsv.cuh"
 
 namespace ks {
 
@@ -74,10 +75,24 @@ __device__ __forceinline__ void gauss_tile(const DevTree& t, const int* rows_pos
   }
 }
 
+// Points to tree order: dst[i] = src[perm[i]] (PartitionTree.perm, tree.py:231-234).
+__global__ void k_gather_rows(const double* src, const int64_t* perm, int64_t n, int64_t d, double* dst) {
+  const int64_t total = n * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / d, k = e % d;
+    dst[e] = src[perm[i] * d + k];
+  }
+}
+
+void launch_gather_rows(const double* src, const int64_t* perm, int64_t n, int64_t d, double* dst, cudaStream_t st) {
+  k_gather_rows<<<1184, 256, 0, st>>>(src, perm, n, d, dst);
+}
+
 // Leaf block K(X_leaf, X_leaf) + lam I into the lower triangle of the leaf
 // workspace (compress.py:271-272 + solver.py:124); padding rows/cols get the
 // identity so the padded Cholesky is blkdiag(L, I) exactly.
-__global__ void __launch_bounds__(256) k_leaf_gauss(DevTree t, LeafBatch lb, double lam) {
+__global__ void __launch_bounds__(256) k_leaf_gauss(DevTree t, LeafBatch lb, const double* lam_p) {
+  const double lam = *lam_p;
   const int leaf = blockIdx.y;
   // lower-triangular tile enumeration: tile (ti, tj), tj <= ti
   int ti = (int)((sqrt(8.0 * blockIdx.x + 1.0) - 1.0) * 0.5);
@@ -122,7 +137,7 @@ __global__ void k_leaf_copy_p(DevTree t, LeafBatch lb) {
   }
 }
 
-void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, double lam, cudaStream_t st) {
+void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, const double* lam, cudaStream_t st) {
   const int nt = lb.m_pad / GT;
   dim3 g1(nt * (nt + 1) / 2, lb.count);
   k_leaf_gauss<<<g1, 256, 0, st>>>(t, lb, lam);
@@ -309,135 +324,200 @@ void launch_aug_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
 }
 
 // 1-norm of Z (max column abs sum, linalg.py:176), before the LU overwrites it.
-__global__ void k_colnorm1(NodeBatch nb) {
-  const int k = blockIdx.x;
+// 32 columns per CTA, rows split over 8 warps; the max over column tiles goes
+// through an integer atomicMax on the (non-negative) double's bit pattern.
+__global__ void __launch_bounds__(256) k_colnorm1(NodeBatch nb) {
+  const int k = blockIdx.y;
   const double* A = nb.Aug + (int64_t)k * nb.T * nb.T;
-  double best = 0.0;
-  for (int j = threadIdx.x; j < nb.t_pad; j += blockDim.x) {
-    double s = 0.0;
-    for (int i = 0; i < nb.t_pad; ++i) s += fabs(A[(int64_t)i * nb.T + j]);
-    best = fmax(best, s);
-  }
-  __shared__ double red[256];
-  red[threadIdx.x] = best;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 32 + lane;
+  __shared__ double red[8][33];
+  double s = 0.0;
+  if (c < nb.t_pad)
+#pragma unroll 8
+    for (int i = warp; i < nb.t_pad; i += 8) s += fabs(A[(int64_t)i * nb.T + c]);
+  red[warp][lane] = s;
   __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
-    __syncthreads();
+  if (warp == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(nb.norm1 + k), __double_as_longlong(t));
   }
-  if (threadIdx.x == 0) nb.norm1[k] = red[0];
 }
 
 void launch_colnorm1(const DevTree&, const NodeBatch& nb, cudaStream_t st) {
-  k_colnorm1<<<nb.count, 256, 0, st>>>(nb);
+  cudaMemsetAsync(nb.norm1, 0, sizeof(double) * nb.count, st);
+  dim3 g((nb.t_pad + 31) / 32, nb.count);
+  k_colnorm1<<<g, 256, 0, st>>>(nb);
 }
 
 // --------------------------------------------------------------------------
 // LU with partial pivoting restricted to rows < t_pad (linalg.py:199-213 on
 // the Z block; the -PG rows are eliminated but never chosen as pivots).
 // Base panel: W columns [c0, c0+W), rows [c0, T), staged column-major in smem.
+// Rows are never moved inside the panel: each thread owns up to RPT physical
+// rows and tracks their LOGICAL position (the row-interchange sequence of the
+// reference, swaps[k] = p), so a column step needs two barriers: one after
+// the pivot search, one after the rank-1 update. Ties in |pivot| go to the
+// smallest logical position, as np.argmax does.
 // --------------------------------------------------------------------------
-template <int W>
+template <int W, int RPT>
 __global__ void __launch_bounds__(512) k_lu_panel(NodeBatch nb, int c0) {
-  extern __shared__ double sp[];  // W x ldp
+  constexpr int NT = 512, NW = NT / 32;
   const int k = blockIdx.x;
   const int T = nb.T;
   double* A = nb.Aug + (int64_t)k * T * T;
   const int rows = T - c0;
-  const int ldp = rows + 1;
-  const int plim = nb.t_pad - c0;  // pivot rows are local rows [kk, plim)
-  __shared__ double rv[16];
-  __shared__ int ri[16];
-  __shared__ int s_piv;
-  for (int e = threadIdx.x; e < rows * W; e += blockDim.x) {
-    const int r = e / W, j = e % W;
-    sp[j * ldp + r] = A[(int64_t)(c0 + r) * T + c0 + j];
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int kk = 0; kk < W; ++kk) {
-    double* col = sp + kk * ldp;
-    // argmax |col[r]|, r in [kk, plim), first index on ties (np.argmax)
-    double bv = -1.0;
-    int bi = 0x7fffffff;
-    for (int r = kk + threadIdx.x; r < plim; r += blockDim.x) {
-      const double a = fabs(col[r]);
-      if (a > bv) { bv = a; bi = r; }
+  const int plim = nb.t_pad - c0;  // eligible pivot rows: physical (= original) local rows < plim
+  // per-warp candidate pivot rows, double buffered by column parity
+  __shared__ __align__(16) double cand[2][NW][W];
+  __shared__ double wv[2][NW];
+  __shared__ int wp[2][NW], wr[2][NW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double a[RPT][W];
+  int pos[RPT];
+  bool done[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int r = threadIdx.x + i * NT;
+    pos[i] = r;
+    done[i] = (r >= rows);
+    const double2* src = reinterpret_cast<const double2*>(A + (int64_t)(c0 + (r < rows ? r : 0)) * T + c0);
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) {
+      const double2 v = (r < rows) ? src[j] : make_double2(0.0, 0.0);
+      a[i][2 * j] = v.x;
+      a[i][2 * j + 1] = v.y;
     }
+  }
+  int* info = nb.info + k;
+  int* piv = nb.piv + (int64_t)k * nb.t_pad + c0;
+#pragma unroll
+  for (int kk = 0; kk < W; ++kk) {
+    const int buf = kk & 1;
+    // 1) pivot search in registers, ties to the smallest logical position
+    double bv = -1.0;
+    int bp = 0x7fffffff, br = -1, bi = -1;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int r = threadIdx.x + i * NT;
+      if (r < plim && !done[i]) {
+        const double v = fabs(a[i][kk]);
+        if (v > bv || (v == bv && pos[i] < bp)) { bv = v; bp = pos[i]; br = r; bi = i; }
+      }
+    }
+    double wbv = bv;
+    int wbp = bp, wbr = br;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      const double ov = __shfl_xor_sync(0xffffffffu, wbv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, wbp, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, wbr, o);
+      if (ov > wbv || (ov == wbv && op < wbp)) { wbv = ov; wbp = op; wbr = orr; }
     }
-    if (lane == 0) { rv[warp] = bv; ri[warp] = bi; }
+    // the winning lane publishes its row for the whole CTA
+    if (wbr >= 0 && wbr == br) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+        if (i == bi) {
+#pragma unroll
+          for (int j = 0; j < W; ++j) cand[buf][warp][j] = a[i][j];
+        }
+    }
+    if (lane == 0) { wv[buf][warp] = wbv; wp[buf][warp] = wbp; wr[buf][warp] = wbr; }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = rv[0];
-      int i = ri[0];
-      for (int w = 1; w < nw; ++w)
-        if (rv[w] > b || (rv[w] == b && ri[w] < i)) { b = rv[w]; i = ri[w]; }
-      if (!(b > 0.0)) {  // exactly zero pivot column (SingularMatrixError)
-        if (nb.info[k] == 0) nb.info[k] = c0 + kk + 1;
-        i = kk;
+    int ww = 0;
+    bv = wv[buf][0]; bp = wp[buf][0]; br = wr[buf][0];
+#pragma unroll
+    for (int w = 1; w < NW; ++w)
+      if (wv[buf][w] > bv || (wv[buf][w] == bv && wp[buf][w] < bp)) { bv = wv[buf][w]; bp = wp[buf][w]; br = wr[buf][w]; ww = w; }
+    const bool singular = !(bv > 0.0);
+    if (singular) {  // exactly zero pivot column: SingularMatrixError (linalg.py:205-206)
+      if (threadIdx.x == 0 && *info == 0) *info = c0 + kk + 1;
+      br = -1;
+    }
+    if (threadIdx.x == 0) piv[kk] = c0 + (singular ? kk : bp);
+    double prow[W];
+#pragma unroll
+    for (int j = kk; j < W; ++j) prow[j] = singular ? (j == kk ? 1.0 : 0.0) : cand[buf][ww][j];
+    // 2) logical swap kk <-> bp, eliminate every other remaining row (linalg.py:209-212)
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      if (done[i]) continue;
+      const int r = threadIdx.x + i * NT;
+      if (!singular) {
+        if (r == br) { pos[i] = kk; done[i] = true; continue; }
+        if (pos[i] == kk) pos[i] = bp;
+      } else if (pos[i] == kk) {
+        done[i] = true;
+        continue;
       }
-      s_piv = i;
-      nb.piv[(int64_t)k * nb.t_pad + c0 + kk] = c0 + i;
+      const double l = a[i][kk] / prow[kk];
+      a[i][kk] = l;
+#pragma unroll
+      for (int j = kk + 1; j < W; ++j) a[i][j] = fma(-l, prow[j], a[i][j]);
     }
-    __syncthreads();
-    const int p = s_piv;
-    if (p != kk && threadIdx.x < W) {
-      double* cj = sp + threadIdx.x * ldp;
-      const double tmp = cj[kk];
-      cj[kk] = cj[p];
-      cj[p] = tmp;
-    }
-    __syncthreads();
-    const double pv = col[kk];
-    const double piv_ok = (pv != 0.0) ? pv : 1.0;
-    for (int r = kk + 1 + threadIdx.x; r < rows; r += blockDim.x) {
-      const double l = col[r] / piv_ok;
-      col[r] = l;
-#pragma unroll 4
-      for (int j = kk + 1; j < W; ++j) sp[j * ldp + r] = fma(-l, sp[j * ldp + kk], sp[j * ldp + r]);
-    }
-    __syncthreads();
   }
-  for (int e = threadIdx.x; e < rows * W; e += blockDim.x) {
-    const int r = e / W, j = e % W;
-    A[(int64_t)(c0 + r) * T + c0 + j] = sp[j * ldp + r];
+  // rows back to their logical positions; moved rows are listed for k_lu_swap
+  __shared__ int nmove;
+  if (threadIdx.x == 0) nmove = 0;
+  __syncthreads();
+  int* mv = nb.moves + (int64_t)k * (2 * 64 + 1);
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int r = threadIdx.x + i * NT;
+    if (r >= rows) continue;
+    double2* dst = reinterpret_cast<double2*>(A + (int64_t)(c0 + pos[i]) * T + c0);
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) dst[j] = make_double2(a[i][2 * j], a[i][2 * j + 1]);
+    if (pos[i] != r) {
+      const int slot = atomicAdd(&nmove, 1);
+      mv[1 + 2 * slot] = c0 + r;       // source row (before this panel)
+      mv[2 + 2 * slot] = c0 + pos[i];  // destination row
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) mv[0] = nmove;
+}
+
+template <int W>
+static void launch_panel_w(const NodeBatch& nb, int c0, cudaStream_t st) {
+  const int rows = nb.T - c0;
+  const int rpt = (rows + 511) / 512;
+  if (rpt <= 1) k_lu_panel<W, 1><<<nb.count, 512, 0, st>>>(nb, c0);
+  else if (rpt <= 2) k_lu_panel<W, 2><<<nb.count, 512, 0, st>>>(nb, c0);
+  else if constexpr (W <= 8) {  // registers: RPT x W doubles per thread
+    if (rpt <= 3) k_lu_panel<W, 3><<<nb.count, 512, 0, st>>>(nb, c0);
+    else k_lu_panel<W, 4><<<nb.count, 512, 0, st>>>(nb, c0);
   }
 }
 
 void launch_lu_panel(const NodeBatch& nb, int c0, int w, cudaStream_t st) {
-  const int rows = nb.T - c0;
-  const size_t smem = (size_t)w * (rows + 1) * sizeof(double);
-  if (w == 32) {
-    cudaFuncSetAttribute(k_lu_panel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_lu_panel<32><<<nb.count, 512, smem, st>>>(nb, c0);
-  } else {
-    cudaFuncSetAttribute(k_lu_panel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_lu_panel<16><<<nb.count, 512, smem, st>>>(nb, c0);
-  }
+  if (w == 16) launch_panel_w<16>(nb, c0, st);
+  else launch_panel_w<8>(nb, c0, st);
 }
 
-// Apply the panel's row interchanges to every column outside the panel
-// (LAPACK getrf convention: L keeps later swaps; linalg.py:209).
+// Apply the panel's row interchanges (swaps[c0..c0+w)) to every column outside
+// the panel (LAPACK getrf convention: L keeps later swaps; linalg.py:209). The
+// panel kernel lists the (at most 2w) rows its swaps moved; every column applies
+// that permutation with all loads issued before any store.
 __global__ void k_lu_swap(NodeBatch nb, int c0, int w) {
   const int k = blockIdx.y;
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int T = nb.T;
+  const int* mv = nb.moves + (int64_t)k * (2 * 64 + 1);
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= T || (col >= c0 && col < c0 + w)) return;
-  double* A = nb.Aug + (int64_t)k * T * T;
-  const int* piv = nb.piv + (int64_t)k * nb.t_pad;
-  for (int kk = 0; kk < w; ++kk) {
-    const int r1 = c0 + kk, r2 = piv[r1];
-    if (r1 != r2) {
-      const double a = A[(int64_t)r1 * T + col];
-      A[(int64_t)r1 * T + col] = A[(int64_t)r2 * T + col];
-      A[(int64_t)r2 * T + col] = a;
-    }
-  }
+  double* A = nb.Aug + (int64_t)k * T * T + col;
+  const int n = mv[0];
+  double v[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i)
+    if (i < n) v[i] = A[(int64_t)mv[1 + 2 * i] * T];
+#pragma unroll
+  for (int i = 0; i < 64; ++i)
+    if (i < n) A[(int64_t)mv[2 + 2 * i] * T] = v[i];
 }
 
 void launch_lu_swap(const NodeBatch& nb, int c0, int w, cudaStream_t st) {
@@ -466,10 +546,17 @@ __global__ void __launch_bounds__(128) k_trsm_ul(NodeBatch nb, int r0, int c0, i
   for (int i = 0; i < W; ++i) x[i] = B[(int64_t)i * T];
 #pragma unroll
   for (int i = 1; i < W; ++i) {
-    double s = x[i];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 chains: DFMA latency, not issue, bounds this loop
 #pragma unroll
-    for (int j = 0; j < i; ++j) s = fma(-L[i][j], x[j], s);
-    x[i] = s;
+    for (int j = 0; j + 3 < i; j += 4) {
+      s0 = fma(L[i][j], x[j], s0);
+      s1 = fma(L[i][j + 1], x[j + 1], s1);
+      s2 = fma(L[i][j + 2], x[j + 2], s2);
+      s3 = fma(L[i][j + 3], x[j + 3], s3);
+    }
+#pragma unroll
+    for (int j = i & ~3; j < i; ++j) s0 = fma(L[i][j], x[j], s0);
+    x[i] -= (s0 + s1) + (s2 + s3);
   }
 #pragma unroll
   for (int i = 0; i < W; ++i) B[(int64_t)i * T] = x[i];
@@ -478,119 +565,120 @@ __global__ void __launch_bounds__(128) k_trsm_ul(NodeBatch nb, int r0, int c0, i
 void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncols, cudaStream_t st) {
   if (ncols <= 0) return;
   dim3 g((ncols + 127) / 128, nb.count);
-  if (w == 16) k_trsm_ul<16><<<g, 128, 0, st>>>(nb, r0, c0, ncols);
+  if (w == 8) k_trsm_ul<8><<<g, 128, 0, st>>>(nb, r0, c0, ncols);
+  else if (w == 16) k_trsm_ul<16><<<g, 128, 0, st>>>(nb, r0, c0, ncols);
   else if (w == 32) k_trsm_ul<32><<<g, 128, 0, st>>>(nb, r0, c0, ncols);
   else k_trsm_ul<64><<<g, 128, 0, st>>>(nb, r0, c0, ncols);
 }
 
 // --------------------------------------------------------------------------
-// Hager 1-norm condition estimate of Z (linalg.py:282-304), one warp per node,
-// on the LU factors in place. Only real (unpadded) indices take part.
+// Hager 1-norm condition estimate of Z (linalg.py:282-304), one CTA per node,
+// on the LU factors in place (blocked CTA triangular solves, trsv.cuh). Only
+// real (unpadded) indices take part, in the reference's index order.
 // --------------------------------------------------------------------------
-struct ZView {
-  const double* A;
-  int T, n;
-  const int* piv;
-  __device__ double at(int i, int j) const { return A[(int64_t)i * T + j]; }
-};
-
-__device__ void warp_lu_solve(const ZView& z, double* v) {  // Z v = b (in place)
-  const int lane = threadIdx.x & 31;
-  for (int k = 0; k < z.n; ++k) {  // row swaps
-    const int p = z.piv[k];
-    if (p != k && lane == 0) { const double t = v[k]; v[k] = v[p]; v[p] = t; }
-    __syncwarp();
+__device__ __forceinline__ void block_argmax(double& bv, int& bi, double* rv, int* ri) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
   }
-  for (int i = 0; i < z.n; ++i) {  // unit lower, rows
-    double s = 0.0;
-    for (int c = lane; c < i; c += 32) s = fma(z.at(i, c), v[c], s);
-    s = warp_sum(s);
-    if (lane == 0) v[i] -= s;
-    __syncwarp();
-  }
-  for (int i = z.n - 1; i >= 0; --i) {  // upper, rows
-    double s = 0.0;
-    for (int c = i + 1 + lane; c < z.n; c += 32) s = fma(z.at(i, c), v[c], s);
-    s = warp_sum(s);
-    if (lane == 0) v[i] = (v[i] - s) / z.at(i, i);
-    __syncwarp();
-  }
+  if (lane == 0) { rv[warp] = bv; ri[warp] = bi; }
+  __syncthreads();
+  bv = rv[0];
+  bi = ri[0];
+  for (int w = 1; w < SWARPS; ++w)
+    if (rv[w] > bv || (rv[w] == bv && ri[w] < bi)) { bv = rv[w]; bi = ri[w]; }
+  __syncthreads();
 }
 
-__device__ void warp_lu_solve_t(const ZView& z, double* v) {  // Z^T v = b (in place)
-  const int lane = threadIdx.x & 31;
-  for (int k = 0; k < z.n; ++k) {  // U^T w = b: forward, right-looking on rows of U
-    if (lane == 0) v[k] /= z.at(k, k);
-    __syncwarp();
-    const double vk = v[k];
-    for (int i = k + 1 + lane; i < z.n; i += 32) v[i] = fma(-z.at(k, i), vk, v[i]);
-    __syncwarp();
-  }
-  for (int k = z.n - 1; k >= 0; --k) {  // L^T x = w: backward, unit, rows of L
-    const double vk = v[k];
-    for (int i = lane; i < k; i += 32) v[i] = fma(-z.at(k, i), vk, v[i]);
-    __syncwarp();
-  }
-  for (int k = z.n - 1; k >= 0; --k) {  // undo swaps in reverse
-    const int p = z.piv[k];
-    if (p != k && lane == 0) { const double t = v[k]; v[k] = v[p]; v[p] = t; }
-    __syncwarp();
-  }
+__device__ __forceinline__ double block_sum(double v, double* rv) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  v = warp_sum(v);
+  if (lane == 0) rv[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < SWARPS; ++w) s += rv[w];
+  __syncthreads();
+  return s;
 }
 
-__global__ void __launch_bounds__(32) k_hager(DevTree t, NodeBatch nb) {
-  extern __shared__ double hv[];  // 3 x t_pad
+__global__ void __launch_bounds__(STHREADS) k_hager(DevTree t, NodeBatch nb) {
+  extern __shared__ double hv[];  // x, y, w (t_pad each) + red (SWARPS*32) ; int perm (t_pad)
+  __shared__ double D[SB][SB + 1];
+  __shared__ double rv[SWARPS];
+  __shared__ int ri[SWARPS];
   const int k = blockIdx.x;
-  const int lane = threadIdx.x;
-  const int TP = nb.t_pad, S = nb.s_pad;
+  const int TP = nb.t_pad, S = nb.s_pad, T = nb.T;
   const int sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]];
   const int n = sl + sr;
-  ZView z{nb.Aug + (int64_t)k * nb.T * nb.T, nb.T, TP, nb.piv + (int64_t)k * TP};
+  const double* A = nb.Aug + (int64_t)k * T * T;
+  const int* piv = nb.piv + (int64_t)k * TP;
   double* x = hv;
   double* y = hv + TP;
   double* w = hv + 2 * TP;
+  double* red = hv + 3 * TP;
+  int* pm = reinterpret_cast<int*>(red + SWARPS * 32);  // (Pi v)[i] = v[pm[i]]
+  if (n == 0) {
+    if (threadIdx.x == 0) nb.cond[k] = 0.0;
+    return;
+  }
+  if (threadIdx.x == 0) {  // compose the row interchanges once (linalg.py:250-253)
+    for (int i = 0; i < TP; ++i) pm[i] = i;
+    for (int i = 0; i < TP; ++i) {
+      const int p = piv[i];
+      if (p != i) { const int tmp = pm[i]; pm[i] = pm[p]; pm[p] = tmp; }
+    }
+  }
   auto real = [&](int i) { return i < S ? (i < sl) : (i - S < sr); };
-  if (n == 0) { if (lane == 0) nb.cond[k] = 0.0; return; }
-  for (int i = lane; i < TP; i += 32) x[i] = real(i) ? 1.0 / n : 0.0;
-  __syncwarp();
+  for (int i = threadIdx.x; i < TP; i += STHREADS) x[i] = real(i) ? 1.0 / n : 0.0;
+  __syncthreads();
   double est = 0.0;
   for (int it = 0; it < 5; ++it) {
-    for (int i = lane; i < TP; i += 32) y[i] = x[i];
-    __syncwarp();
-    warp_lu_solve(z, y);
+    // y = Z^-1 x   (dense_solve: swaps, unit L, U)
+    for (int i = threadIdx.x; i < TP; i += STHREADS) y[i] = x[pm[i]];
+    __syncthreads();
+    cta_trsv_rows<1, false, true>(A, T, TP, y, D);
+    cta_trsv_rows<1, true, false>(A, T, TP, y, D);
     double s = 0.0;
-    for (int i = lane; i < TP; i += 32) s += real(i) ? fabs(y[i]) : 0.0;
-    est = warp_sum(s);
-    for (int i = lane; i < TP; i += 32) w[i] = real(i) ? (y[i] >= 0.0 ? 1.0 : -1.0) : 0.0;
-    __syncwarp();
-    warp_lu_solve_t(z, w);
-    // j = argmax |z| (first on ties, in reference index order), z.x
+    for (int i = threadIdx.x; i < TP; i += STHREADS) s += real(i) ? fabs(y[i]) : 0.0;
+    est = block_sum(s, rv);
+    // z = Z^-T sign(y)   (solve_transposed: U^T, unit L^T, undo swaps)
+    for (int i = threadIdx.x; i < TP; i += STHREADS) w[i] = real(i) ? (y[i] >= 0.0 ? 1.0 : -1.0) : 0.0;
+    __syncthreads();
+    cta_trsv_trans<1, true, false>(A, T, TP, w, D, red);
+    cta_trsv_trans<1, false, true>(A, T, TP, w, D, red);
+    for (int i = threadIdx.x; i < TP; i += STHREADS) y[pm[i]] = w[i];  // y <- z (unpermuted)
+    __syncthreads();
+    // j = argmax |z| (first in reference order on ties), z . x
     double bv = -1.0, dot = 0.0;
     int bi = 0x7fffffff;
-    for (int i = lane; i < TP; i += 32) {
+    for (int i = threadIdx.x; i < TP; i += STHREADS) {
       if (!real(i)) continue;
-      const double a = fabs(w[i]);
-      const int ri = i < S ? i : sl + (i - S);
-      if (a > bv || (a == bv && ri < bi)) { bv = a; bi = ri; }
-      dot = fma(w[i], x[i], dot);
+      const double a = fabs(y[i]);
+      const int r = i < S ? i : sl + (i - S);
+      if (a > bv || (a == bv && r < bi)) { bv = a; bi = r; }
+      dot = fma(y[i], x[i], dot);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
-    dot = warp_sum(dot);
+    block_argmax(bv, bi, rv, ri);
+    dot = block_sum(dot, rv);
     if (bv <= dot) break;
-    const int jp = bi < sl ? bi : S + (bi - sl);  // back to padded index
-    for (int i = lane; i < TP; i += 32) x[i] = (i == jp) ? 1.0 : 0.0;
-    __syncwarp();
+    const int jp = bi < sl ? bi : S + (bi - sl);
+    for (int i = threadIdx.x; i < TP; i += STHREADS) x[i] = (i == jp) ? 1.0 : 0.0;
+    __syncthreads();
   }
-  if (lane == 0) nb.cond[k] = isfinite(est) ? nb.norm1[k] * est : INFINITY;
+  if (threadIdx.x == 0) nb.cond[k] = isfinite(est) ? nb.norm1[k] * est : INFINITY;
 }
 
 void launch_hager(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
-  k_hager<<<nb.count, 32, 3 * nb.t_pad * sizeof(double), st>>>(t, nb);
+  const size_t smem = (3 * (size_t)nb.t_pad + SWARPS * 32) * sizeof(double) + nb.t_pad * sizeof(int);
+  static size_t set = 0;
+  if (smem > set) {
+    cudaFuncSetAttribute(k_hager, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = smem;
+  }
+  k_hager<<<nb.count, STHREADS, smem, st>>>(t, nb);
 }
 
 // H = sym(trailing block) -> Hbuf[node] (solver.py:163).

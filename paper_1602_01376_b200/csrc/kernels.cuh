@@ -43,10 +43,12 @@ struct NodeBatch {
   double* norm1;        // count
   double* cond;         // count
   int* info;            // count (LU: first zero pivot column + 1)
+  int* moves;           // count x (1 + 2*64): rows moved by the last LU panel
 };
 
 // --- factor launchers (factor_kernels.cu) ---
-void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, double lam, cudaStream_t st);
+void launch_gather_rows(const double* src, const int64_t* perm, int64_t n, int64_t d, double* dst, cudaStream_t st);
+void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, const double* lam, cudaStream_t st);
 void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStream_t st);
 void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st);
 void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st);

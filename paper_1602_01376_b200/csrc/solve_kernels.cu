@@ -9,152 +9,13 @@
 //
 // Every kernel streams its node's factor rows once, coalesced along rows, with
 // warp-shuffle reductions; right-hand sides are processed QC columns at a time.
+#include <utility>
+#include <vector>
+
 #include "kernels.cuh"
+#include "trsv.cuh"
 
 namespace ks {
-
-constexpr int SB = 32;       // diagonal block of the blocked triangular solves
-constexpr int STHREADS = 256;
-constexpr int SWARPS = STHREADS / 32;
-
-// Row-oriented blocked triangular solve, in place on the shared vector x (n x QC):
-// lower (ascending blocks) or upper (descending), unit or not. Rows of A are
-// contiguous (ld = lda); n is a multiple of SB.
-template <int QC, bool UPPER, bool UNIT>
-__device__ void cta_trsv_rows(const double* __restrict__ A, int64_t lda, int n, double* x, double (*D)[SB + 1]) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nb = n / SB;
-  for (int s = 0; s < nb; ++s) {
-    const int bi = UPPER ? nb - 1 - s : s;
-    const int r0 = bi * SB;
-    const int cb = UPPER ? r0 + SB : 0, ce = UPPER ? n : r0;
-    // 1) off-diagonal GEMV: 4 rows per warp
-    {
-      double acc[4][QC];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int q = 0; q < QC; ++q) acc[i][q] = 0.0;
-      const int rb = r0 + warp * 4;
-      for (int c = cb + lane; c < ce; c += 32) {
-        double a[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = __ldg(A + (int64_t)(rb + i) * lda + c);
-#pragma unroll
-        for (int q = 0; q < QC; ++q) {
-          const double xv = x[c * QC + q];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) acc[i][q] = fma(a[i], xv, acc[i][q]);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int q = 0; q < QC; ++q) {
-          const double v = warp_sum(acc[i][q]);
-          if (lane == 0) x[(rb + i) * QC + q] -= v;
-        }
-    }
-    // 2) diagonal block to shared memory
-    for (int e = threadIdx.x; e < SB * SB; e += STHREADS) {
-      const int i = e / SB, j = e % SB;
-      D[i][j] = A[(int64_t)(r0 + i) * lda + r0 + j];
-    }
-    __syncthreads();
-    // 3) one warp: column-oriented substitution, lane r owns row r0+r
-    if (warp == 0) {
-      double v[QC];
-#pragma unroll
-      for (int q = 0; q < QC; ++q) v[q] = x[(r0 + lane) * QC + q];
-#pragma unroll 4
-      for (int s2 = 0; s2 < SB; ++s2) {
-        const int c = UPPER ? SB - 1 - s2 : s2;
-        if (!UNIT && lane == c) {
-#pragma unroll
-          for (int q = 0; q < QC; ++q) v[q] /= D[c][c];
-        }
-        const double dl = D[lane][c];
-        const bool upd = UPPER ? (lane < c) : (lane > c);
-#pragma unroll
-        for (int q = 0; q < QC; ++q) {
-          const double xc = __shfl_sync(0xffffffffu, v[q], c);
-          if (upd) v[q] = fma(-dl, xc, v[q]);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < QC; ++q) x[(r0 + lane) * QC + q] = v[q];
-    }
-    __syncthreads();
-  }
-}
-
-// y[r] = sum_c A[r][c] x[c] for rows [0, nrows): warps over rows, lanes over c.
-template <int QC>
-__device__ void cta_gemv_rows(const double* __restrict__ A, int64_t lda, int nrows, int ncols, const double* x,
-                              double* out, int64_t ldo, bool accumulate) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int rb = warp * 4; rb < nrows; rb += SWARPS * 4) {
-    double acc[4][QC];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < QC; ++q) acc[i][q] = 0.0;
-    for (int c = lane; c < ncols; c += 32) {
-      double a[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = (rb + i < nrows) ? __ldg(A + (int64_t)(rb + i) * lda + c) : 0.0;
-#pragma unroll
-      for (int q = 0; q < QC; ++q) {
-        const double xv = x[c * QC + q];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i][q] = fma(a[i], xv, acc[i][q]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < QC; ++q) {
-        const double v = warp_sum(acc[i][q]);
-        if (lane == 0 && rb + i < nrows) {
-          double* o = out + (int64_t)(rb + i) * ldo + q;
-          *o = accumulate ? *o + v : v;
-        }
-      }
-  }
-}
-
-// out[c] (+)= sum_r A[r][c] x[r] for columns [0, ncols): lanes over c, warps
-// over r, cross-warp reduction in shared memory. red: SWARPS x 32 x QC.
-template <int QC>
-__device__ void cta_gemv_cols(const double* __restrict__ A, int64_t lda, int nrows, int ncols, const double* x,
-                              double* out, double sign, double* red) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int c0 = 0; c0 < ncols; c0 += 32) {
-    const int c = c0 + lane;
-    double acc[QC];
-#pragma unroll
-    for (int q = 0; q < QC; ++q) acc[q] = 0.0;
-    if (c < ncols) {
-      for (int r = warp; r < nrows; r += SWARPS) {
-        const double a = __ldg(A + (int64_t)r * lda + c);
-#pragma unroll
-        for (int q = 0; q < QC; ++q) acc[q] = fma(a, x[r * QC + q], acc[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < QC; ++q) red[(warp * 32 + lane) * QC + q] = acc[q];
-    __syncthreads();
-    if (warp == 0 && c < ncols) {
-#pragma unroll
-      for (int q = 0; q < QC; ++q) {
-        double s = 0.0;
-        for (int w = 0; w < SWARPS; ++w) s += red[(w * 32 + lane) * QC + q];
-        out[c * QC + q] += sign * s;
-      }
-    }
-    __syncthreads();
-  }
-}
 
 // ---------------------------------------------------------------------------
 // leaf up: z = L^-1 b, c = L21 z
@@ -205,54 +66,7 @@ __global__ void __launch_bounds__(STHREADS) k_leaf_bwd(LeafBatch lb, double* X, 
   }
   __syncthreads();
   if (has_tin) cta_gemv_cols<QC>(A + (int64_t)M * M, M, S, M, tv, x, -1.0, red);
-  // backward with L^T, blocks descending; column-oriented reads of L rows
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nb = M / SB;
-  for (int bi = nb - 1; bi >= 0; --bi) {
-    const int r0 = bi * SB;
-    {
-      double acc[QC];
-#pragma unroll
-      for (int q = 0; q < QC; ++q) acc[q] = 0.0;
-      for (int r = r0 + SB + warp; r < M; r += SWARPS) {
-        const double a = __ldg(A + (int64_t)r * M + r0 + lane);
-#pragma unroll
-        for (int q = 0; q < QC; ++q) acc[q] = fma(a, x[r * QC + q], acc[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < QC; ++q) red[(warp * 32 + lane) * QC + q] = acc[q];
-    }
-    for (int e = threadIdx.x; e < SB * SB; e += STHREADS) {
-      const int i = e / SB, j = e % SB;
-      D[i][j] = A[(int64_t)(r0 + i) * M + r0 + j];
-    }
-    __syncthreads();
-    if (warp == 0) {
-      double v[QC];
-#pragma unroll
-      for (int q = 0; q < QC; ++q) {
-        double s = 0.0;
-        for (int w = 0; w < SWARPS; ++w) s += red[(w * 32 + lane) * QC + q];
-        v[q] = x[(r0 + lane) * QC + q] - s;
-      }
-#pragma unroll 4
-      for (int k = SB - 1; k >= 0; --k) {
-        if (lane == k) {
-#pragma unroll
-          for (int q = 0; q < QC; ++q) v[q] /= D[k][k];
-        }
-        const double dl = D[k][lane];  // (L^T)[lane][k] = L[k][lane]
-#pragma unroll
-        for (int q = 0; q < QC; ++q) {
-          const double xk = __shfl_sync(0xffffffffu, v[q], k);
-          if (lane < k) v[q] = fma(-dl, xk, v[q]);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < QC; ++q) x[(r0 + lane) * QC + q] = v[q];
-    }
-    __syncthreads();
-  }
+  cta_trsv_trans<QC, false, false>(A, M, M, x, D, red);  // L^T x = r
   for (int e = threadIdx.x; e < m * QC; e += STHREADS) X[(int64_t)(begin + e / QC) * ldx + q0 + e % QC] = x[e];
 }
 
@@ -353,7 +167,17 @@ static void for_chunks(int q, F f) {
 
 template <typename K>
 static void set_smem(K kern, size_t bytes) {
+  // one cached ceiling per kernel instantiation (the attribute call is not free)
+  static thread_local std::vector<std::pair<const void*, size_t>> seen;
+  for (auto& e : seen)
+    if (e.first == (const void*)kern) {
+      if (bytes <= e.second) return;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      e.second = bytes;
+      return;
+    }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  seen.push_back({(const void*)kern, bytes});
 }
 
 void launch_leaf_fwd(const LeafBatch& lb, const double* B, int64_t ldb, const SolveBufs& sb, cudaStream_t st) {

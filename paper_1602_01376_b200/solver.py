@@ -139,6 +139,16 @@ class GpuHierFactor:
         n = _lib.load().ks_get_phase_ms(self.handle, ms, 6)
         return [float(ms[i]) for i in range(n)]
 
+    def level_ms(self) -> list[float]:
+        ms = (C.c_double * 64)()
+        n = _lib.load().ks_get_level_ms(self.handle, ms, 64)
+        return [float(ms[i]) for i in range(n)]
+
+    def trace_report(self) -> str:
+        buf = C.create_string_buffer(1 << 16)
+        _lib.load().ks_trace_report(self.handle, buf, len(buf))
+        return buf.value.decode()
+
     def last_launches(self, which: int) -> int:
         return int(_lib.load().ks_last_launches(self.handle, which))
 
