@@ -82,6 +82,24 @@ int ks_factorize(ks_factor* f, double lam, void* stream);
 /* X = (K~ + lam I)^-1 B, B and X n x q row-major, tree order; q >= 0. */
 int ks_solve(ks_factor* f, const double* B, double* X, int64_t q, void* stream);
 
+/* ---- subtree sharding (one process per GPU) ----
+ * ks_create_shard: the handle factors the subtree of `shard_root` (a node at
+ * level k = log2 p) with ks_factorize, and the levels above k with
+ * ks_factorize_top once the H of every level-k node has been imported with
+ * ks_node_exchange (the caller all-gathers them, e.g. NCCL). The solve runs as
+ * ks_solve_up (local rows) -> exchange c of the level-k nodes ->
+ * ks_solve_top -> ks_solve_down (local rows). B_local / X_local are device
+ * pointers to the shard's rows [begin, end) of the tree-order RHS. */
+int ks_create_shard(const ks_problem* prob, int device, int64_t shard_root, ks_factor** out);
+int ks_factorize_top(ks_factor* f, void* stream);
+int ks_solve_up(ks_factor* f, const double* B_local, int64_t q, void* stream);
+int ks_solve_top(ks_factor* f, int64_t q, void* stream);
+int ks_solve_down(ks_factor* f, double* X_local, int64_t q, void* stream);
+/* which: 0 = H (s_pad x s_pad), 1 = c (s_pad x q), 2 = t (s_pad x q); dir 0 out, 1 in. */
+int ks_node_exchange(ks_factor* f, int which, int64_t node, double* dev, int64_t q, int dir, void* stream);
+/* [shard_root, level, begin, end, s_pad, n_peers, peer node ids...]; returns length. */
+int ks_shard_info(const ks_factor* f, int64_t* out, int64_t cap);
+
 int ks_get_diag(const ks_factor* f, ks_diag* out);
 /* Fill up to cap (node id, Z condition estimate) pairs, ascending node id. */
 int64_t ks_get_z_cond(const ks_factor* f, int64_t* nodes, double* conds, int64_t cap);

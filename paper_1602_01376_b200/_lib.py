@@ -55,6 +55,13 @@ SIGNATURES = {
     "ks_create": (C.c_int, [C.POINTER(KsProblem), C.c_int, C.POINTER(C.c_void_p)]),
     "ks_factorize": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p]),
     "ks_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "ks_create_shard": (C.c_int, [C.POINTER(KsProblem), C.c_int, C.c_int64, C.POINTER(C.c_void_p)]),
+    "ks_factorize_top": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ks_solve_up": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "ks_solve_top": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
+    "ks_solve_down": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "ks_node_exchange": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
+    "ks_shard_info": (C.c_int, [C.c_void_p, _i64p, C.c_int64]),
     "ks_get_diag": (C.c_int, [C.c_void_p, C.POINTER(KsDiag)]),
     "ks_get_z_cond": (C.c_int64, [C.c_void_p, _i64p, _f64p, C.c_int64]),
     "ks_get_fallback_nodes": (C.c_int64, [C.c_void_p, _i64p, C.c_int64]),

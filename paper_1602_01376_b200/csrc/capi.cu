@@ -72,6 +72,14 @@ struct ks_factor {
   std::vector<int> level_first;                // internal index of each level's first node
   std::vector<int> int_nodes;                  // internal index -> node
   int n_int = 0;
+  // subtree sharding (multi-GPU): this handle factors the subtree of shard_root
+  // ("local" levels) and, after the level-k exchange, the levels above it ("top")
+  int64_t shard_root = 0;
+  int shard_level = 0;
+  int n_local_levels = 0;
+  int64_t loc_begin = 0, loc_end = 0;   // tree-order rows owned by the shard
+  std::vector<int64_t> peers;           // nodes at the shard level (all shards' roots)
+  bool local_factored = false;
   int m_pad = 0, s_pad = 0, t_pad = 0, T = 0, R = 0, pw = 32;
   // device tables
   DBuf<double> coords;
@@ -335,7 +343,7 @@ int ks_last_error(char* buf, int64_t len) {
 
 const char* ks_version(void) { return "libinvaskit 0.1 sm_100a (DMMA fp64, telescoping solve)"; }
 
-int ks_create(const ks_problem* p, int device, ks_factor** out) {
+static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor** out) {
   if (!p || !out) return fail(KS_ERR_INVALID, "null argument");
   *out = nullptr;
   if (p->n < 1 || p->d < 1 || p->n_nodes < 1) return fail(KS_ERR_INVALID, "empty problem");
@@ -395,12 +403,45 @@ int ks_create(const ks_problem* p, int device, ks_factor** out) {
     if (p->skel_off[v + 1] - p->skel_off[v] != f->rank[v]) return bad("skel_off inconsistent with rank");
     if (p->coeff_off[v + 1] - p->coeff_off[v] != f->rank[v] * cand) return bad("coeff_off inconsistent with rank x |cand|");
   }
-  f->levels.assign(depth, {});
+  if (shard_root < 0 || shard_root >= nn) return bad("shard root out of range");
+  f->shard_root = shard_root;
+  f->shard_level = (int)f->level[shard_root];
+  f->loc_begin = f->begin[shard_root];
+  f->loc_end = f->end[shard_root];
+  std::vector<char> in_sub(nn, 0);
+  {
+    std::vector<int64_t> st{shard_root};
+    while (!st.empty()) {
+      const int64_t v = st.back();
+      st.pop_back();
+      in_sub[v] = 1;
+      if (f->left[v] >= 0) { st.push_back(f->left[v]); st.push_back(f->right[v]); }
+    }
+  }
+  for (int64_t v = 0; v < nn; ++v) {
+    if (f->level[v] < f->shard_level && f->left[v] < 0)
+      return bad("sharding needs every node above the shard level to be internal");
+    if (f->level[v] == f->shard_level) f->peers.push_back(v);
+  }
+  f->leaf_nodes.clear();
+  m_max = 0;
   for (int64_t v = 0; v < nn; ++v)
-    if (f->left[v] >= 0) f->levels[f->level[v]].push_back((int)v);
-  std::reverse(f->levels.begin(), f->levels.end());
-  f->levels.erase(std::remove_if(f->levels.begin(), f->levels.end(), [](const std::vector<int>& l) { return l.empty(); }),
-                  f->levels.end());
+    if (in_sub[v] && f->left[v] < 0) {
+      f->leaf_nodes.push_back((int)v);
+      m_max = std::max(m_max, f->end[v] - f->begin[v]);
+    }
+  // internal levels: the shard's own (deepest first), then the top levels
+  std::vector<std::vector<int>> loc(depth), top(depth);
+  for (int64_t v = 0; v < nn; ++v) {
+    if (f->left[v] < 0) continue;
+    if (in_sub[v]) loc[f->level[v]].push_back((int)v);
+    else if (f->level[v] < f->shard_level) top[f->level[v]].push_back((int)v);
+  }
+  for (int l = depth - 1; l >= 0; --l)
+    if (!loc[l].empty()) f->levels.push_back(loc[l]);
+  f->n_local_levels = (int)f->levels.size();
+  for (int l = depth - 1; l >= 0; --l)
+    if (!top[l].empty()) f->levels.push_back(top[l]);
   for (auto& lv : f->levels) {
     f->level_first.push_back((int)f->int_nodes.size());
     for (int v : lv) f->int_nodes.push_back(v);
@@ -507,9 +548,17 @@ int ks_create(const ks_problem* p, int device, ks_factor** out) {
   return KS_OK;
 }
 
+int ks_create(const ks_problem* p, int device, ks_factor** out) { return create_impl(p, device, 0, out); }
+
+int ks_create_shard(const ks_problem* p, int device, int64_t shard_root, ks_factor** out) {
+  return create_impl(p, device, shard_root, out);
+}
+
 // Enqueue the whole factorization on `st` (no host synchronization inside, so
 // the sequence can be captured into a CUDA graph). Leaf Cholesky failures are
 // recorded on the device and handled by the caller afterwards.
+static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1);
+
 static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   Launcher L{f, st, &f->launches[0]};
   const ks::DevTree dt = f->devtree();
@@ -566,10 +615,24 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   }
   KS_CUDA(cudaGetLastError());
   if (int rc = mark(f->ev_phase[3])) return rc;
-  // ---- internal levels, deepest first ----
+  // ---- the shard's internal levels, deepest first ----
+  if (int rc = enqueue_levels(f, st, L, 0, f->n_local_levels)) return rc;
+  if (int rc = mark(f->ev_phase[4])) return rc;
+  return KS_OK;
+}
+
+// Internal levels [lev0, lev1) of the plan (deepest first), then join the
+// side stream that ran the condition estimates.
+static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1) {
+  const ks::DevTree dt = f->devtree();
+  const int S = f->s_pad;
+  auto mark = [&](cudaEvent_t e) -> int {
+    if (f->profiling) KS_CUDA(cudaEventRecord(e, st));
+    return KS_OK;
+  };
   const int TP = f->t_pad, T = f->T;
   const int64_t TT = (int64_t)T * T, SS = (int64_t)S * S;
-  for (size_t lev = 0; lev < f->levels.size(); ++lev) {
+  for (int lev = lev0; lev < lev1; ++lev) {
     f->cur_tag = (int)lev;
     const ks::NodeBatch nb = f->nodebatch((int)lev);
     const int cnt = nb.count;
@@ -611,7 +674,7 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
     KS_CUDA(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
     ks::launch_hager(dt, nb, f->side);
     ++L.count[0];
-    const bool is_root_level = (lev + 1 == f->levels.size());
+    const bool is_root_level = (f->levels[lev][0] == 0);
     if (!is_root_level) {
       ks::launch_extract_h(nb, f->hbuf.p, SS, st);
       ++L.count[0];
@@ -622,7 +685,22 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   }
   KS_CUDA(cudaEventRecord(f->ev_join, f->side));
   KS_CUDA(cudaStreamWaitEvent(st, f->ev_join, 0));
-  if (int rc = mark(f->ev_phase[4])) return rc;
+  return KS_OK;
+}
+
+// The reference raises at the first failing node in its processing order
+// (levels bottom-up, ids ascending): singular LU (linalg.py:205-206), then the
+// condition estimate above 1e14 (solver.py:150-152).
+static int check_nodes(ks_factor* f, int k0, int k1) {
+  for (int k = k0; k < k1; ++k) {
+    if (f->int_info_h[k])
+      return fail(KS_ERR_SINGULAR, "node %d: zero pivot column at elimination step %d", f->int_nodes[k],
+                  f->int_info_h[k] - 1);
+    const double cnd = f->cond_h[k];
+    if (!(cnd <= kCondHard))
+      return fail(KS_ERR_ILL_COND, "reduced system at node %d is numerically singular (1-norm condition estimate %.3e)",
+                  f->int_nodes[k], cnd);
+  }
   return KS_OK;
 }
 
@@ -700,8 +778,8 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
     f->phase_ms[2] = el(f->ev_phase[2], f->ev_phase[3]);
     f->phase_ms[3] = el(f->ev_phase[3], f->ev_phase[4]);
     f->phase_ms[4] = el(f->ev_phase[0], f->ev_phase[4]);
-    f->level_ms.assign(f->levels.size(), 0.0);
-    for (size_t i = 0; i < f->levels.size(); ++i)
+    f->level_ms.assign(f->n_local_levels, 0.0);
+    for (int i = 0; i < f->n_local_levels; ++i)
       f->level_ms[i] = el(i == 0 ? f->ev_phase[3] : f->ev_level[i - 1], f->ev_level[i]);
   }
   if (trace_on() && f->trace_n > 1) {
@@ -731,28 +809,79 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
     }
     f->trace_report = rep;
   }
-  // the reference raises at the first failing node in its processing order
-  for (int k = 0; k < f->n_int; ++k) {
-    if (f->int_info_h[k])
-      return fail(KS_ERR_SINGULAR, "node %d: zero pivot column at elimination step %d", f->int_nodes[k],
-                  f->int_info_h[k] - 1);
-    const double cnd = f->cond_h[k];
-    if (!(cnd <= kCondHard)) {
-      g_err = "";
-      char buf[256];
-      std::snprintf(buf, sizeof buf, "reduced system at node %d is numerically singular (1-norm condition estimate %.3e)",
-                    f->int_nodes[k], cnd);
-      g_err = buf;
-      return KS_ERR_ILL_COND;
-    }
+  const int k1 = f->n_local_levels < (int)f->levels.size() ? f->level_first[f->n_local_levels] : f->n_int;
+  if (int rc = check_nodes(f, 0, k1)) return rc;
+  f->local_factored = true;
+  f->factored = (f->n_local_levels == (int)f->levels.size());
+  return KS_OK;
+}
+
+int ks_factorize_top(ks_factor* f, void* stream) {
+  if (!f) return fail(KS_ERR_INVALID, "null handle");
+  if (!f->local_factored) return fail(KS_ERR_INVALID, "factor the shard (ks_factorize) first");
+  KS_CUDA(cudaSetDevice(f->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Launcher L{f, st, &f->launches[0]};
+  if (int rc = enqueue_levels(f, st, L, f->n_local_levels, (int)f->levels.size())) return rc;
+  const int k0 = f->n_local_levels < (int)f->levels.size() ? f->level_first[f->n_local_levels] : f->n_int;
+  if (f->n_int > k0) {
+    KS_CUDA(cudaMemcpyAsync(f->int_info_h.data() + k0, f->int_info.p + k0, sizeof(int) * (f->n_int - k0),
+                            cudaMemcpyDeviceToHost, st));
+    KS_CUDA(cudaMemcpyAsync(f->cond_h.data() + k0, f->cond.p + k0, sizeof(double) * (f->n_int - k0),
+                            cudaMemcpyDeviceToHost, st));
   }
+  KS_CUDA(cudaStreamSynchronize(st));
+  if (int rc = check_nodes(f, k0, f->n_int)) return rc;
   f->factored = true;
+  return KS_OK;
+}
+
+// Solve phases. Shard-local rows are [loc_begin, loc_end) of tree order; the
+// kernels index B and X by absolute tree position, so local buffers are passed
+// with a virtual base (ptr - loc_begin * q).
+static int solve_up(ks_factor* f, const double* Bd, int64_t q, cudaStream_t st) {
+  ks::SolveBufs sb{(int)q, f->z.p, f->c.p, f->tin.p, f->y.p};
+  ks::launch_leaf_fwd(f->leafbatch(), Bd, q, sb, st);
+  ++f->launches[1];
+  for (int lev = 0; lev < f->n_local_levels; ++lev) {
+    ks::launch_node_up(f->nodebatch(lev), sb, f->levels[lev][0] == 0, st);
+    ++f->launches[1];
+  }
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+static int solve_top(ks_factor* f, int64_t q, cudaStream_t st) {
+  ks::SolveBufs sb{(int)q, f->z.p, f->c.p, f->tin.p, f->y.p};
+  const int nlev = (int)f->levels.size();
+  for (int lev = f->n_local_levels; lev < nlev; ++lev) {
+    ks::launch_node_up(f->nodebatch(lev), sb, f->levels[lev][0] == 0, st);
+    ++f->launches[1];
+  }
+  for (int lev = nlev - 1; lev >= f->n_local_levels; --lev) {
+    ks::launch_node_down(f->nodebatch(lev), sb, f->levels[lev][0] == 0, st);
+    ++f->launches[1];
+  }
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+static int solve_down(ks_factor* f, double* Xd, int64_t q, cudaStream_t st) {
+  ks::SolveBufs sb{(int)q, f->z.p, f->c.p, f->tin.p, f->y.p};
+  for (int lev = f->n_local_levels - 1; lev >= 0; --lev) {
+    ks::launch_node_down(f->nodebatch(lev), sb, f->levels[lev][0] == 0, st);
+    ++f->launches[1];
+  }
+  ks::launch_leaf_bwd(f->leafbatch(), Xd, q, sb, f->n_nodes > 1, st);
+  ++f->launches[1];
+  KS_CUDA(cudaGetLastError());
   return KS_OK;
 }
 
 int ks_solve(ks_factor* f, const double* B, double* X, int64_t q, void* stream) {
   if (!f) return fail(KS_ERR_INVALID, "null handle");
   if (!f->factored) return fail(KS_ERR_INVALID, "handle is not factored");
+  if (f->shard_root != 0) return fail(KS_ERR_INVALID, "sharded handle: use ks_solve_up / ks_solve_top / ks_solve_down");
   if (q < 0) return fail(KS_ERR_INVALID, "q must be >= 0");
   if (q == 0) return KS_OK;
   if (!B || !X) return fail(KS_ERR_INVALID, "null B or X");
@@ -772,22 +901,9 @@ int ks_solve(ks_factor* f, const double* B, double* X, int64_t q, void* stream) 
     Bd = f->bdev.p;
   }
   if (!xdev) Xd = f->xdev.p;
-  ks::SolveBufs sb{(int)q, f->z.p, f->c.p, f->tin.p, f->y.p};
-  const ks::LeafBatch lb = f->leafbatch();
-  ks::launch_leaf_fwd(lb, Bd, q, sb, st);
-  ++f->launches[1];
-  const int nlev = (int)f->levels.size();
-  for (int lev = 0; lev < nlev; ++lev) {
-    ks::launch_node_up(f->nodebatch(lev), sb, lev == nlev - 1, st);
-    ++f->launches[1];
-  }
-  for (int lev = nlev - 1; lev >= 0; --lev) {
-    ks::launch_node_down(f->nodebatch(lev), sb, lev == nlev - 1, st);
-    ++f->launches[1];
-  }
-  ks::launch_leaf_bwd(lb, Xd, q, sb, nlev > 0, st);
-  ++f->launches[1];
-  KS_CUDA(cudaGetLastError());
+  if ((rc = solve_up(f, Bd, q, st))) return rc;
+  if ((rc = solve_top(f, q, st))) return rc;
+  if ((rc = solve_down(f, Xd, q, st))) return rc;
   if (!xdev) KS_CUDA(cudaMemcpyAsync(X, Xd, bytes, cudaMemcpyDeviceToHost, st));
   tm.mark(1);
   if (!xdev || !bdev) KS_CUDA(cudaStreamSynchronize(st));
@@ -796,6 +912,60 @@ int ks_solve(ks_factor* f, const double* B, double* X, int64_t q, void* stream) 
     f->phase_ms[5] = tm.between(0, 1);
   }
   return KS_OK;
+}
+
+int ks_solve_up(ks_factor* f, const double* B_local, int64_t q, void* stream) {
+  if (!f || !f->local_factored) return fail(KS_ERR_INVALID, "shard is not factored");
+  if (q <= 0 || !B_local) return fail(KS_ERR_INVALID, "need q >= 1 and a device B");
+  KS_CUDA(cudaSetDevice(f->device));
+  if (int rc = ensure_solve_bufs(f, q)) return rc;
+  f->launches[1] = 0;
+  return solve_up(f, B_local - f->loc_begin * q, q, (cudaStream_t)stream);
+}
+
+int ks_solve_top(ks_factor* f, int64_t q, void* stream) {
+  if (!f || !f->factored) return fail(KS_ERR_INVALID, "handle is not factored (ks_factorize_top)");
+  KS_CUDA(cudaSetDevice(f->device));
+  return solve_top(f, q, (cudaStream_t)stream);
+}
+
+int ks_solve_down(ks_factor* f, double* X_local, int64_t q, void* stream) {
+  if (!f || !f->factored) return fail(KS_ERR_INVALID, "handle is not factored");
+  if (q <= 0 || !X_local) return fail(KS_ERR_INVALID, "need q >= 1 and a device X");
+  KS_CUDA(cudaSetDevice(f->device));
+  return solve_down(f, X_local - f->loc_begin * q, q, (cudaStream_t)stream);
+}
+
+// Skeleton-sized exchange buffers of one node (device pointers): 0 = H
+// (s_pad x s_pad), 1 = c (up-pass skeleton weights, s_pad x q), 2 = t (incoming
+// down-pass vector, s_pad x q). dir 0 copies out of the handle, 1 into it.
+int ks_node_exchange(ks_factor* f, int which, int64_t node, double* dev, int64_t q, int dir, void* stream) {
+  if (!f || !dev || node < 0 || node >= f->n_nodes) return fail(KS_ERR_INVALID, "bad exchange arguments");
+  KS_CUDA(cudaSetDevice(f->device));
+  double* buf;
+  size_t count;
+  if (which == 0) {
+    buf = f->hbuf.p + node * (int64_t)f->s_pad * f->s_pad;
+    count = (size_t)f->s_pad * f->s_pad;
+  } else {
+    if (q > f->q_cap) return fail(KS_ERR_INVALID, "solve buffers hold q <= %lld", (long long)f->q_cap);
+    buf = (which == 1 ? f->c.p : f->tin.p) + node * (int64_t)f->s_pad * q;
+    count = (size_t)f->s_pad * q;
+  }
+  if (dir == 0)
+    KS_CUDA(cudaMemcpyAsync(dev, buf, count * sizeof(double), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  else
+    KS_CUDA(cudaMemcpyAsync(buf, dev, count * sizeof(double), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return KS_OK;
+}
+
+int ks_shard_info(const ks_factor* f, int64_t* out, int64_t cap) {
+  // [shard_root, shard_level, loc_begin, loc_end, s_pad, n_peers, peers...]
+  if (!f || !out) return fail(KS_ERR_INVALID, "null argument");
+  std::vector<int64_t> v{f->shard_root, f->shard_level, f->loc_begin, f->loc_end, f->s_pad, (int64_t)f->peers.size()};
+  for (int64_t p : f->peers) v.push_back(p);
+  for (int64_t i = 0; i < (int64_t)v.size() && i < cap; ++i) out[i] = v[i];
+  return (int)v.size();
 }
 
 int ks_get_diag(const ks_factor* f, ks_diag* out) {
