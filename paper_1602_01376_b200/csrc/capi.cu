@@ -87,7 +87,7 @@ struct ks_factor {
   DBuf<int64_t> skel_off, coeff_off;
   DBuf<double> coeff;
   DBuf<int> leaf_node, leaf_begin, leaf_size, leaf_info;
-  DBuf<int> int_node, int_left, int_right, int_info, piv, moves;
+  DBuf<int> int_node, int_left, int_right, int_info, piv, moves, pm;
   DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
   // solve scratch
   DBuf<double> z, c, tin, y, bdev, xdev;
@@ -166,12 +166,13 @@ struct ks_factor {
     nb.cond = cond.p + first;
     nb.info = int_info.p + first;
     nb.moves = moves.p + (int64_t)first * (2 * 64 + 1);
+    nb.pm = pm.p + (int64_t)first * t_pad;
     return nb;
   }
   void release_all() {
     coords.release(); rank_d.release(); skel_pos.release(); skel_off.release(); coeff_off.release();
     coeff.release(); leaf_node.release(); leaf_begin.release(); leaf_size.release(); leaf_info.release();
-    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release();
+    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
     norm1.release(); cond.release(); z.release(); c.release(); tin.release(); y.release();
     bdev.release(); xdev.release();
@@ -520,6 +521,7 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     KS_CUDA(f->int_info.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->piv.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
     KS_CUDA(f->moves.alloc((size_t)std::max(f->n_int, 1) * (2 * 64 + 1)));
+    KS_CUDA(f->pm.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
     KS_CUDA(f->leafA.alloc(nl * (size_t)f->R * f->m_pad));
     KS_CUDA(f->inv.alloc(nl * 64 * 64));
     KS_CUDA(f->hbuf.alloc((size_t)nn * f->s_pad * f->s_pad + 1));
@@ -669,6 +671,8 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
                    Operand{nb.Aug + TP, T, TT, nullptr}, OperandW{nb.Aug + (int64_t)TP * T + TP, T, TT, nullptr},
                    -1.0, 1.0), false, false);
     if (rc) return rc;
+    ks::launch_compose_perm(nb, st);
+    ++L.count[0];
     // condition estimate off the critical path (it only feeds diagnostics)
     KS_CUDA(cudaEventRecord(f->ev_fork, st));
     KS_CUDA(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
@@ -836,16 +840,49 @@ int ks_factorize_top(ks_factor* f, void* stream) {
   return KS_OK;
 }
 
+static void trace_mark(ks_factor* f, cudaStream_t st, const char* what) {
+  Launcher L{f, st, &f->launches[1]};
+  L.check(what);
+}
+
+static void trace_build_report(ks_factor* f) {
+  if (!trace_on() || f->trace_n < 2) return;
+  cudaDeviceSynchronize();
+  std::vector<std::pair<std::string, std::pair<int, double>>> agg;
+  for (int i = 1; i < f->trace_n; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, f->trace_ev[i - 1], f->trace_ev[i]);
+    std::string nm = (f->trace_tag[i] < 0 ? std::string("leaf ") : "L" + std::to_string(f->trace_tag[i]) + " ") +
+                     f->trace_name[i];
+    bool found = false;
+    for (auto& a : agg)
+      if (a.first == nm) { a.second.first++; a.second.second += ms; found = true; }
+    if (!found) agg.push_back({nm, {1, (double)ms}});
+  }
+  std::string rep;
+  char line[160];
+  for (auto& a : agg) {
+    std::snprintf(line, sizeof line, "%-24s %5d x %10.3f ms\n", a.first.c_str(), a.second.first, a.second.second);
+    rep += line;
+  }
+  f->trace_report = rep;
+}
+
 // Solve phases. Shard-local rows are [loc_begin, loc_end) of tree order; the
 // kernels index B and X by absolute tree position, so local buffers are passed
 // with a virtual base (ptr - loc_begin * q).
 static int solve_up(ks_factor* f, const double* Bd, int64_t q, cudaStream_t st) {
   ks::SolveBufs sb{(int)q, f->z.p, f->c.p, f->tin.p, f->y.p};
+  f->cur_tag = -1;
+  trace_mark(f, st, "start");
   ks::launch_leaf_fwd(f->leafbatch(), Bd, q, sb, st);
   ++f->launches[1];
+  trace_mark(f, st, "leaf_fwd");
   for (int lev = 0; lev < f->n_local_levels; ++lev) {
+    f->cur_tag = lev;
     ks::launch_node_up(f->nodebatch(lev), sb, f->levels[lev][0] == 0, st);
     ++f->launches[1];
+    trace_mark(f, st, "node_up");
   }
   KS_CUDA(cudaGetLastError());
   return KS_OK;
@@ -859,8 +896,10 @@ static int solve_top(ks_factor* f, int64_t q, cudaStream_t st) {
     ++f->launches[1];
   }
   for (int lev = nlev - 1; lev >= f->n_local_levels; --lev) {
+    f->cur_tag = lev;
     ks::launch_node_down(f->nodebatch(lev), sb, f->levels[lev][0] == 0, st);
     ++f->launches[1];
+    trace_mark(f, st, "node_down");
   }
   KS_CUDA(cudaGetLastError());
   return KS_OK;
@@ -869,11 +908,15 @@ static int solve_top(ks_factor* f, int64_t q, cudaStream_t st) {
 static int solve_down(ks_factor* f, double* Xd, int64_t q, cudaStream_t st) {
   ks::SolveBufs sb{(int)q, f->z.p, f->c.p, f->tin.p, f->y.p};
   for (int lev = f->n_local_levels - 1; lev >= 0; --lev) {
+    f->cur_tag = lev;
     ks::launch_node_down(f->nodebatch(lev), sb, f->levels[lev][0] == 0, st);
     ++f->launches[1];
+    trace_mark(f, st, "node_down");
   }
+  f->cur_tag = -1;
   ks::launch_leaf_bwd(f->leafbatch(), Xd, q, sb, f->n_nodes > 1, st);
   ++f->launches[1];
+  trace_mark(f, st, "leaf_bwd");
   KS_CUDA(cudaGetLastError());
   return KS_OK;
 }
@@ -890,6 +933,7 @@ int ks_solve(ks_factor* f, const double* B, double* X, int64_t q, void* stream) 
   int rc = ensure_solve_bufs(f, q);
   if (rc) return rc;
   f->launches[1] = 0;
+  f->trace_n = 0;
   PhaseTimer tm(f->profiling, st, 2);
   tm.mark(0);
   const bool bdev = is_device_ptr(B), xdev = is_device_ptr(X);
@@ -907,6 +951,7 @@ int ks_solve(ks_factor* f, const double* B, double* X, int64_t q, void* stream) 
   if (!xdev) KS_CUDA(cudaMemcpyAsync(X, Xd, bytes, cudaMemcpyDeviceToHost, st));
   tm.mark(1);
   if (!xdev || !bdev) KS_CUDA(cudaStreamSynchronize(st));
+  trace_build_report(f);
   if (f->profiling) {
     KS_CUDA(cudaStreamSynchronize(st));
     f->phase_ms[5] = tm.between(0, 1);

@@ -624,13 +624,7 @@ __global__ void __launch_bounds__(STHREADS) k_hager(DevTree t, NodeBatch nb) {
     if (threadIdx.x == 0) nb.cond[k] = 0.0;
     return;
   }
-  if (threadIdx.x == 0) {  // compose the row interchanges once (linalg.py:250-253)
-    for (int i = 0; i < TP; ++i) pm[i] = i;
-    for (int i = 0; i < TP; ++i) {
-      const int p = piv[i];
-      if (p != i) { const int tmp = pm[i]; pm[i] = pm[p]; pm[p] = tmp; }
-    }
-  }
+  for (int i = threadIdx.x; i < TP; i += STHREADS) pm[i] = nb.pm[(int64_t)k * TP + i];  // composed swaps
   auto real = [&](int i) { return i < S ? (i < sl) : (i - S < sr); };
   for (int i = threadIdx.x; i < TP; i += STHREADS) x[i] = real(i) ? 1.0 / n : 0.0;
   __syncthreads();
@@ -680,6 +674,23 @@ void launch_hager(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
   }
   k_hager<<<nb.count, STHREADS, smem, st>>>(t, nb);
 }
+
+// Composed row interchanges of each node's LU: (Pi v)[i] = v[pm[i]], from the
+// LAPACK-style swap sequence (linalg.py:250-253). One warp per node.
+__global__ void k_compose_perm(NodeBatch nb) {
+  const int k = blockIdx.x;
+  const int* piv = nb.piv + (int64_t)k * nb.t_pad;
+  int* pm = nb.pm + (int64_t)k * nb.t_pad;
+  for (int i = threadIdx.x; i < nb.t_pad; i += blockDim.x) pm[i] = i;
+  __syncwarp();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < nb.t_pad; ++i) {
+      const int p = piv[i];
+      if (p != i) { const int t = pm[i]; pm[i] = pm[p]; pm[p] = t; }
+    }
+}
+
+void launch_compose_perm(const NodeBatch& nb, cudaStream_t st) { k_compose_perm<<<nb.count, 32, 0, st>>>(nb); }
 
 // H = sym(trailing block) -> Hbuf[node] (solver.py:163).
 __global__ void k_extract_h(NodeBatch nb, double* H, int64_t stride) {

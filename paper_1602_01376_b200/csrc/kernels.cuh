@@ -44,6 +44,7 @@ struct NodeBatch {
   double* cond;         // count
   int* info;            // count (LU: first zero pivot column + 1)
   int* moves;           // count x (1 + 2*64): rows moved by the last LU panel
+  int* pm;              // count x t_pad: composed row interchanges, (Pi v)[i] = v[pm[i]]
 };
 
 // --- factor launchers (factor_kernels.cu) ---
@@ -59,6 +60,7 @@ void launch_lu_swap(const NodeBatch& nb, int c0, int w, cudaStream_t st);
 void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncols, cudaStream_t st);
 void launch_hager(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
 void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st);
+void launch_compose_perm(const NodeBatch& nb, cudaStream_t st);
 // leaf LU fallback (NotSPD leaves): augmented [[A, P^T], [-P, 0]]
 void launch_leaf_aug_init(const DevTree& t, const LeafBatch& lb, const NodeBatch& fb, double lam,
                           cudaStream_t st);
@@ -76,6 +78,8 @@ void launch_leaf_bwd(const LeafBatch& lb, double* X, int64_t ldx, const SolveBuf
                      cudaStream_t st);
 void launch_node_up(const NodeBatch& nb, const SolveBufs& sb, bool root, cudaStream_t st);
 void launch_node_down(const NodeBatch& nb, const SolveBufs& sb, bool root, cudaStream_t st);
+void launch_node_up_cluster(const NodeBatch& nb, const SolveBufs& sb, bool root, int q0, int qc, cudaStream_t st);
+void launch_node_down_cluster(const NodeBatch& nb, const SolveBufs& sb, bool root, int q0, int qc, cudaStream_t st);
 // leaf LU fallback solves
 void launch_leaf_lu_fwd(const LeafBatch& lb, const NodeBatch& fb, const int* leaf_idx, const double* B,
                         int64_t ldb, const SolveBufs& sb, cudaStream_t st);

@@ -96,12 +96,20 @@ __global__ void __launch_bounds__(STHREADS) k_node_up(NodeBatch nb, SolveBufs sb
   cta_gemv_rows<QC>(Bc, S, S, S, cc + S * QC, w, QC, false);      // B c_r
   cta_gemv_cols<QC>(Bc, S, S, S, cc, w + S * QC, 1.0, red);       // B^T c_l
   __syncthreads();
-  const int* piv = nb.piv + (int64_t)k * TP;
-  if (threadIdx.x < QC) {
-    const int q = threadIdx.x;
-    for (int i = 0; i < TP; ++i) {
-      const int p = piv[i];
-      if (p != i) { const double t = w[i * QC + q]; w[i * QC + q] = w[p * QC + q]; w[p * QC + q] = t; }
+  {  // Pi w through the composed row interchanges (cc is free as scratch only after c)
+    const int* pm = nb.pm + (int64_t)k * TP;
+    double* tmp = red;  // reuse: needs TP*QC <= SWARPS*32*QC -> only when TP <= 256
+    if (TP <= SWARPS * 32) {
+      for (int e = threadIdx.x; e < TP * QC; e += STHREADS) tmp[e] = w[pm[e / QC] * QC + e % QC];
+      __syncthreads();
+      for (int e = threadIdx.x; e < TP * QC; e += STHREADS) w[e] = tmp[e];
+    } else if (threadIdx.x < QC) {
+      const int q = threadIdx.x;
+      const int* piv = nb.piv + (int64_t)k * TP;
+      for (int i = 0; i < TP; ++i) {
+        const int p = piv[i];
+        if (p != i) { const double t = w[i * QC + q]; w[i * QC + q] = w[p * QC + q]; w[p * QC + q] = t; }
+      }
     }
   }
   __syncthreads();
@@ -177,6 +185,7 @@ static void set_smem(K kern, size_t bytes) {
       return;
     }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   seen.push_back({(const void*)kern, bytes});
 }
 
@@ -207,8 +216,16 @@ void launch_leaf_bwd(const LeafBatch& lb, double* X, int64_t ldx, const SolveBuf
   });
 }
 
+// Levels with many nodes keep one CTA per node (enough CTAs to saturate HBM);
+// levels with few nodes use an 8-CTA cluster per node (solve_cluster.cu).
+constexpr int kClusterMaxNodes = 128;
+
 void launch_node_up(const NodeBatch& nb, const SolveBufs& sb, bool root, cudaStream_t st) {
   for_chunks(sb.q, [&](int q0, int qc) {
+    if (nb.count <= kClusterMaxNodes) {
+      launch_node_up_cluster(nb, sb, root, q0, qc, st);
+      return;
+    }
     const size_t smem = ((size_t)2 * nb.t_pad + SWARPS * 32) * qc * sizeof(double);
 #define KS_CASE(QC)                                                                 \
   if (qc == QC) {                                                                   \
@@ -222,6 +239,10 @@ void launch_node_up(const NodeBatch& nb, const SolveBufs& sb, bool root, cudaStr
 
 void launch_node_down(const NodeBatch& nb, const SolveBufs& sb, bool root, cudaStream_t st) {
   for_chunks(sb.q, [&](int q0, int qc) {
+    if (nb.count <= kClusterMaxNodes) {
+      launch_node_down_cluster(nb, sb, root, q0, qc, st);
+      return;
+    }
     const size_t smem = ((size_t)nb.t_pad + nb.s_pad) * qc * sizeof(double);
 #define KS_CASE(QC)                                                                 \
   if (qc == QC) {                                                                   \

@@ -1,6 +1,11 @@
 // CTA-level (256 threads) blocked triangular solves and GEMVs on matrices in
 // global memory with vectors in shared memory; used by the solve kernels and
-// by the Hager condition estimator. Rows of A are contiguous (ld = lda).
+// by the Hager condition estimator. Rows of A are contiguous (ld = lda, even).
+//
+// These loops stream factor rows from HBM once per pass, so they are written
+// for memory-level parallelism: 16-byte loads, several independent loads per
+// lane in flight, and the next diagonal block fetched into registers while the
+// off-diagonal GEMV of the current block runs.
 #pragma once
 
 #include "common.cuh"
@@ -11,9 +16,55 @@ constexpr int SB = 32;       // diagonal block of the blocked triangular solves
 constexpr int STHREADS = 256;
 constexpr int SWARPS = STHREADS / 32;
 
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+
+// acc[i][q] += sum_{c in [cb, ce)} A[rb+i][c] x[c][q], i < 4, for one warp.
+// [cb, ce) is a multiple of 32 wide and starts even; partial sums per lane.
+template <int QC>
+__device__ __forceinline__ void warp_rows4(const double* __restrict__ A, int64_t lda, int rb, int nrows, int cb,
+                                           int ce, const double* x, double (&acc)[4][QC]) {
+  const int lane = threadIdx.x & 31;
+  int c = cb + 2 * lane;
+  for (; c + 64 < ce; c += 128) {  // two 64-column strips per iteration: 8 loads in flight
+    double2 a0[4], a1[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool ok = rb + i < nrows;
+      a0[i] = ok ? ldg2(A + (int64_t)(rb + i) * lda + c) : make_double2(0.0, 0.0);
+      a1[i] = ok ? ldg2(A + (int64_t)(rb + i) * lda + c + 64) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < QC; ++q) {
+      const double x0 = x[c * QC + q], x1 = x[(c + 1) * QC + q];
+      const double x2 = x[(c + 64) * QC + q], x3 = x[(c + 65) * QC + q];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i][q] = fma(a0[i].x, x0, acc[i][q]);
+        acc[i][q] = fma(a0[i].y, x1, acc[i][q]);
+        acc[i][q] = fma(a1[i].x, x2, acc[i][q]);
+        acc[i][q] = fma(a1[i].y, x3, acc[i][q]);
+      }
+    }
+  }
+  for (; c < ce; c += 64) {
+    double2 a0[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      a0[i] = (rb + i < nrows) ? ldg2(A + (int64_t)(rb + i) * lda + c) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < QC; ++q) {
+      const double x0 = x[c * QC + q], x1 = x[(c + 1) * QC + q];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i][q] = fma(a0[i].x, x0, acc[i][q]);
+        acc[i][q] = fma(a0[i].y, x1, acc[i][q]);
+      }
+    }
+  }
+}
+
 // Row-oriented blocked triangular solve, in place on the shared vector x (n x QC):
-// lower (ascending blocks) or upper (descending), unit or not. Rows of A are
-// contiguous (ld = lda); n is a multiple of SB.
+// lower (ascending blocks) or upper (descending), unit or not. n is a multiple of SB.
 template <int QC, bool UPPER, bool UNIT>
 __device__ void cta_trsv_rows(const double* __restrict__ A, int64_t lda, int n, double* x, double (*D)[SB + 1]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -22,7 +73,13 @@ __device__ void cta_trsv_rows(const double* __restrict__ A, int64_t lda, int n, 
     const int bi = UPPER ? nb - 1 - s : s;
     const int r0 = bi * SB;
     const int cb = UPPER ? r0 + SB : 0, ce = UPPER ? n : r0;
-    // 1) off-diagonal GEMV: 4 rows per warp
+    // diagonal block: issue its loads first, store after the GEMV
+    double dreg[SB * SB / STHREADS];
+#pragma unroll
+    for (int u = 0; u < SB * SB / STHREADS; ++u) {
+      const int e = threadIdx.x + u * STHREADS;
+      dreg[u] = A[(int64_t)(r0 + e / SB) * lda + r0 + e % SB];
+    }
     {
       double acc[4][QC];
 #pragma unroll
@@ -30,17 +87,7 @@ __device__ void cta_trsv_rows(const double* __restrict__ A, int64_t lda, int n, 
 #pragma unroll
         for (int q = 0; q < QC; ++q) acc[i][q] = 0.0;
       const int rb = r0 + warp * 4;
-      for (int c = cb + lane; c < ce; c += 32) {
-        double a[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = __ldg(A + (int64_t)(rb + i) * lda + c);
-#pragma unroll
-        for (int q = 0; q < QC; ++q) {
-          const double xv = x[c * QC + q];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) acc[i][q] = fma(a[i], xv, acc[i][q]);
-        }
-      }
+      warp_rows4<QC>(A, lda, rb, n, cb, ce, x, acc);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -49,13 +96,13 @@ __device__ void cta_trsv_rows(const double* __restrict__ A, int64_t lda, int n, 
           if (lane == 0) x[(rb + i) * QC + q] -= v;
         }
     }
-    // 2) diagonal block to shared memory
-    for (int e = threadIdx.x; e < SB * SB; e += STHREADS) {
-      const int i = e / SB, j = e % SB;
-      D[i][j] = A[(int64_t)(r0 + i) * lda + r0 + j];
+#pragma unroll
+    for (int u = 0; u < SB * SB / STHREADS; ++u) {
+      const int e = threadIdx.x + u * STHREADS;
+      D[e / SB][e % SB] = dreg[u];
     }
     __syncthreads();
-    // 3) one warp: column-oriented substitution, lane r owns row r0+r
+    // one warp: column-oriented substitution, lane r owns row r0+r
     if (warp == 0) {
       double v[QC];
 #pragma unroll
@@ -82,7 +129,8 @@ __device__ void cta_trsv_rows(const double* __restrict__ A, int64_t lda, int n, 
   }
 }
 
-// y[r] = sum_c A[r][c] x[c] for rows [0, nrows): warps over rows, lanes over c.
+// y[r] (+)= sum_c A[r][c] x[c] for rows [0, nrows): warps over rows, lanes over c.
+// ncols is a multiple of 32.
 template <int QC>
 __device__ void cta_gemv_rows(const double* __restrict__ A, int64_t lda, int nrows, int ncols, const double* x,
                               double* out, int64_t ldo, bool accumulate) {
@@ -93,17 +141,7 @@ __device__ void cta_gemv_rows(const double* __restrict__ A, int64_t lda, int nro
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int q = 0; q < QC; ++q) acc[i][q] = 0.0;
-    for (int c = lane; c < ncols; c += 32) {
-      double a[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = (rb + i < nrows) ? __ldg(A + (int64_t)(rb + i) * lda + c) : 0.0;
-#pragma unroll
-      for (int q = 0; q < QC; ++q) {
-        const double xv = x[c * QC + q];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i][q] = fma(a[i], xv, acc[i][q]);
-      }
-    }
+    warp_rows4<QC>(A, lda, rb, nrows, 0, ncols, x, acc);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -117,7 +155,29 @@ __device__ void cta_gemv_rows(const double* __restrict__ A, int64_t lda, int nro
   }
 }
 
-// out[c] (+)= sum_r A[r][c] x[r] for columns [0, ncols): lanes over c, warps
+// acc[q] += sum_{k in [kb, ke), k = warp (mod SWARPS)} A[k][col] x[k][q]: 8 loads in flight.
+template <int QC>
+__device__ __forceinline__ void warp_cols(const double* __restrict__ A, int64_t lda, int kb, int ke, int col,
+                                          const double* x, double (&acc)[QC]) {
+  const int warp = threadIdx.x >> 5;
+  int k = kb + warp;
+  for (; k + 7 * SWARPS < ke; k += 8 * SWARPS) {
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = __ldg(A + (int64_t)(k + u * SWARPS) * lda + col);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int q = 0; q < QC; ++q) acc[q] = fma(a[u], x[(k + u * SWARPS) * QC + q], acc[q]);
+  }
+  for (; k < ke; k += SWARPS) {
+    const double a = __ldg(A + (int64_t)k * lda + col);
+#pragma unroll
+    for (int q = 0; q < QC; ++q) acc[q] = fma(a, x[k * QC + q], acc[q]);
+  }
+}
+
+// out[c] += sign * sum_r A[r][c] x[r] for columns [0, ncols): lanes over c, warps
 // over r, cross-warp reduction in shared memory. red: SWARPS x 32 x QC.
 template <int QC>
 __device__ void cta_gemv_cols(const double* __restrict__ A, int64_t lda, int nrows, int ncols, const double* x,
@@ -128,13 +188,7 @@ __device__ void cta_gemv_cols(const double* __restrict__ A, int64_t lda, int nro
     double acc[QC];
 #pragma unroll
     for (int q = 0; q < QC; ++q) acc[q] = 0.0;
-    if (c < ncols) {
-      for (int r = warp; r < nrows; r += SWARPS) {
-        const double a = __ldg(A + (int64_t)r * lda + c);
-#pragma unroll
-        for (int q = 0; q < QC; ++q) acc[q] = fma(a, x[r * QC + q], acc[q]);
-      }
-    }
+    if (c < ncols) warp_cols<QC>(A, lda, 0, nrows, c, x, acc);
 #pragma unroll
     for (int q = 0; q < QC; ++q) red[(warp * 32 + lane) * QC + q] = acc[q];
     __syncthreads();
@@ -150,7 +204,6 @@ __device__ void cta_gemv_cols(const double* __restrict__ A, int64_t lda, int nro
   }
 }
 
-
 // Transposed blocked triangular solve op(A)^T x = b, in place on x (n x QC):
 // FORWARD: A upper, A^T lower, blocks ascending (U^T w = b, linalg.py:257);
 // !FORWARD: A lower, A^T upper, blocks descending (L^T x = b, linalg.py:235-243,
@@ -165,21 +218,24 @@ __device__ void cta_trsv_trans(const double* __restrict__ A, int64_t lda, int n,
     const int bi = FORWARD ? s : nb - 1 - s;
     const int r0 = bi * SB;
     const int kb = FORWARD ? 0 : r0 + SB, ke = FORWARD ? r0 : n;
+    double dreg[SB * SB / STHREADS];
+#pragma unroll
+    for (int u = 0; u < SB * SB / STHREADS; ++u) {
+      const int e = threadIdx.x + u * STHREADS;
+      dreg[u] = A[(int64_t)(r0 + e / SB) * lda + r0 + e % SB];
+    }
     {
       double acc[QC];
 #pragma unroll
       for (int q = 0; q < QC; ++q) acc[q] = 0.0;
-      for (int k = kb + warp; k < ke; k += SWARPS) {
-        const double a = __ldg(A + (int64_t)k * lda + r0 + lane);
-#pragma unroll
-        for (int q = 0; q < QC; ++q) acc[q] = fma(a, x[k * QC + q], acc[q]);
-      }
+      warp_cols<QC>(A, lda, kb, ke, r0 + lane, x, acc);
 #pragma unroll
       for (int q = 0; q < QC; ++q) red[(warp * 32 + lane) * QC + q] = acc[q];
     }
-    for (int e = threadIdx.x; e < SB * SB; e += STHREADS) {
-      const int i = e / SB, j = e % SB;
-      D[i][j] = A[(int64_t)(r0 + i) * lda + r0 + j];
+#pragma unroll
+    for (int u = 0; u < SB * SB / STHREADS; ++u) {
+      const int e = threadIdx.x + u * STHREADS;
+      D[e / SB][e % SB] = dreg[u];
     }
     __syncthreads();
     if (warp == 0) {

@@ -31,3 +31,8 @@ if os.environ.get("KS_TRACE") == "1":
     hf.refactorize(cfg.lam)
     print(hf.trace_report())
     print("levels", [round(x, 3) for x in hf.level_ms()])
+if os.environ.get("KS_TRACE") == "1":
+    ks.solve_many(hf, B)
+    torch.cuda.synchronize()
+    print("solve trace q=%d" % a.q)
+    print(hf.trace_report())
