@@ -267,12 +267,9 @@ int trsm_ul(Launcher& L, const ks::NodeBatch& nb, int r0, int w, int c0, int nco
 // Recursive LU of columns [c0, c0+w) over rows [c0, T), pivots among rows < t_pad.
 int rlu(Launcher& L, const ks::NodeBatch& nb, int c0, int w, int pw) {
   if (w <= pw) {
-    ks::launch_lu_panel(nb, c0, w, L.st);
-    int rc = L.check("lu_panel");
-    if (rc) return rc;
-    ks::launch_lu_swap(nb, c0, w, L.st);
-    *L.count += 2;
-    return L.check("lu_swap");
+    ks::launch_lu_panel(nb, c0, w, L.st);  // panel LU + its row interchanges everywhere else
+    *L.count += 1;
+    return L.check("lu_panel");
   }
   const int h = (int)roundup(w / 2, pw);
   int rc = rlu(L, nb, c0, h, pw);

@@ -363,19 +363,21 @@ void launch_colnorm1(const DevTree&, const NodeBatch& nb, cudaStream_t st) {
 // the pivot search, one after the rank-1 update. Ties in |pivot| go to the
 // smallest logical position, as np.argmax does.
 // --------------------------------------------------------------------------
-template <int W, int RPT>
-__global__ void __launch_bounds__(512) k_lu_panel(NodeBatch nb, int c0) {
-  constexpr int NT = 512, NW = NT / 32;
+template <int W, int RPT, int NT>
+__global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0) {
+  constexpr int NW = NT / 32;
   const int k = blockIdx.x;
   const int T = nb.T;
   double* A = nb.Aug + (int64_t)k * T * T;
   const int rows = T - c0;
   const int plim = nb.t_pad - c0;  // eligible pivot rows: physical (= original) local rows < plim
+  extern __shared__ double fin[];  // rows x W finished values (column kk written at step kk)
   // per-warp candidate pivot rows, double buffered by column parity
   __shared__ __align__(16) double cand[2][NW][W];
   __shared__ double wv[2][NW];
   __shared__ int wp[2][NW], wr[2][NW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // a[i][0] is always the current column: after each step the window rotates left
   double a[RPT][W];
   int pos[RPT];
   bool done[RPT];
@@ -394,103 +396,147 @@ __global__ void __launch_bounds__(512) k_lu_panel(NodeBatch nb, int c0) {
   }
   int* info = nb.info + k;
   int* piv = nb.piv + (int64_t)k * nb.t_pad + c0;
-#pragma unroll
+#pragma unroll 1
   for (int kk = 0; kk < W; ++kk) {
     const int buf = kk & 1;
-    // 1) pivot search in registers, ties to the smallest logical position
+    // 1) pivot search in registers; warp max by shuffles, ties to the smallest
+    //    logical position through a warp min-reduction (np.argmax semantics)
     double bv = -1.0;
-    int bp = 0x7fffffff, br = -1, bi = -1;
+    int bp = 0x7fffffff, bi = -1;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int r = threadIdx.x + i * NT;
       if (r < plim && !done[i]) {
-        const double v = fabs(a[i][kk]);
-        if (v > bv || (v == bv && pos[i] < bp)) { bv = v; bp = pos[i]; br = r; bi = i; }
+        const double v = fabs(a[i][0]);
+        if (v > bv || (v == bv && pos[i] < bp)) { bv = v; bp = pos[i]; bi = i; }
       }
     }
-    double wbv = bv;
-    int wbp = bp, wbr = br;
+    double wmax = bv;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, wbv, o);
-      const int op = __shfl_xor_sync(0xffffffffu, wbp, o);
-      const int orr = __shfl_xor_sync(0xffffffffu, wbr, o);
-      if (ov > wbv || (ov == wbv && op < wbp)) { wbv = ov; wbp = op; wbr = orr; }
-    }
-    // the winning lane publishes its row for the whole CTA
-    if (wbr >= 0 && wbr == br) {
+    for (int o = 16; o > 0; o >>= 1) wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    const int wpos = (int)__reduce_min_sync(0xffffffffu, (unsigned)(bv == wmax ? bp : 0x7fffffff));
+    if (bv == wmax && bp == wpos && bi >= 0) {  // the winning lane publishes its row
 #pragma unroll
       for (int i = 0; i < RPT; ++i)
         if (i == bi) {
 #pragma unroll
           for (int j = 0; j < W; ++j) cand[buf][warp][j] = a[i][j];
+          wr[buf][warp] = threadIdx.x + i * NT;
         }
     }
-    if (lane == 0) { wv[buf][warp] = wbv; wp[buf][warp] = wbp; wr[buf][warp] = wbr; }
+    if (lane == 0) { wv[buf][warp] = wmax; wp[buf][warp] = wpos; }
     __syncthreads();
     int ww = 0;
-    bv = wv[buf][0]; bp = wp[buf][0]; br = wr[buf][0];
+    bv = wv[buf][0];
+    bp = wp[buf][0];
 #pragma unroll
-    for (int w = 1; w < NW; ++w)
-      if (wv[buf][w] > bv || (wv[buf][w] == bv && wp[buf][w] < bp)) { bv = wv[buf][w]; bp = wp[buf][w]; br = wr[buf][w]; ww = w; }
-    const bool singular = !(bv > 0.0);
-    if (singular) {  // exactly zero pivot column: SingularMatrixError (linalg.py:205-206)
-      if (threadIdx.x == 0 && *info == 0) *info = c0 + kk + 1;
-      br = -1;
+    for (int w = 1; w < NW; ++w) {
+      const double v = wv[buf][w];
+      const int p = wp[buf][w];
+      if (v > bv || (v == bv && p < bp)) { bv = v; bp = p; ww = w; }
     }
-    if (threadIdx.x == 0) piv[kk] = c0 + (singular ? kk : bp);
+    const bool singular = !(bv > 0.0);
+    const int br = singular ? -1 : wr[buf][ww];
+    if (threadIdx.x == 0) {
+      if (singular && *info == 0) *info = c0 + kk + 1;  // linalg.py:205-206
+      piv[kk] = c0 + (singular ? kk : bp);
+    }
     double prow[W];
 #pragma unroll
-    for (int j = kk; j < W; ++j) prow[j] = singular ? (j == kk ? 1.0 : 0.0) : cand[buf][ww][j];
+    for (int j = 0; j < W; ++j) prow[j] = singular ? (j == 0 ? 1.0 : 0.0) : cand[buf][ww][j];
+    const double rcp = 1.0 / prow[0];
     // 2) logical swap kk <-> bp, eliminate every other remaining row (linalg.py:209-212)
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      if (done[i]) continue;
       const int r = threadIdx.x + i * NT;
-      if (!singular) {
-        if (r == br) { pos[i] = kk; done[i] = true; continue; }
-        if (pos[i] == kk) pos[i] = bp;
-      } else if (pos[i] == kk) {
-        done[i] = true;
-        continue;
-      }
-      const double l = a[i][kk] / prow[kk];
-      a[i][kk] = l;
+      if (!done[i]) {
+        bool piv_row = false;
+        if (!singular) {
+          if (r == br) { pos[i] = kk; piv_row = true; }
+          else if (pos[i] == kk) pos[i] = bp;
+        } else if (pos[i] == kk) {
+          piv_row = true;
+        }
+        if (piv_row) {  // U row: its values from column kk on are final
+          done[i] = true;
 #pragma unroll
-      for (int j = kk + 1; j < W; ++j) a[i][j] = fma(-l, prow[j], a[i][j]);
+          for (int j = 0; j < W; ++j)
+            if (j < W - kk) fin[r * W + kk + j] = a[i][j];
+        } else {
+          const double l = a[i][0] * rcp;
+          fin[r * W + kk] = l;
+#pragma unroll
+          for (int j = 1; j < W; ++j) a[i][j] = fma(-l, prow[j], a[i][j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < W - 1; ++j) a[i][j] = a[i][j + 1];
+      a[i][W - 1] = 0.0;
     }
   }
-  // rows back to their logical positions; moved rows are listed for k_lu_swap
-  __shared__ int nmove;
-  if (threadIdx.x == 0) nmove = 0;
   __syncthreads();
-  int* mv = nb.moves + (int64_t)k * (2 * 64 + 1);
+  // panel rows back to their logical positions
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     const int r = threadIdx.x + i * NT;
     if (r >= rows) continue;
     double2* dst = reinterpret_cast<double2*>(A + (int64_t)(c0 + pos[i]) * T + c0);
+    const double2* f2 = reinterpret_cast<const double2*>(fin + r * W);
 #pragma unroll
-    for (int j = 0; j < W / 2; ++j) dst[j] = make_double2(a[i][2 * j], a[i][2 * j + 1]);
-    if (pos[i] != r) {
+    for (int j = 0; j < W / 2; ++j) dst[j] = f2[j];
+  }
+  // the same row interchanges for every column outside the panel: at most 2W
+  // rows moved; the list goes through shared memory, all loads before stores
+  __shared__ int msrc[2 * W], mdst[2 * W];
+  __shared__ int nmove;
+  if (threadIdx.x == 0) nmove = 0;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int r = threadIdx.x + i * NT;
+    if (r < rows && pos[i] != r) {
       const int slot = atomicAdd(&nmove, 1);
-      mv[1 + 2 * slot] = c0 + r;       // source row (before this panel)
-      mv[2 + 2 * slot] = c0 + pos[i];  // destination row
+      msrc[slot] = c0 + r;
+      mdst[slot] = c0 + pos[i];
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) mv[0] = nmove;
+  const int nm = nmove;
+  for (int col = threadIdx.x; col < T; col += NT) {
+    if (col >= c0 && col < c0 + W) continue;
+    double v[2 * W];
+#pragma unroll
+    for (int m = 0; m < 2 * W; ++m)
+      if (m < nm) v[m] = A[(int64_t)msrc[m] * T + col];
+#pragma unroll
+    for (int m = 0; m < 2 * W; ++m)
+      if (m < nm) A[(int64_t)mdst[m] * T + col] = v[m];
+  }
+}
+
+template <int W, int RPT, int NT>
+static void launch_panel(const NodeBatch& nb, int c0, cudaStream_t st) {
+  const size_t smem = (size_t)(nb.T - c0) * W * sizeof(double);
+  static size_t set = 0;
+  if (smem > set) {
+    cudaFuncSetAttribute(k_lu_panel<W, RPT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = smem;
+  }
+  k_lu_panel<W, RPT, NT><<<nb.count, NT, smem, st>>>(nb, c0);
 }
 
 template <int W>
 static void launch_panel_w(const NodeBatch& nb, int c0, cudaStream_t st) {
   const int rows = nb.T - c0;
-  const int rpt = (rows + 511) / 512;
-  if (rpt <= 1) k_lu_panel<W, 1><<<nb.count, 512, 0, st>>>(nb, c0);
-  else if (rpt <= 2) k_lu_panel<W, 2><<<nb.count, 512, 0, st>>>(nb, c0);
-  else if constexpr (W <= 8) {  // registers: RPT x W doubles per thread
-    if (rpt <= 3) k_lu_panel<W, 3><<<nb.count, 512, 0, st>>>(nb, c0);
-    else k_lu_panel<W, 4><<<nb.count, 512, 0, st>>>(nb, c0);
+  // 256 threads x (up to 3 rows x 16 columns) in registers up to 768 rows;
+  // 512 threads beyond
+  if (W == 16 && rows <= 256) launch_panel<W, 1, 256>(nb, c0, st);
+  else if (W == 16 && rows <= 512) launch_panel<W, 2, 256>(nb, c0, st);
+  else if (W == 16 && rows <= 768) launch_panel<W, 3, 256>(nb, c0, st);
+  else if (rows <= 1024) launch_panel<W, 2, 512>(nb, c0, st);
+  else if constexpr (W <= 8) {
+    if (rows <= 1536) launch_panel<W, 3, 512>(nb, c0, st);
+    else launch_panel<W, 4, 512>(nb, c0, st);
   }
 }
 

@@ -25,6 +25,8 @@ cudaError_t dispatch(const GemmArgs& g, cudaStream_t st) {
   // Large output tiles when there is enough work to fill the 148 SMs with
   // them; otherwise narrower tiles (N <= 64 panels, small per-node blocks).
   const long tiles128 = (long)((g.M + 127) / 128) * ((g.N + 127) / 128) * g.batch;
+  if (g.N <= 16) return launch<128, 16, 4, 1, TA, TB, 3>(g, st);
+  if (g.N <= 32) return launch<128, 32, 4, 1, TA, TB, 3>(g, st);
   if (g.N <= 64) {
     if (g.M >= 128 && (long)((g.M + 127) / 128) * g.batch >= 2 * 148)
       return launch<128, 64, 4, 2, TA, TB, 3>(g, st);

@@ -32,3 +32,23 @@ for (M, N, K, batch) in [(256, 256, 1024, 1024), (1280, 64, 512, 1024), (768, 64
     fl = 2.0 * M * N * K * batch
     print(f"NT {M}x{N}x{K} x{batch}: ours {fl/t/1e9:6.2f} TF/s  cublas {fl/tr/1e9:6.2f} TF/s  maxerr {err:.1e}", flush=True)
     del A, B, Cm
+# the leaf SYRK exactly as the factorization issues it: A = L21 rows inside the
+# (m+s) x m leaf trapezoid (batch stride (m+s)*m), C = H buffer indexed by node id
+R, M, S, nl = 1280, 1024, 256, 1024
+big = torch.randn(nl, R, M, dtype=torch.float64, device="cuda")
+A = big[:, M:, :]
+Hb = torch.empty(2 * nl, S, S, dtype=torch.float64, device="cuda")
+s = torch.cuda.current_stream().cuda_stream
+def run_syrk():
+    rc = lib.ks_test_gemm(S, S, M, nl, 0, A.data_ptr(), A.data_ptr(), Hb.data_ptr() + nl * S * S * 8 - 0,
+                          M, R * M, M, R * M, S, S * S, 1.0, 0.0, 0, 1, C.c_void_p(s))
+    assert rc == 0
+t = ref(run_syrk)
+print(f"leaf SYRK layout 256x256x1024 x1024: ours {2.0*S*S*M*nl/t/1e9:6.2f} TF/s")
+A2 = A.contiguous()
+def run2():
+    rc = lib.ks_test_gemm(S, S, M, nl, 0, A2.data_ptr(), A2.data_ptr(), Hb.data_ptr(), M, S * M, M, S * M, S, S * S,
+                          1.0, 0.0, 0, 1, C.c_void_p(s))
+    assert rc == 0
+t = ref(run2)
+print(f"same, contiguous A: ours {2.0*S*S*M*nl/t/1e9:6.2f} TF/s")
