@@ -267,7 +267,11 @@ def run_ours(args) -> None:
     e1.record(stream)
     torch.cuda.synchronize()
     ms_sol_q = e0.elapsed_time(e1) / 3
-    # residual check of the benchmarked solve (oracle-free, size-independent)
+    # residual of the benchmarked solve through the GPU compressed matvec
+    # (hss_matvec, compress.py:352-411): ||(K~ + lam I) u - b|| / ||b||
+    Ku = ks.hss_matvec(hf, X)
+    resid = float(torch.linalg.norm(Ku + cfg.lam * X - B1) / torch.linalg.norm(B1))
+    del Ku
     u = X.cpu().numpy()
     del X, XQ
     # e2e through the public API from pinned host memory
@@ -324,6 +328,7 @@ def run_ours(args) -> None:
         "e2e": {"value": F / (ms_e2e_fac * 1e-3) / 1e12, "unit": "TFLOP/s", "factor_ms": ms_e2e_fac,
                 "solve_ms": ms_e2e_sol, "h2d_bytes_per_step": h2d + b1.nbytes, "d2h_bytes_per_step": u2.nbytes,
                 "matches_device_run": same},
+        "residual": resid,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "producer_s": t_prod,

@@ -100,6 +100,11 @@ int ks_node_exchange(ks_factor* f, int which, int64_t node, double* dev, int64_t
 /* [shard_root, level, begin, end, s_pad, n_peers, peer node ids...]; returns length. */
 int ks_shard_info(const ks_factor* f, int64_t* out, int64_t cap);
 
+/* Y = K~ W, the compressed operator itself (hss_matvec, compress.py:352-411),
+ * n x q row-major tree order, host or device; for residual checks
+ * ||(K~ + lam I) X - B|| at any size. Needs a factorized (unsharded) handle. */
+int ks_matvec(ks_factor* f, const double* W, double* Y, int64_t q, void* stream);
+
 int ks_get_diag(const ks_factor* f, ks_diag* out);
 /* Fill up to cap (node id, Z condition estimate) pairs, ascending node id. */
 int64_t ks_get_z_cond(const ks_factor* f, int64_t* nodes, double* conds, int64_t cap);

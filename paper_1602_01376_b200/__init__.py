@@ -16,7 +16,7 @@ from .errors import (
     SingularMatrixError,
 )
 from .problem import Problem, as_problem, from_arrays, from_compressed_kernel
-from .solver import GpuHierFactor, factorize, solve, solve_many
+from .solver import GpuHierFactor, factorize, hss_matvec, solve, solve_many
 
 HierFactor = GpuHierFactor
 
@@ -34,6 +34,7 @@ __all__ = [
     "factorize",
     "from_arrays",
     "from_compressed_kernel",
+    "hss_matvec",
     "solve",
     "solve_many",
 ]

@@ -82,7 +82,7 @@ struct ks_factor {
   bool local_factored = false;
   int m_pad = 0, s_pad = 0, t_pad = 0, T = 0, R = 0, pw = 32;
   // device tables
-  DBuf<double> coords;
+  DBuf<double> coords, xx;   // coords: n + m_pad rows (zero tail), tree order
   DBuf<int> rank_d, skel_pos;
   DBuf<int64_t> skel_off, coeff_off;
   DBuf<double> coeff;
@@ -91,11 +91,18 @@ struct ks_factor {
   DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
   // solve scratch
   DBuf<double> z, c, tin, y, bdev, xdev;
+  DBuf<double> mv_c, mv_inc, mv_tot;
+  int64_t mv_q = 0;
   int64_t q_cap = 0;
   double h = 1.0;
   double lam = 0.0;
   bool factored = false;
   cudaStream_t side = nullptr, cap = nullptr;
+  // independent node groups run on their own streams so latency-bound kernels
+  // (POTRF, LU panels, TRSM) of one group overlap the GEMMs of another
+  static constexpr int kGroups = 2;
+  cudaStream_t gst[kGroups] = {};
+  cudaEvent_t gfork = nullptr, gjoin[kGroups] = {};
   cudaEvent_t ev_phase[5] = {};
   std::vector<cudaEvent_t> ev_level;
   cudaGraphExec_t graph_exec = nullptr;
@@ -170,12 +177,12 @@ struct ks_factor {
     return nb;
   }
   void release_all() {
-    coords.release(); rank_d.release(); skel_pos.release(); skel_off.release(); coeff_off.release();
+    coords.release(); xx.release(); rank_d.release(); skel_pos.release(); skel_off.release(); coeff_off.release();
     coeff.release(); leaf_node.release(); leaf_begin.release(); leaf_size.release(); leaf_info.release();
     int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
     norm1.release(); cond.release(); z.release(); c.release(); tin.release(); y.release();
-    bdev.release(); xdev.release();
+    bdev.release(); xdev.release(); mv_c.release(); mv_inc.release(); mv_tot.release();
   }
 };
 
@@ -493,10 +500,13 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
       DBuf<int64_t> pm;
       KS_CUDA(orig.alloc((size_t)p->n * p->d));
       KS_CUDA(pm.alloc((size_t)p->n));
-      KS_CUDA(f->coords.alloc((size_t)p->n * p->d));
+      KS_CUDA(f->coords.alloc((size_t)(p->n + f->m_pad) * p->d));
+      KS_CUDA(cudaMemset(f->coords.p + (size_t)p->n * p->d, 0, sizeof(double) * f->m_pad * p->d));
       KS_CUDA(cudaMemcpy(orig.p, p->coords, sizeof(double) * p->n * p->d, cudaMemcpyHostToDevice));
       KS_CUDA(cudaMemcpy(pm.p, p->perm, sizeof(int64_t) * p->n, cudaMemcpyHostToDevice));
       ks::launch_gather_rows(orig.p, pm.p, p->n, p->d, f->coords.p, nullptr);
+      KS_CUDA(f->xx.alloc((size_t)p->n + f->m_pad));
+      ks::launch_row_sqnorms(f->coords.p, p->n + f->m_pad, p->d, f->xx.p, nullptr);
       KS_CUDA(cudaDeviceSynchronize());
       orig.release();
       pm.release();
@@ -529,6 +539,9 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     KS_CUDA(f->cond.alloc(std::max(f->n_int, 1)));
     KS_CUDA(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
     KS_CUDA(cudaStreamCreateWithFlags(&f->cap, cudaStreamNonBlocking));
+    for (auto& g : f->gst) KS_CUDA(cudaStreamCreateWithFlags(&g, cudaStreamNonBlocking));
+    KS_CUDA(cudaEventCreateWithFlags(&f->gfork, cudaEventDisableTiming));
+    for (auto& e : f->gjoin) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : f->ev_phase) KS_CUDA(cudaEventCreate(&e));
     f->ev_level.resize(f->levels.size());
     for (auto& e : f->ev_level) KS_CUDA(cudaEventCreate(&e));
@@ -556,6 +569,56 @@ int ks_create_shard(const ks_problem* p, int device, int64_t shard_root, ks_fact
 // Enqueue the whole factorization on `st` (no host synchronization inside, so
 // the sequence can be captured into a CUDA graph). Leaf Cholesky failures are
 // recorded on the device and handled by the caller afterwards.
+// Leaves [l0, l1): left-looking Cholesky of the (m+s) x m trapezoids in 64-column
+// panels (panel update GEMM, 64x64 POTRF + inverse, panel TRSM as GEMM with the
+// inverse), then H = L21 L21^T (solver.py:123-135).
+static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
+  const ks::LeafBatch all = f->leafbatch();
+  ks::LeafBatch lb = all;
+  lb.count = l1 - l0;
+  lb.node = all.node + l0;
+  lb.begin = all.begin + l0;
+  lb.size = all.size + l0;
+  lb.A = all.A + (int64_t)l0 * all.a_stride;
+  const int nl = lb.count;
+  const int M = f->m_pad, S = f->s_pad, R = f->R;
+  const int64_t AS = lb.a_stride;
+  double* leafA = lb.A;
+  double* inv = f->inv.p + (int64_t)l0 * 64 * 64;
+  int* info = f->leaf_info.p + l0;
+  cudaStream_t st = L.st;
+  for (int j0 = 0; j0 < M; j0 += 64) {
+    if (j0 > 0) {
+      Operand A{leafA + (int64_t)j0 * M, M, AS, nullptr};
+      Operand B{leafA + (int64_t)j0 * M, M, AS, nullptr};
+      OperandW C{leafA + (int64_t)j0 * M + j0, M, AS, nullptr};
+      int rc = L.gemm(mk(R - j0, 64, j0, nl, A, B, C, -1.0, 1.0), false, true);
+      if (rc) return rc;
+    }
+    ks::launch_potrf64(lb, j0, inv, info, st);
+    ++L.count[0];
+    if (int rc = L.check("potrf64")) return rc;
+    if (R - j0 - 64 > 0) {
+      Operand A{leafA + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
+      Operand B{inv, 64, 64 * 64, nullptr};
+      OperandW C{leafA + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
+      int rc = L.gemm(mk(R - j0 - 64, 64, 64, nl, A, B, C, 1.0, 0.0), false, true);
+      if (rc) return rc;
+    }
+  }
+  if (S > 0 && f->n_int > 0) {
+    Operand A{leafA + (int64_t)M * M, M, AS, nullptr};
+    OperandW C{f->hbuf.p, S, (int64_t)S * S, lb.node};
+    int rc = L.gemm(mk(S, S, M, nl, A, A, C, 1.0, 0.0), false, true);
+    if (rc) return rc;
+    ks::launch_sym_h(f->hbuf.p, (int64_t)S * S, lb.node, nl, S, st);
+    ++L.count[0];
+    if (int rc = L.check("sym_h")) return rc;
+  }
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
 static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1);
 
 static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
@@ -574,45 +637,45 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   if (f->n_int) KS_CUDA(cudaMemsetAsync(f->int_info.p, 0, sizeof(int) * f->n_int, st));
   // ---- leaves: assemble [[K + lam I], [P]] ----
   if (int rc = L.check("start")) return rc;
-  ks::launch_leaf_assemble(dt, lb, f->lam_dev.p, st);
-  L.count[0] += 2;
+  if ((f->d & 1) == 0) {
+    // K(X_leaf, X_leaf) + lam I as a DMMA Gram GEMM with the Gaussian epilogue
+    GemmArgs g = mk(M, M, (int)f->d, nl, Operand{f->coords.p, f->d, f->d, f->leaf_begin.p},
+                    Operand{f->coords.p, f->d, f->d, f->leaf_begin.p}, OperandW{f->leafA.p, M, lb.a_stride, nullptr},
+                    1.0, 0.0);
+    g.ge = ks::GaussEpi{f->xx.p, f->leaf_begin.p, f->leaf_size.p, f->lam_dev.p, f->h};
+    ++L.count[0];
+    cudaError_t e = ks::gemm_gauss(g, st);
+    if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf gauss gemm: %s", cudaGetErrorString(e));
+    ks::launch_leaf_copy_p(dt, lb, st);
+  } else {
+    ks::launch_leaf_assemble(dt, lb, f->lam_dev.p, st);
+  }
+  L.count[0] += 1;
   if (int rc = L.check("leaf_assemble")) return rc;
   KS_CUDA(cudaGetLastError());
   if (int rc = mark(f->ev_phase[1])) return rc;
-  // ---- left-looking Cholesky of the trapezoid, 64-column panels ----
-  const int64_t AS = lb.a_stride;
-  for (int j0 = 0; j0 < M; j0 += 64) {
-    if (j0 > 0) {
-      Operand A{f->leafA.p + (int64_t)j0 * M, M, AS, nullptr};
-      Operand B{f->leafA.p + (int64_t)j0 * M, M, AS, nullptr};
-      OperandW C{f->leafA.p + (int64_t)j0 * M + j0, M, AS, nullptr};
-      int rc = L.gemm(mk(R - j0, 64, j0, nl, A, B, C, -1.0, 1.0), false, true);
-      if (rc) return rc;
+  // ---- left-looking Cholesky of the trapezoid (64-column panels) and the
+  // SYRK H = L21 L21^T, leaves split into independent groups on their own streams
+  {
+    const int G = (nl >= 2 * 64) ? ks_factor::kGroups : 1;
+    if (G > 1) {
+      KS_CUDA(cudaEventRecord(f->gfork, st));
+      for (int g = 0; g < G; ++g) KS_CUDA(cudaStreamWaitEvent(f->gst[g], f->gfork, 0));
     }
-    ks::launch_potrf64(lb, j0, f->inv.p, f->leaf_info.p, st);
-    ++L.count[0];
-    if (int rc = L.check("potrf64")) return rc;
-    if (R - j0 - 64 > 0) {
-      Operand A{f->leafA.p + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
-      Operand B{f->inv.p, 64, 64 * 64, nullptr};
-      OperandW C{f->leafA.p + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
-      int rc = L.gemm(mk(R - j0 - 64, 64, 64, nl, A, B, C, 1.0, 0.0), false, true);
-      if (rc) return rc;
+    for (int g = 0; g < G; ++g) {
+      const int l0 = (int)((int64_t)nl * g / G), l1 = (int)((int64_t)nl * (g + 1) / G);
+      cudaStream_t gs = (G > 1) ? f->gst[g] : st;
+      Launcher Lg{f, gs, &f->launches[0]};
+      if (int rc = enqueue_leaf_chol(f, Lg, l0, l1)) return rc;
     }
+    if (G > 1)
+      for (int g = 0; g < G; ++g) {
+        KS_CUDA(cudaEventRecord(f->gjoin[g], f->gst[g]));
+        KS_CUDA(cudaStreamWaitEvent(st, f->gjoin[g], 0));
+      }
   }
   KS_CUDA(cudaGetLastError());
   if (int rc = mark(f->ev_phase[2])) return rc;
-  // ---- H = L21 L21^T for every non-root leaf ----
-  if (S > 0 && f->n_int > 0) {
-    Operand A{f->leafA.p + (int64_t)M * M, M, AS, nullptr};
-    OperandW C{f->hbuf.p, S, (int64_t)S * S, f->leaf_node.p};
-    int rc = L.gemm(mk(S, S, M, nl, A, A, C, 1.0, 0.0), false, true);
-    if (rc) return rc;
-    ks::launch_sym_h(f->hbuf.p, (int64_t)S * S, f->leaf_node.p, nl, S, st);
-    ++L.count[0];
-    if (int rc = L.check("sym_h")) return rc;
-  }
-  KS_CUDA(cudaGetLastError());
   if (int rc = mark(f->ev_phase[3])) return rc;
   // ---- the shard's internal levels, deepest first ----
   if (int rc = enqueue_levels(f, st, L, 0, f->n_local_levels)) return rc;
@@ -620,21 +683,15 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   return KS_OK;
 }
 
-// Internal levels [lev0, lev1) of the plan (deepest first), then join the
-// side stream that ran the condition estimates.
-static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1) {
+// One level's node work on L's stream for the node sub-batch nb (coupling,
+// augmented assembly, recursive LU, U12 / Schur, pivot composition, H out).
+static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool is_root_level) {
   const ks::DevTree dt = f->devtree();
   const int S = f->s_pad;
-  auto mark = [&](cudaEvent_t e) -> int {
-    if (f->profiling) KS_CUDA(cudaEventRecord(e, st));
-    return KS_OK;
-  };
   const int TP = f->t_pad, T = f->T;
   const int64_t TT = (int64_t)T * T, SS = (int64_t)S * S;
-  for (int lev = lev0; lev < lev1; ++lev) {
-    f->cur_tag = (int)lev;
-    const ks::NodeBatch nb = f->nodebatch((int)lev);
-    const int cnt = nb.count;
+  const int cnt = nb.count;
+  cudaStream_t st = L.st;
     ks::launch_coupling(dt, nb, st);
     ks::launch_aug_init(dt, nb, st);
     L.count[0] += 2;
@@ -670,17 +727,67 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
     if (rc) return rc;
     ks::launch_compose_perm(nb, st);
     ++L.count[0];
-    // condition estimate off the critical path (it only feeds diagnostics)
-    KS_CUDA(cudaEventRecord(f->ev_fork, st));
-    KS_CUDA(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
-    ks::launch_hager(dt, nb, f->side);
-    ++L.count[0];
-    const bool is_root_level = (f->levels[lev][0] == 0);
     if (!is_root_level) {
       ks::launch_extract_h(nb, f->hbuf.p, SS, st);
       ++L.count[0];
       if (int rc2 = L.check("extract_h")) return rc2;
     }
+    KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt, int T, int S, int TP) {
+  ks::NodeBatch s = nb;
+  s.count = cnt;
+  s.first = nb.first + off;
+  s.node = nb.node + off;
+  s.left = nb.left + off;
+  s.right = nb.right + off;
+  s.Aug = nb.Aug + (int64_t)off * T * T;
+  s.Bc = nb.Bc + (int64_t)off * S * S;
+  s.Pn = nb.Pn + (int64_t)off * S * TP;
+  s.piv = nb.piv + (int64_t)off * TP;
+  s.norm1 = nb.norm1 + off;
+  s.cond = nb.cond + off;
+  s.info = nb.info + off;
+  s.moves = nb.moves + (int64_t)off * (2 * 64 + 1);
+  s.pm = nb.pm + (int64_t)off * TP;
+  return s;
+}
+
+// Internal levels [lev0, lev1) of the plan (deepest first); wide levels split
+// into node groups on the group streams. Condition estimates run on the side
+// stream (they only feed diagnostics), joined at the end.
+static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1) {
+  const ks::DevTree dt = f->devtree();
+  auto mark = [&](cudaEvent_t e) -> int {
+    if (f->profiling) KS_CUDA(cudaEventRecord(e, st));
+    return KS_OK;
+  };
+  for (int lev = lev0; lev < lev1; ++lev) {
+    f->cur_tag = (int)lev;
+    const ks::NodeBatch nb = f->nodebatch((int)lev);
+    const bool is_root_level = (f->levels[lev][0] == 0);
+    const int G = (nb.count >= 64) ? ks_factor::kGroups : 1;
+    if (G == 1) {
+      if (int rc = enqueue_level_body(f, L, nb, is_root_level)) return rc;
+    } else {
+      KS_CUDA(cudaEventRecord(f->gfork, st));
+      for (int g = 0; g < G; ++g) {
+        KS_CUDA(cudaStreamWaitEvent(f->gst[g], f->gfork, 0));
+        const int o0 = (int)((int64_t)nb.count * g / G), o1 = (int)((int64_t)nb.count * (g + 1) / G);
+        Launcher Lg{f, f->gst[g], &f->launches[0]};
+        if (int rc = enqueue_level_body(f, Lg, sub_batch(nb, o0, o1 - o0, f->T, f->s_pad, f->t_pad), is_root_level))
+          return rc;
+        KS_CUDA(cudaEventRecord(f->gjoin[g], f->gst[g]));
+        KS_CUDA(cudaStreamWaitEvent(st, f->gjoin[g], 0));
+      }
+    }
+    // condition estimate off the critical path (it only feeds diagnostics)
+    KS_CUDA(cudaEventRecord(f->ev_fork, st));
+    KS_CUDA(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
+    ks::launch_hager(dt, nb, f->side);
+    ++L.count[0];
     KS_CUDA(cudaGetLastError());
     if (int rc2 = mark(f->ev_level[lev])) return rc2;
   }
@@ -1010,6 +1117,52 @@ int ks_shard_info(const ks_factor* f, int64_t* out, int64_t cap) {
   return (int)v.size();
 }
 
+// Y = K~ W, the compressed operator (hss_matvec, compress.py:352-411), on the
+// handle's resident inputs and coupling blocks (needs a factorized handle).
+int ks_matvec(ks_factor* f, const double* W, double* Y, int64_t q, void* stream) {
+  if (!f || !f->factored) return fail(KS_ERR_INVALID, "handle is not factored");
+  if (f->shard_root != 0) return fail(KS_ERR_INVALID, "matvec on a sharded handle is not supported");
+  if (q < 0) return fail(KS_ERR_INVALID, "q must be >= 0");
+  if (q == 0) return KS_OK;
+  KS_CUDA(cudaSetDevice(f->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (int rc = ensure_solve_bufs(f, q)) return rc;
+  if (q > f->mv_q) {
+    f->mv_c.release(); f->mv_inc.release(); f->mv_tot.release();
+    const size_t cnt = (size_t)std::max<int64_t>(f->n_nodes * f->s_pad * q, 1);
+    KS_CUDA(f->mv_c.alloc(cnt));
+    KS_CUDA(f->mv_inc.alloc(cnt));
+    KS_CUDA(f->mv_tot.alloc(cnt));
+    f->mv_q = q;
+  }
+  const size_t vb = (size_t)f->n_nodes * f->s_pad * q * sizeof(double);
+  KS_CUDA(cudaMemsetAsync(f->mv_c.p, 0, vb, st));
+  KS_CUDA(cudaMemsetAsync(f->mv_inc.p, 0, vb, st));
+  KS_CUDA(cudaMemsetAsync(f->mv_tot.p, 0, vb, st));
+  const bool wdev = is_device_ptr(W), ydev = is_device_ptr(Y);
+  const size_t bytes = (size_t)f->n * q * sizeof(double);
+  const double* Wd = W;
+  double* Yd = Y;
+  if (!wdev) {
+    KS_CUDA(cudaMemcpyAsync(f->bdev.p, W, bytes, cudaMemcpyHostToDevice, st));
+    Wd = f->bdev.p;
+  }
+  if (!ydev) Yd = f->xdev.p;
+  const ks::DevTree dt = f->devtree();
+  const ks::LeafBatch lb = f->leafbatch();
+  const int S = f->s_pad, nlev = (int)f->levels.size();
+  if (S > 0) ks::launch_mv_up_leaf(dt, lb, Wd, q, f->mv_c.p, S, (int)q, st);
+  for (int lev = 0; lev < nlev; ++lev) ks::launch_mv_up_node(dt, f->nodebatch(lev), f->mv_c.p, S, (int)q, st);
+  for (int lev = 0; lev < nlev; ++lev) ks::launch_mv_couple(dt, f->nodebatch(lev), f->mv_c.p, f->mv_inc.p, S, (int)q, st);
+  for (int lev = nlev - 1; lev >= 0; --lev)
+    ks::launch_mv_down(dt, f->nodebatch(lev), f->mv_inc.p, f->mv_tot.p, S, (int)q, f->levels[lev][0] != 0, st);
+  ks::launch_mv_leaf(dt, lb, Wd, q, f->mv_tot.p, Yd, S, (int)q, nlev > 0, st);
+  KS_CUDA(cudaGetLastError());
+  if (!ydev) KS_CUDA(cudaMemcpyAsync(Y, Yd, bytes, cudaMemcpyDeviceToHost, st));
+  if (!ydev || !wdev) KS_CUDA(cudaStreamSynchronize(st));
+  return KS_OK;
+}
+
 int ks_get_diag(const ks_factor* f, ks_diag* out) {
   if (!f || !out) return fail(KS_ERR_INVALID, "null argument");
   out->cholesky_fallbacks = (int64_t)f->fallback.size();
@@ -1160,6 +1313,11 @@ void ks_destroy(ks_factor* f) {
   if (f->graph_exec) cudaGraphExecDestroy(f->graph_exec);
   if (f->side) cudaStreamDestroy(f->side);
   if (f->cap) cudaStreamDestroy(f->cap);
+  for (auto g : f->gst)
+    if (g) cudaStreamDestroy(g);
+  if (f->gfork) cudaEventDestroy(f->gfork);
+  for (auto e : f->gjoin)
+    if (e) cudaEventDestroy(e);
   for (auto e : f->ev_phase)
     if (e) cudaEventDestroy(e);
   for (auto e : f->ev_level) cudaEventDestroy(e);

@@ -13,6 +13,7 @@
 // block is then H = P G Z^-1 P^T (the reference's P M P^T, M = G Z^-1).
 #include <cfloat>
 
+#include "gauss.cuh"
 #include "kernels.cuh"
 #include "trsv.cuh"
 
@@ -22,59 +23,6 @@ namespace ks {
 // Gaussian blocks. Difference form exactly as kernels.py:107-111:
 //   sq = sum_d (x_d - y_d)^2 ;  k = exp(sq / (-2 h h))
 // --------------------------------------------------------------------------
-constexpr int GT = 64;   // output tile
-constexpr int GD = 32;   // dimension chunk staged in shared memory
-
-template <bool GATHER>
-__device__ __forceinline__ void gauss_tile(const DevTree& t, const int* rows_pos, int row_base, int nrows,
-                                           const int* cols_pos, int col_base, int ncols, int r0, int c0,
-                                           double (&sq)[4][4]) {
-  __shared__ double xs[GT][GD + 1];
-  __shared__ double ys[GT][GD + 1];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) sq[i][j] = 0.0;
-  const int64_t d = t.d;
-  for (int d0 = 0; d0 < d; d0 += GD) {
-    const int dc = (int)((d - d0) < GD ? (d - d0) : GD);
-    for (int e = threadIdx.x; e < GT * GD; e += 256) {
-      const int r = e / GD, k = e % GD;
-      double xv = 0.0, yv = 0.0;
-      if (k < dc) {
-        const int rr = r0 + r, cc = c0 + r;
-        if (rr < nrows) {
-          const int64_t p = GATHER ? rows_pos[rr] : (int64_t)row_base + rr;
-          xv = t.coords[p * d + d0 + k];
-        }
-        if (cc < ncols) {
-          const int64_t p = GATHER ? cols_pos[cc] : (int64_t)col_base + cc;
-          yv = t.coords[p * d + d0 + k];
-        }
-      }
-      xs[r][k] = xv;
-      ys[r][k] = yv;
-    }
-    __syncthreads();
-    for (int k = 0; k < dc; ++k) {
-      double xv[4], yv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) xv[i] = xs[ty + 16 * i][k];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) yv[j] = ys[tx + 16 * j][k];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double df = xv[i] - yv[j];
-          sq[i][j] = fma(df, df, sq[i][j]);
-        }
-    }
-    __syncthreads();
-  }
-}
-
 // Points to tree order: dst[i] = src[perm[i]] (PartitionTree.perm, tree.py:231-234).
 __global__ void k_gather_rows(const double* src, const int64_t* perm, int64_t n, int64_t d, double* dst) {
   const int64_t total = n * d;
@@ -134,6 +82,25 @@ __global__ void k_leaf_copy_p(DevTree t, LeafBatch lb) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / lb.m_pad), j = (int)(e % lb.m_pad);
     A[e] = (i < r && j < m) ? P[(int64_t)i * m + j] : 0.0;
+  }
+}
+
+__global__ void k_row_sqnorms(const double* X, int64_t n, int64_t d, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = 0; k < d; ++k) s = fma(X[i * d + k], X[i * d + k], s);
+    out[i] = s;
+  }
+}
+
+void launch_row_sqnorms(const double* X, int64_t n, int64_t d, double* out, cudaStream_t st) {
+  k_row_sqnorms<<<1184, 128, 0, st>>>(X, n, d, out);
+}
+
+void launch_leaf_copy_p(const DevTree& t, const LeafBatch& lb, cudaStream_t st) {
+  if (lb.s_pad > 0) {
+    dim3 g2(64, lb.count);
+    k_leaf_copy_p<<<g2, 256, 0, st>>>(t, lb);
   }
 }
 

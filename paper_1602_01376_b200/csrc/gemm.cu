@@ -5,10 +5,10 @@ namespace ks {
 
 namespace {
 
-template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
+template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES, int EPI = 0>
 cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, WM, WN, TA, TB, STAGES>;
-  auto kern = k_gemm<BM, BN, WM, WN, TA, TB, STAGES>;
+  auto kern = k_gemm<BM, BN, WM, WN, TA, TB, STAGES, EPI>;
   static bool attr = false;  // per instantiation; set before first launch
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -37,6 +37,14 @@ cudaError_t dispatch(const GemmArgs& g, cudaStream_t st) {
 }
 
 }  // namespace
+
+cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st) {
+  if ((g.K & 1) || (g.A.ld & 1) || (g.C.ld & 1)) return cudaErrorInvalidValue;
+  GemmArgs t = g;
+  t.tri = 1;
+  // K = d is small and the exp epilogue dominates: small tiles, 2 stages, many warps per SM
+  return launch<64, 64, 2, 2, false, true, 2, 1>(t, st);
+}
 
 cudaError_t gemm(const GemmArgs& g, bool ta, bool tb, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;

@@ -17,12 +17,28 @@
 
 namespace ks {
 
+// Optional fused epilogues (template EPI):
+//   0  C = alpha*AB + beta*C
+//   1  Gaussian kernel block from the Gram matrix G = X X^T of a leaf
+//      (kernels.py:107-111 in GEMM form): C[r][c] = exp(max(xx_r + xx_c - 2G, 0)
+//      / (-2 h h)) for r > c, 1 + lam on the diagonal (r == c: distance exactly 0,
+//      kernel exactly 1, solver.py:124), identity on padded rows/columns
+//      (r or c >= size[b]) and 0 above the diagonal.
+struct GaussEpi {
+  const double* xx;   // squared norms of the points, tree order
+  const int* begin;   // per batch: first point of the leaf
+  const int* size;    // per batch: points in the leaf
+  const double* lam;  // device scalar
+  double h;
+};
+
 struct GemmArgs {
   int M, N, K, batch;
   Operand A, B;
   OperandW C;
   double alpha, beta;
   int tri;  // 1: skip CTA tiles strictly above the diagonal of C
+  GaussEpi ge;
 };
 
 template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
@@ -54,7 +70,7 @@ __device__ __forceinline__ void load_tile(double* dst, const double* src, int64_
   }
 }
 
-template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
+template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES, int EPI = 0>
 __global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
   using Cfg = GemmCfg<BM, BN, WM, WN, TA, TB, STAGES>;
   constexpr int BK = Cfg::BK;
@@ -132,22 +148,49 @@ __global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
   cp_async_wait<0>();
 
   const double alpha = g.alpha, beta = g.beta;
+  double den = 0.0, lam = 0.0;
+  int bsz = 0, bbeg = 0;
+  if (EPI == 1) {
+    den = 1.0 / (-2.0 * g.ge.h * g.ge.h);  // multiply by the reciprocal: one rounding in the exponent
+    lam = *g.ge.lam;
+    bsz = g.ge.size[b];
+    bbeg = g.ge.begin[b];
+  }
 #pragma unroll
   for (int i = 0; i < Cfg::MT; ++i) {
     const int r = m0 + wm0 + i * 8 + gq;
     if (r >= g.M) continue;
+    double xr = 0.0;
+    if (EPI == 1 && r < bsz) xr = g.ge.xx[bbeg + r];
 #pragma unroll
     for (int j = 0; j < Cfg::NT; ++j) {
       const int c = n0 + wn0 + j * 8 + 2 * tq;
       if (c >= g.N) continue;
       double2* p = reinterpret_cast<double2*>(C + (int64_t)r * g.C.ld + c);
       double2 v;
-      v.x = alpha * acc[i][j][0];
-      v.y = alpha * acc[i][j][1];
-      if (beta != 0.0) {
-        const double2 o = *p;
-        v.x = fma(beta, o.x, v.x);
-        v.y = fma(beta, o.y, v.y);
+      if (EPI == 1) {
+        double o[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int cc = c + u;
+          if (cc > r) o[u] = 0.0;
+          else if (r >= bsz || cc >= bsz) o[u] = (r == cc) ? 1.0 : 0.0;
+          else if (r == cc) o[u] = 1.0 + lam;
+          else {
+            const double sq = fmax(xr + g.ge.xx[bbeg + cc] - 2.0 * acc[i][j][u], 0.0);
+            o[u] = exp(sq * den);
+          }
+        }
+        v.x = o[0];
+        v.y = o[1];
+      } else {
+        v.x = alpha * acc[i][j][0];
+        v.y = alpha * acc[i][j][1];
+        if (beta != 0.0) {
+          const double2 ov = *p;
+          v.x = fma(beta, ov.x, v.x);
+          v.y = fma(beta, ov.y, v.y);
+        }
       }
       *p = v;
     }
@@ -157,5 +200,8 @@ __global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
 // Host launcher: picks a tile shape for the problem; all dims must be even,
 // leading dimensions even and base pointers 16-byte aligned.
 cudaError_t gemm(const GemmArgs& g, bool ta, bool tb, cudaStream_t st);
+// Leaf Gaussian blocks through the Gram GEMM with the EPI == 1 epilogue
+// (lower-triangular tiles only).
+cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st);
 
 }  // namespace ks

@@ -49,6 +49,8 @@ struct NodeBatch {
 
 // --- factor launchers (factor_kernels.cu) ---
 void launch_gather_rows(const double* src, const int64_t* perm, int64_t n, int64_t d, double* dst, cudaStream_t st);
+void launch_row_sqnorms(const double* X, int64_t n, int64_t d, double* out, cudaStream_t st);
+void launch_leaf_copy_p(const DevTree& t, const LeafBatch& lb, cudaStream_t st);
 void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, const double* lam, cudaStream_t st);
 void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStream_t st);
 void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st);
@@ -85,5 +87,16 @@ void launch_leaf_lu_fwd(const LeafBatch& lb, const NodeBatch& fb, const int* lea
                         int64_t ldb, const SolveBufs& sb, cudaStream_t st);
 void launch_leaf_lu_bwd(const LeafBatch& lb, const NodeBatch& fb, const int* leaf_idx, double* X,
                         int64_t ldx, const SolveBufs& sb, bool has_tin, cudaStream_t st);
+
+// --- compressed matvec (matvec_kernels.cu), hss_matvec compress.py:352-411 ---
+void launch_mv_up_leaf(const DevTree& t, const LeafBatch& lb, const double* W, int64_t ldw, double* c, int S, int q,
+                       cudaStream_t st);
+void launch_mv_up_node(const DevTree& t, const NodeBatch& nb, double* c, int S, int q, cudaStream_t st);
+void launch_mv_couple(const DevTree& t, const NodeBatch& nb, const double* c, double* inc, int S, int q,
+                      cudaStream_t st);
+void launch_mv_down(const DevTree& t, const NodeBatch& nb, const double* inc, double* tot, int S, int q, bool has_tot,
+                    cudaStream_t st);
+void launch_mv_leaf(const DevTree& t, const LeafBatch& lb, const double* W, int64_t ldw, const double* tot, double* Y,
+                    int S, int q, bool has_tot, cudaStream_t st);
 
 }  // namespace ks

@@ -234,6 +234,34 @@ def solve_many(hf: GpuHierFactor, B):
     return X
 
 
+def hss_matvec(hf: GpuHierFactor, w):
+    """K~ @ w for the factor's compressed operator (compress.py:352-411): a
+    length-n vector or an n x q matrix in tree order, numpy or CUDA torch."""
+    if _is_torch_cuda(w):
+        import torch
+
+        W = w[:, None] if w.dim() == 1 else w
+        if W.shape[0] != hf.n:
+            raise InvalidArgumentError(f"vector length {W.shape[0]} != n = {hf.n}")
+        W = W.contiguous().to(torch.float64)
+        Y = torch.empty_like(W)
+        stream = torch.cuda.current_stream(W.device).cuda_stream
+        rc = _lib.load().ks_matvec(hf.handle, C.c_void_p(W.data_ptr()), C.c_void_p(Y.data_ptr()), W.shape[1],
+                                   C.c_void_p(stream))
+        if rc:
+            _raise(rc)
+        return Y[:, 0] if w.dim() == 1 else Y
+    w = np.asarray(w, dtype=np.float64)
+    if w.shape[0] != hf.n:
+        raise InvalidArgumentError(f"vector length {w.shape[0]} != n = {hf.n}")
+    W = np.ascontiguousarray(w[:, None] if w.ndim == 1 else w)
+    Y = np.empty_like(W)
+    rc = _lib.load().ks_matvec(hf.handle, W.ctypes.data_as(C.c_void_p), Y.ctypes.data_as(C.c_void_p), W.shape[1], None)
+    if rc:
+        _raise(rc)
+    return Y[:, 0] if w.ndim == 1 else Y
+
+
 def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 

@@ -71,3 +71,20 @@ def test_multi_rhs(gpu_factors):
     U = ks.solve_many(hf, g["b3"])
     for j in range(3):
         assert rel(ks.solve(hf, g["b3"][:, j]), U[:, j]) <= 1e-14
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_hss_matvec_matches_reference_operator(gpu_factors, case):
+    """GPU K~ w against the oracle's restatement of hss_matvec, and the
+    reference round trip (K~ + lam I) u = b on the golden solution."""
+    import paper_1602_01376_b200 as ks
+    from oracle import ks_oracle as O
+    g, hf = gpu_factors(case)
+    prob = O.Problem(g)
+    w = np.random.default_rng(5).standard_normal((g["coords"].shape[0], 2))
+    y = ks.hss_matvec(hf, w)
+    y_ref = np.stack([O.hss_matvec(prob, w[:, j]) for j in range(2)], axis=1)
+    assert rel(y, y_ref) <= 1e-12, rel(y, y_ref)
+    u = g["u"]
+    r = ks.hss_matvec(hf, u) + float(g["lam"]) * u - g["b"]
+    assert np.linalg.norm(r) / np.linalg.norm(g["b"]) <= 1e-10
