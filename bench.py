@@ -309,7 +309,7 @@ def run_ours(args) -> None:
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (config-3 recipe points; reference tree restated bit-exactly; skeletons by GPU ID restatement with uniform exterior sampling)",
+        "data": "synthetic (config-3 recipe points from the reference RNG; tree restated bit-exactly; skeletons/P by a GPU restatement of the reference ID with kNN-guided sampling)",
         "config": {"workload": f"{cfg.name} factor+solve q=1", "n": cfg.n, "d": cfg.d, "leaf": cfg.leaf_size,
                    "rank": cfg.max_rank, "h": cfg.h, "lambda": cfg.lam, "q": 1,
                    "l2": "inputs larger than L2 (factor working set %.1f GB)" % (hf_keep.device_bytes() / 1e9)},

@@ -90,7 +90,7 @@ struct ks_factor {
   DBuf<int> int_node, int_left, int_right, int_info, piv, moves, pm;
   DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
   // solve scratch
-  DBuf<double> z, c, tin, y, bdev, xdev;
+  DBuf<double> z, c, tin, y, wtmp, bdev, xdev;
   DBuf<double> mv_c, mv_inc, mv_tot;
   int64_t mv_q = 0;
   int64_t q_cap = 0;
@@ -182,7 +182,7 @@ struct ks_factor {
     int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
     norm1.release(); cond.release(); z.release(); c.release(); tin.release(); y.release();
-    bdev.release(); xdev.release(); mv_c.release(); mv_inc.release(); mv_tot.release();
+    wtmp.release(); bdev.release(); xdev.release(); mv_c.release(); mv_inc.release(); mv_tot.release();
   }
 };
 
@@ -316,11 +316,13 @@ struct PhaseTimer {
 
 int ensure_solve_bufs(ks_factor* f, int64_t q) {
   if (q <= f->q_cap) return KS_OK;
-  f->z.release(); f->c.release(); f->tin.release(); f->y.release(); f->bdev.release(); f->xdev.release();
+  f->z.release(); f->c.release(); f->tin.release(); f->y.release(); f->wtmp.release(); f->bdev.release();
+  f->xdev.release();
   KS_CUDA(f->z.alloc((size_t)f->leaf_nodes.size() * f->m_pad * q));
   KS_CUDA(f->c.alloc((size_t)std::max<int64_t>(f->n_nodes * f->s_pad * q, 1)));
   KS_CUDA(f->tin.alloc((size_t)std::max<int64_t>(f->n_nodes * f->s_pad * q, 1)));
   KS_CUDA(f->y.alloc((size_t)std::max<int64_t>((int64_t)f->n_int * f->t_pad * q, 1)));
+  KS_CUDA(f->wtmp.alloc((size_t)std::max<int64_t>((int64_t)f->n_int * f->t_pad * q, 1)));
   KS_CUDA(f->bdev.alloc((size_t)f->n * q));
   KS_CUDA(f->xdev.alloc((size_t)f->n * q));
   f->q_cap = q;
@@ -530,7 +532,7 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     KS_CUDA(f->moves.alloc((size_t)std::max(f->n_int, 1) * (2 * 64 + 1)));
     KS_CUDA(f->pm.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
     KS_CUDA(f->leafA.alloc(nl * (size_t)f->R * f->m_pad));
-    KS_CUDA(f->inv.alloc(nl * 64 * 64));
+    KS_CUDA(f->inv.alloc(nl * (size_t)f->m_pad * 64));
     KS_CUDA(f->hbuf.alloc((size_t)nn * f->s_pad * f->s_pad + 1));
     KS_CUDA(f->aug.alloc((size_t)f->n_int * f->T * f->T + 1));
     KS_CUDA(f->bc.alloc((size_t)f->n_int * f->s_pad * f->s_pad + 1));
@@ -584,7 +586,7 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
   const int M = f->m_pad, S = f->s_pad, R = f->R;
   const int64_t AS = lb.a_stride;
   double* leafA = lb.A;
-  double* inv = f->inv.p + (int64_t)l0 * 64 * 64;
+  double* inv = f->inv.p + (int64_t)l0 * M * 64;
   int* info = f->leaf_info.p + l0;
   cudaStream_t st = L.st;
   for (int j0 = 0; j0 < M; j0 += 64) {
@@ -600,7 +602,7 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
     if (int rc = L.check("potrf64")) return rc;
     if (R - j0 - 64 > 0) {
       Operand A{leafA + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
-      Operand B{inv, 64, 64 * 64, nullptr};
+      Operand B{inv + (int64_t)(j0 / 64) * 64 * 64, 64, (int64_t)M * 64, nullptr};
       OperandW C{leafA + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
       int rc = L.gemm(mk(R - j0 - 64, 64, 64, nl, A, B, C, 1.0, 0.0), false, true);
       if (rc) return rc;
@@ -944,6 +946,137 @@ int ks_factorize_top(ks_factor* f, void* stream) {
   return KS_OK;
 }
 
+// ---- multi-RHS path (q >= kGemmSolveQ): factors applied as DMMA GEMMs ----
+constexpr int64_t kGemmSolveQ = 8;
+
+// op(T)^-1 B for an n x n triangle T (ld lda, batch stride sa) and B (n x ncols,
+// ld ldb, batch stride sb): recursive halves, GEMM for the off-diagonal block,
+// k_trsm_rhs at 8/16/32/64.
+static int gemm_trsm(Launcher& L, bool upper, bool unit, const double* A, int64_t lda, int64_t sa, double* B,
+                     int64_t ldb, int64_t sb, int n, int ncols, int batch) {
+  if (n == 64 || n == 32 || n == 16 || n == 8) {
+    ks::launch_trsm_rhs(n, upper, unit, A, lda, sa, B, ldb, sb, ncols, batch, L.st);
+    ++*L.count;
+    return L.check("trsm_rhs");
+  }
+  const int h = (n > 64) ? (int)roundup(n / 2, 8) : (n > 32 ? 32 : (n > 16 ? 16 : 8));
+  int rc;
+  if (!upper) {
+    if ((rc = gemm_trsm(L, upper, unit, A, lda, sa, B, ldb, sb, h, ncols, batch))) return rc;
+    rc = L.gemm(mk(n - h, ncols, h, batch, Operand{A + (int64_t)h * lda, lda, sa, nullptr}, Operand{B, ldb, sb, nullptr},
+                   OperandW{B + (int64_t)h * ldb, ldb, sb, nullptr}, -1.0, 1.0), false, false);
+    if (rc) return rc;
+    return gemm_trsm(L, upper, unit, A + (int64_t)h * lda + h, lda, sa, B + (int64_t)h * ldb, ldb, sb, n - h, ncols,
+                     batch);
+  }
+  if ((rc = gemm_trsm(L, upper, unit, A + (int64_t)h * lda + h, lda, sa, B + (int64_t)h * ldb, ldb, sb, n - h, ncols,
+                      batch)))
+    return rc;
+  rc = L.gemm(mk(h, ncols, n - h, batch, Operand{A + h, lda, sa, nullptr}, Operand{B + (int64_t)h * ldb, ldb, sb, nullptr},
+                 OperandW{B, ldb, sb, nullptr}, -1.0, 1.0), false, false);
+  if (rc) return rc;
+  return gemm_trsm(L, upper, unit, A, lda, sa, B, ldb, sb, h, ncols, batch);
+}
+
+// up pass at the leaves: z = L^-1 b (64-row blocks: GEMM update, then the block's
+// stored inverse), c = L21 z
+static int leaf_up_gemm(ks_factor* f, Launcher& L, const double* Bd, int q) {
+  const ks::LeafBatch lb = f->leafbatch();
+  const int nl = lb.count, M = f->m_pad, S = f->s_pad;
+  const int64_t AS = lb.a_stride, ZS = (int64_t)M * q;
+  ks::launch_leaf_gather(lb, Bd, q, f->z.p, q, L.st);
+  ++*L.count;
+  for (int r0 = 0; r0 < M; r0 += 64) {
+    int rc;
+    if (r0 > 0) {
+      rc = L.gemm(mk(64, q, r0, nl, Operand{f->leafA.p + (int64_t)r0 * M, M, AS, nullptr}, Operand{f->z.p, q, ZS, nullptr},
+                     OperandW{f->z.p + (int64_t)r0 * q, q, ZS, nullptr}, -1.0, 1.0), false, false);
+      if (rc) return rc;
+    }
+    rc = L.gemm(mk(64, q, 64, nl, Operand{f->inv.p + (int64_t)(r0 / 64) * 4096, 64, (int64_t)M * 64, nullptr},
+                   Operand{f->z.p + (int64_t)r0 * q, q, ZS, nullptr}, OperandW{f->z.p + (int64_t)r0 * q, q, ZS, nullptr},
+                   1.0, 0.0), false, false);
+    if (rc) return rc;
+  }
+  if (S > 0 && f->n_nodes > 1)
+    return L.gemm(mk(S, q, M, nl, Operand{f->leafA.p + (int64_t)M * M, M, AS, nullptr}, Operand{f->z.p, q, ZS, nullptr},
+                     OperandW{f->c.p, q, (int64_t)S * q, lb.node}, 1.0, 0.0), false, false);
+  return KS_OK;
+}
+
+// down pass at the leaves: x = L^-T (z - L21^T t)
+static int leaf_down_gemm(ks_factor* f, Launcher& L, double* Xd, int q) {
+  const ks::LeafBatch lb = f->leafbatch();
+  const int nl = lb.count, M = f->m_pad, S = f->s_pad;
+  const int64_t AS = lb.a_stride, ZS = (int64_t)M * q;
+  int rc;
+  if (S > 0 && f->n_nodes > 1) {
+    rc = L.gemm(mk(M, q, S, nl, Operand{f->leafA.p + (int64_t)M * M, M, AS, nullptr},
+                   Operand{f->tin.p, q, (int64_t)S * q, lb.node}, OperandW{f->z.p, q, ZS, nullptr}, -1.0, 1.0),
+                true, false);
+    if (rc) return rc;
+  }
+  for (int r0 = M - 64; r0 >= 0; r0 -= 64) {
+    if (r0 + 64 < M) {
+      rc = L.gemm(mk(64, q, M - r0 - 64, nl, Operand{f->leafA.p + (int64_t)(r0 + 64) * M + r0, M, AS, nullptr},
+                     Operand{f->z.p + (int64_t)(r0 + 64) * q, q, ZS, nullptr},
+                     OperandW{f->z.p + (int64_t)r0 * q, q, ZS, nullptr}, -1.0, 1.0), true, false);
+      if (rc) return rc;
+    }
+    rc = L.gemm(mk(64, q, 64, nl, Operand{f->inv.p + (int64_t)(r0 / 64) * 4096, 64, (int64_t)M * 64, nullptr},
+                   Operand{f->z.p + (int64_t)r0 * q, q, ZS, nullptr}, OperandW{f->z.p + (int64_t)r0 * q, q, ZS, nullptr},
+                   1.0, 0.0), true, false);
+    if (rc) return rc;
+  }
+  ks::launch_leaf_scatter(lb, f->z.p, Xd, q, q, L.st);
+  ++*L.count;
+  return KS_OK;
+}
+
+// up pass at one level: w = [B c_r; B^T c_l], y = L^-1 Pi w, c = P cc + L21aug y
+static int node_up_gemm(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool root, int q) {
+  const int S = f->s_pad, TP = f->t_pad, T = f->T, cnt = nb.count;
+  const int64_t SS = (int64_t)S * S, TT = (int64_t)T * T, CS = (int64_t)S * q, YS = (int64_t)TP * q;
+  double* w = f->wtmp.p + (int64_t)nb.first * YS;
+  double* y = f->y.p + (int64_t)nb.first * YS;
+  int rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->c.p, q, CS, nb.right},
+                     OperandW{w, q, YS, nullptr}, 1.0, 0.0), false, false);
+  if (rc) return rc;
+  rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->c.p, q, CS, nb.left},
+                 OperandW{w + (int64_t)S * q, q, YS, nullptr}, 1.0, 0.0), true, false);
+  if (rc) return rc;
+  ks::launch_permute_rows(nb, f->wtmp.p, f->y.p, q, L.st);
+  ++*L.count;
+  if ((rc = gemm_trsm(L, false, true, nb.Aug, T, TT, y, q, YS, TP, q, cnt))) return rc;
+  if (root) return KS_OK;
+  const int64_t PS = (int64_t)S * TP;
+  rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Pn, TP, PS, nullptr}, Operand{f->c.p, q, CS, nb.left},
+                 OperandW{f->c.p, q, CS, nb.node}, 1.0, 0.0), false, false);
+  if (rc) return rc;
+  rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Pn + S, TP, PS, nullptr}, Operand{f->c.p, q, CS, nb.right},
+                 OperandW{f->c.p, q, CS, nb.node}, 1.0, 1.0), false, false);
+  if (rc) return rc;
+  return L.gemm(mk(S, q, TP, cnt, Operand{nb.Aug + (int64_t)TP * T, T, TT, nullptr}, Operand{y, q, YS, nullptr},
+                   OperandW{f->c.p, q, CS, nb.node}, 1.0, 1.0), false, false);
+}
+
+// down pass at one level: u = U^-1 (y + U12aug t); children get split(u)
+static int node_down_gemm(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool root, int q) {
+  const int S = f->s_pad, TP = f->t_pad, T = f->T, cnt = nb.count;
+  const int64_t TT = (int64_t)T * T, CS = (int64_t)S * q, YS = (int64_t)TP * q;
+  double* y = f->y.p + (int64_t)nb.first * YS;
+  int rc;
+  if (!root) {
+    rc = L.gemm(mk(TP, q, S, cnt, Operand{nb.Aug + TP, T, TT, nullptr}, Operand{f->tin.p, q, CS, nb.node},
+                   OperandW{y, q, YS, nullptr}, 1.0, 1.0), false, false);
+    if (rc) return rc;
+  }
+  if ((rc = gemm_trsm(L, true, false, nb.Aug, T, TT, y, q, YS, TP, q, cnt))) return rc;
+  ks::launch_split_u(nb, f->y.p, f->tin.p, q, L.st);
+  ++*L.count;
+  return KS_OK;
+}
+
 static void trace_mark(ks_factor* f, cudaStream_t st, const char* what) {
   Launcher L{f, st, &f->launches[1]};
   L.check(what);
@@ -976,6 +1109,14 @@ static void trace_build_report(ks_factor* f) {
 // kernels index B and X by absolute tree position, so local buffers are passed
 // with a virtual base (ptr - loc_begin * q).
 static int solve_up(ks_factor* f, const double* Bd, int64_t q, cudaStream_t st) {
+  if (q >= kGemmSolveQ && (q & 1) == 0) {  // DMMA tiles need an even q
+    Launcher L{f, st, &f->launches[1]};
+    if (int rc = leaf_up_gemm(f, L, Bd, (int)q)) return rc;
+    for (int lev = 0; lev < f->n_local_levels; ++lev)
+      if (int rc = node_up_gemm(f, L, f->nodebatch(lev), f->levels[lev][0] == 0, (int)q)) return rc;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+  }
   ks::SolveBufs sb{(int)q, f->z.p, f->c.p, f->tin.p, f->y.p};
   f->cur_tag = -1;
   trace_mark(f, st, "start");
@@ -993,6 +1134,16 @@ static int solve_up(ks_factor* f, const double* Bd, int64_t q, cudaStream_t st) 
 }
 
 static int solve_top(ks_factor* f, int64_t q, cudaStream_t st) {
+  if (q >= kGemmSolveQ && (q & 1) == 0) {  // DMMA tiles need an even q
+    Launcher L{f, st, &f->launches[1]};
+    const int nlev = (int)f->levels.size();
+    for (int lev = f->n_local_levels; lev < nlev; ++lev)
+      if (int rc = node_up_gemm(f, L, f->nodebatch(lev), f->levels[lev][0] == 0, (int)q)) return rc;
+    for (int lev = nlev - 1; lev >= f->n_local_levels; --lev)
+      if (int rc = node_down_gemm(f, L, f->nodebatch(lev), f->levels[lev][0] == 0, (int)q)) return rc;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+  }
   ks::SolveBufs sb{(int)q, f->z.p, f->c.p, f->tin.p, f->y.p};
   const int nlev = (int)f->levels.size();
   for (int lev = f->n_local_levels; lev < nlev; ++lev) {
@@ -1010,6 +1161,14 @@ static int solve_top(ks_factor* f, int64_t q, cudaStream_t st) {
 }
 
 static int solve_down(ks_factor* f, double* Xd, int64_t q, cudaStream_t st) {
+  if (q >= kGemmSolveQ && (q & 1) == 0) {  // DMMA tiles need an even q
+    Launcher L{f, st, &f->launches[1]};
+    for (int lev = f->n_local_levels - 1; lev >= 0; --lev)
+      if (int rc = node_down_gemm(f, L, f->nodebatch(lev), f->levels[lev][0] == 0, (int)q)) return rc;
+    if (int rc = leaf_down_gemm(f, L, Xd, (int)q)) return rc;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+  }
   ks::SolveBufs sb{(int)q, f->z.p, f->c.p, f->tin.p, f->y.p};
   for (int lev = f->n_local_levels - 1; lev >= 0; --lev) {
     f->cur_tag = lev;

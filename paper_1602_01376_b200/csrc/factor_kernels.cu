@@ -167,7 +167,9 @@ __global__ void __launch_bounds__(256) k_potrf64(LeafBatch lb, int j0, double* i
     }
   }
   __syncthreads();
-  double* iv = inv + (int64_t)leaf * 64 * 64;
+  // every panel's inverse is kept: [leaf][panel][64][64] (the multi-RHS solve
+  // applies the diagonal blocks as GEMMs)
+  double* iv = inv + ((int64_t)leaf * (lb.m_pad / 64) + j0 / 64) * 64 * 64;
   for (int e = threadIdx.x; e < 64 * 64; e += 256) {
     const int r = e >> 6, c = e & 63;
     A[r * ld + c] = (c <= r) ? a[r][c] : 0.0;

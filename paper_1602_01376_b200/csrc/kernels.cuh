@@ -88,6 +88,14 @@ void launch_leaf_lu_fwd(const LeafBatch& lb, const NodeBatch& fb, const int* lea
 void launch_leaf_lu_bwd(const LeafBatch& lb, const NodeBatch& fb, const int* leaf_idx, double* X,
                         int64_t ldx, const SolveBufs& sb, bool has_tin, cudaStream_t st);
 
+// --- multi-RHS solve building blocks (solve_gemm.cu) ---
+void launch_trsm_rhs(int w, bool upper, bool unit, const double* A, int64_t lda, int64_t sa, double* B, int64_t ldb,
+                     int64_t sb, int ncols, int batch, cudaStream_t st);
+void launch_leaf_gather(const LeafBatch& lb, const double* B, int64_t ldb, double* Z, int q, cudaStream_t st);
+void launch_leaf_scatter(const LeafBatch& lb, const double* Z, double* X, int64_t ldx, int q, cudaStream_t st);
+void launch_permute_rows(const NodeBatch& nb, const double* W, double* Y, int q, cudaStream_t st);
+void launch_split_u(const NodeBatch& nb, const double* U, double* tin, int q, cudaStream_t st);
+
 // --- compressed matvec (matvec_kernels.cu), hss_matvec compress.py:352-411 ---
 void launch_mv_up_leaf(const DevTree& t, const LeafBatch& lb, const double* W, int64_t ldw, double* c, int S, int q,
                        cudaStream_t st);

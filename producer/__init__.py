@@ -6,7 +6,8 @@ fixtures carry the reference's own inputs at small N; at BASELINE sizes the
 GPU box has no reference, so `make_operator` rebuilds them: the points from
 the config recipe (paper_1602_01376_b200.configs), the tree with the
 bit-exact restatement in producer.tree, and skeletons/P with the batched GPU
-interpolative decomposition in producer.skeletons (uniform exterior sampling).
+interpolative decomposition in producer.skeletons, rows sampled as the
+reference does (kNN-guided exterior rows, producer.knn).
 Not part of the product path.
 """
 
@@ -21,7 +22,7 @@ from paper_1602_01376_b200.configs import Config, gen_points, gen_rhs
 from .tree import build_tree
 
 
-def make_operator(cfg: Config, device: str = "cuda", verbose: bool = False) -> dict:
+def make_operator(cfg: Config, device: str = "cuda", verbose: bool = False, sampling: str = "knn") -> dict:
     from .skeletons import skeletonize
 
     t0 = time.perf_counter()
@@ -29,7 +30,7 @@ def make_operator(cfg: Config, device: str = "cuda", verbose: bool = False) -> d
     t1 = time.perf_counter()
     tree = build_tree(coords, cfg.leaf_size)
     t2 = time.perf_counter()
-    sk = skeletonize(coords, tree, cfg.h, cfg.max_rank, cfg.tol, cfg.n_neighbors, cfg.seed, device)
+    sk = skeletonize(coords, tree, cfg.h, cfg.max_rank, cfg.tol, cfg.n_neighbors, cfg.seed, device, sampling)
     t3 = time.perf_counter()
     if verbose:
         print(f"[producer] {cfg.name}: points {t1 - t0:.1f}s tree {t2 - t1:.1f}s skeletons {t3 - t2:.1f}s "

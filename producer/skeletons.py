@@ -9,11 +9,11 @@ Per node, bottom-up, level by level (compress.py:196-228, 285-287):
   ID    = column-pivoted Householder QR truncated at tol*|R00| or s, with the
           norm-downdate recompute guard (linalg.py:39-105);
           coeff[:, piv[:r]] = I, coeff[:, piv[r:]] = R11^-1 R12.
-The one deliberate difference: rows are a seeded uniform exterior draw rather
-than neighbor-guided (sample_rows' kNN list is O(N^2) in the reference,
-tree.py:146-172); the bench states this. Operator parity with the reference is
-pinned separately on the golden fixtures, where the reference's own
-skeletons are used.
+Rows are neighbor-guided as in the reference (producer.knn: GPU kNN restating
+tree.py:146-172, sample_rows restating compress.py:145-193), or a seeded
+uniform exterior draw with sampling="uniform". Operator parity with the
+reference is pinned separately on the golden fixtures, where the reference's
+own skeletons are used.
 """
 
 from __future__ import annotations
@@ -83,7 +83,7 @@ def _cpqr_id(A: torch.Tensor, tol: float, max_rank: int):
 
 
 def skeletonize(coords: np.ndarray, tree: dict, h: float, max_rank: int, tol: float = 1e-5,
-                n_neighbors: int = 32, seed: int = 0, device: str = "cuda") -> dict:
+                n_neighbors: int = 32, seed: int = 0, device: str = "cuda", sampling: str = "knn") -> dict:
     n, d = coords.shape
     perm = tree["perm"]
     begin, end = tree["node_begin"], tree["node_end"]
@@ -96,6 +96,12 @@ def skeletonize(coords: np.ndarray, tree: dict, h: float, max_rank: int, tol: fl
     coeff: list = [None] * nn
     gen = torch.Generator(device=device)
     depth = int(level.max()) + 1
+    if sampling == "knn":
+        from .knn import knn, sample_rows
+        kappa = min(n_neighbors, n - 1)
+        nbr, dist = knn(X, kappa)
+        pos_t = torch.empty(n, dtype=torch.int64, device=device)
+        pos_t[perm_t] = torch.arange(n, device=device)
     for lev in range(depth - 1, 0, -1):  # the root has no skeleton
         nodes = [v for v in range(nn) if level[v] == lev]
         groups: dict = {}
@@ -109,11 +115,18 @@ def skeletonize(coords: np.ndarray, tree: dict, h: float, max_rank: int, tol: fl
             sizes = torch.tensor([int(end[v] - begin[v]) for v in vs], device=device)
             starts = torch.tensor([int(begin[v]) for v in vs], device=device)
             budget = min(ns, n - int(sizes.max()))
-            gen.manual_seed(seed * 1_000_003 + lev * 7919 + nc)
-            r = torch.rand(len(vs), budget, generator=gen, device=device, dtype=torch.float64)
-            r = (r * (n - sizes)[:, None].to(torch.float64)).long()
-            pos = r + (r >= starts[:, None]).long() * sizes[:, None]
-            rows = perm_t[pos]
+            if sampling == "knn":
+                rl = []
+                for v in vs:
+                    gen.manual_seed(seed * 1_000_003 + v)
+                    rl.append(sample_rows(pos_t, perm_t, int(begin[v]), int(end[v]), nbr, dist, budget, gen))
+                rows = torch.stack(rl)
+            else:
+                gen.manual_seed(seed * 1_000_003 + lev * 7919 + nc)
+                r = torch.rand(len(vs), budget, generator=gen, device=device, dtype=torch.float64)
+                r = (r * (n - sizes)[:, None].to(torch.float64)).long()
+                pos = r + (r >= starts[:, None]).long() * sizes[:, None]
+                rows = perm_t[pos]
             A = _gauss(X[rows], X[cand], h)
             R, piv, rank = _cpqr_id(A, tol, max_rank)
             for rk in torch.unique(rank).tolist():

@@ -5,7 +5,8 @@ reference cannot run at these sizes; the oracle only at the mid size):
   ||(K~ + lam I) u - b|| / ||b|| through the GPU hss_matvec, linearity in the
   right-hand side, bitwise run-to-run determinism, q-column equivalence;
 * config 2 recipe at N = 65,536 (its BASELINE size) against the CPU oracle on
-  the same producer operator.
+  the same producer operator, whose kNN-guided skeletons reproduce the
+  reference's rank profile (74-128) and Z conditioning (4.5, F4).
 """
 import numpy as np
 import pytest
@@ -40,12 +41,7 @@ def test_cfg3_residual_linearity_determinism(cfg3_full):
     X = ks.solve_many(hf, B)
     R = ks.hss_matvec(hf, X) + cfg.lam * X - B
     res = float(torch.linalg.norm(R) / torch.linalg.norm(B))
-    # the producer's operator (uniform exterior sampling) has max cond1(Z) ~3e7,
-    # against single digits for the reference's kNN-guided skeletons; the
-    # round trip loses digits in proportion (the reference's own verify uses 1e-8,
-    # report.py:133)
-    zmax = max(hf.diagnostics["z_cond"].values())
-    assert res <= max(1e-12, 1e-16 * zmax * 100), (res, zmax)
+    assert res <= 1e-12, res
     # linearity: solve(2 b0 - b1) = 2 x0 - x1
     x_lin = ks.solve(hf, 2.0 * B[:, 0] - B[:, 1])
     lin = float(torch.linalg.norm(x_lin - (2.0 * X[:, 0] - X[:, 1])) / torch.linalg.norm(X[:, 0]))
@@ -87,4 +83,6 @@ def test_cfg2_fullsize_matches_oracle():
     zc = hf.diagnostics["z_cond"]
     for v, c in of.diagnostics["z_cond"].items():
         assert abs(zc[v] / c - 1) <= 1e-6
+    ranks = op["rank"][1:]
+    assert ranks.min() >= 64 and ranks.max() == cfg.max_rank  # variable ranks exercised (F3)
     hf.close()

@@ -88,3 +88,17 @@ def test_hss_matvec_matches_reference_operator(gpu_factors, case):
     u = g["u"]
     r = ks.hss_matvec(hf, u) + float(g["lam"]) * u - g["b"]
     assert np.linalg.norm(r) / np.linalg.norm(g["b"]) <= 1e-10
+
+
+@pytest.mark.parametrize("case,q", [("cfg1", 32), ("cfg1", 9), ("ragged", 8), ("cfg2s", 32), ("cfg3s", 16)])
+def test_multi_rhs_paths_match_oracle(gpu_factors, case, q):
+    """q >= 8 (even) runs the DMMA GEMM solve path, odd q the chunked path:
+    both equal the oracle's telescoping solve column by column."""
+    import paper_1602_01376_b200 as ks
+    from oracle import ks_oracle as O
+    g, hf = gpu_factors(case)
+    B = np.random.default_rng(q).standard_normal((g["coords"].shape[0], q))
+    X = ks.solve_many(hf, B)
+    of = O.factorize(O.Problem(g), float(g["lam"]))
+    X_ref = O.solve_many_telescoping(of, B)
+    assert rel(X, X_ref) <= 1e-10, rel(X, X_ref)
