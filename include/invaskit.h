@@ -35,7 +35,7 @@ extern "C" {
 
 #define KS_OK 0
 #define KS_ERR_INVALID 1      /* InvalidArgumentError            (errors.py:13) */
-#define KS_ERR_NOT_SPD 2      /* NotSPDError (never escapes: LU fallback, solver.py:127-130) */
+#define KS_ERR_NOT_SPD 2      /* NotSPDError (not returned: non-SPD leaves take the LU fallback, solver.py:127-130) */
 #define KS_ERR_SINGULAR 3     /* SingularMatrixError             (errors.py:25, linalg.py:205-206) */
 #define KS_ERR_ILL_COND 4     /* IllConditionedError(node, cond) (errors.py:29-39, solver.py:150-152) */
 #define KS_ERR_CUDA 5         /* device / runtime failure */

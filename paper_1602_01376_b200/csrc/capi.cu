@@ -115,6 +115,33 @@ struct ks_factor {
   std::vector<int> leaf_info_h, int_info_h;
   std::vector<double> cond_h;
   std::vector<int64_t> fallback;
+  // LU fallback leaves (non-SPD leaf blocks, solver.py:125-131)
+  std::vector<int> fb_leaf;  // leaf indices
+  int fb_T = 0;
+  DBuf<double> fb_aug, fb_y, fb_norm1, fb_cond;
+  DBuf<int> fb_piv, fb_info, fb_moves, fb_pm, fb_node, fb_begin, fb_size;
+  int64_t fb_q = 0;
+  ks::NodeBatch fb_batch() const {
+    ks::NodeBatch nb{};
+    nb.count = (int)fb_leaf.size();
+    nb.first = 0;
+    nb.node = fb_node.p;
+    nb.left = fb_node.p;
+    nb.right = fb_node.p;
+    nb.s_pad = fb_T - m_pad;
+    nb.t_pad = m_pad;
+    nb.T = fb_T;
+    nb.Aug = fb_aug.p;
+    nb.Bc = nullptr;
+    nb.Pn = nullptr;
+    nb.piv = fb_piv.p;
+    nb.norm1 = fb_norm1.p;
+    nb.cond = fb_cond.p;
+    nb.info = fb_info.p;
+    nb.moves = fb_moves.p;
+    nb.pm = fb_pm.p;
+    return nb;
+  }
   // profiling
   bool profiling = false;
   double phase_ms[6] = {0, 0, 0, 0, 0, 0};
@@ -182,6 +209,8 @@ struct ks_factor {
     int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
     norm1.release(); cond.release(); z.release(); c.release(); tin.release(); y.release();
+    fb_aug.release(); fb_y.release(); fb_norm1.release(); fb_cond.release(); fb_piv.release(); fb_info.release();
+    fb_moves.release(); fb_pm.release(); fb_node.release(); fb_begin.release(); fb_size.release();
     wtmp.release(); bdev.release(); xdev.release(); mv_c.release(); mv_inc.release(); mv_tot.release();
   }
 };
@@ -814,6 +843,70 @@ static int check_nodes(ks_factor* f, int k0, int k1) {
   return KS_OK;
 }
 
+static bool force_leaf_lu() {
+  const char* e = std::getenv("KS_FORCE_LEAF_LU");  // test hook: every leaf takes the LU path
+  return e && e[0] == '1';
+}
+
+// Non-SPD leaves: LU with partial pivoting of [[A, -P^T], [P, 0]] for the
+// first m_pad pivots (dense_factor(..., "lu-partial-pivot"), solver.py:127-130);
+// the Schur complement is H = P A^-1 P^T (solver.py:134-135).
+static int factor_fallback_leaves(ks_factor* f, cudaStream_t st) {
+  const int nf = (int)f->fb_leaf.size();
+  const int M = f->m_pad;
+  const int S = (f->n_nodes > 1) ? f->s_pad : 0;
+  const int T = M + S;
+  if (nf == 0) return KS_OK;
+  if (T != f->fb_T || f->fb_node.n != (size_t)nf) {
+    f->fb_aug.release(); f->fb_piv.release(); f->fb_info.release(); f->fb_moves.release(); f->fb_pm.release();
+    f->fb_node.release(); f->fb_begin.release(); f->fb_size.release(); f->fb_norm1.release(); f->fb_cond.release();
+    f->fb_y.release();
+    f->fb_q = 0;
+    f->fb_T = T;
+    std::vector<int> nd, bg, sz;
+    for (int li : f->fb_leaf) {
+      const int v = f->leaf_nodes[li];
+      nd.push_back(v);
+      bg.push_back((int)f->begin[v]);
+      sz.push_back((int)(f->end[v] - f->begin[v]));
+    }
+    KS_CUDA(f->fb_aug.alloc((size_t)nf * T * T));
+    KS_CUDA(f->fb_piv.alloc((size_t)nf * M));
+    KS_CUDA(f->fb_info.alloc(nf));
+    KS_CUDA(f->fb_moves.alloc((size_t)nf * (2 * 64 + 1)));
+    KS_CUDA(f->fb_pm.alloc((size_t)nf * M));
+    KS_CUDA(f->fb_norm1.alloc(nf));
+    KS_CUDA(f->fb_cond.alloc(nf));
+    KS_CUDA(f->fb_node.upload(nd));
+    KS_CUDA(f->fb_begin.upload(bg));
+    KS_CUDA(f->fb_size.upload(sz));
+  }
+  const ks::NodeBatch fb = f->fb_batch();
+  Launcher L{f, st, &f->launches[0]};
+  KS_CUDA(cudaMemsetAsync(f->fb_info.p, 0, sizeof(int) * nf, st));
+  ks::launch_fb_assemble(f->devtree(), fb, f->fb_begin.p, f->fb_size.p, f->lam_dev.p, st);
+  int rc = rlu(L, fb, 0, M, T <= 1024 ? 16 : 8);
+  if (rc) return rc;
+  if (S > 0) {
+    if ((rc = trsm_ul(L, fb, 0, M, M, S))) return rc;
+    const int64_t TT = (int64_t)T * T;
+    rc = L.gemm(mk(S, S, M, nf, Operand{fb.Aug + (int64_t)M * T, T, TT, nullptr}, Operand{fb.Aug + M, T, TT, nullptr},
+                   OperandW{fb.Aug + (int64_t)M * T + M, T, TT, nullptr}, -1.0, 1.0), false, false);
+    if (rc) return rc;
+    ks::launch_extract_h(fb, f->hbuf.p, (int64_t)f->s_pad * f->s_pad, st);
+  }
+  ks::launch_compose_perm(fb, st);
+  KS_CUDA(cudaGetLastError());
+  std::vector<int> info(nf, 0);
+  KS_CUDA(cudaMemcpyAsync(info.data(), f->fb_info.p, sizeof(int) * nf, cudaMemcpyDeviceToHost, st));
+  KS_CUDA(cudaStreamSynchronize(st));
+  for (int k = 0; k < nf; ++k)
+    if (info[k])  // linalg.py:205-206 inside the fallback (solver.py:129)
+      return fail(KS_ERR_SINGULAR, "leaf %d: zero pivot column at elimination step %d", f->leaf_nodes[f->fb_leaf[k]],
+                  info[k] - 1);
+  return KS_OK;
+}
+
 static int graph_mode() {
   static int v = -1;
   if (v < 0) {
@@ -864,11 +957,24 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
   KS_CUDA(cudaMemcpyAsync(f->leaf_info_h.data(), f->leaf_info.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, st));
   KS_CUDA(cudaStreamSynchronize(st));
   f->fallback.clear();
+  std::vector<int> failed;
+  const bool force = force_leaf_lu();
   for (int i = 0; i < nl; ++i)
-    if (f->leaf_info_h[i]) f->fallback.push_back(f->leaf_nodes[i]);
-  if (!f->fallback.empty())
-    return fail(KS_ERR_NOT_SPD, "leaf %d: Cholesky hit a non-positive pivot; LU fallback not built yet",
-                (int)f->fallback[0]);
+    if (f->leaf_info_h[i] || force) {
+      f->fallback.push_back(f->leaf_nodes[i]);
+      failed.push_back(i);
+    }
+  if (failed != f->fb_leaf) {
+    f->fb_leaf = failed;
+    f->fb_T = 0;  // re-plan the fallback buffers
+  }
+  if (!failed.empty()) {
+    // LU for those leaves, then the internal levels again on the corrected H
+    if (int rc = factor_fallback_leaves(f, st)) return rc;
+    if (f->n_int) KS_CUDA(cudaMemsetAsync(f->int_info.p, 0, sizeof(int) * f->n_int, st));
+    Launcher L{f, st, &f->launches[0]};
+    if (int rc = enqueue_levels(f, st, L, 0, f->n_local_levels)) return rc;
+  }
   // ---- diagnostics and errors (solver.py:150-152, 175-188) ----
   f->int_info_h.assign(f->n_int, 0);
   f->cond_h.assign(f->n_int, 0.0);
@@ -1077,6 +1183,27 @@ static int node_down_gemm(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bo
   return KS_OK;
 }
 
+// LU-fallback leaves overwrite their Cholesky-path results (c at the leaf, x rows)
+static int fb_up(ks_factor* f, const double* Bd, int64_t q, cudaStream_t st) {
+  if (f->fb_leaf.empty()) return KS_OK;
+  if (q > f->fb_q) {
+    f->fb_y.release();
+    KS_CUDA(f->fb_y.alloc((size_t)f->fb_leaf.size() * f->m_pad * q));
+    f->fb_q = q;
+  }
+  ks::launch_fb_up(f->fb_batch(), f->fb_begin.p, f->fb_size.p, Bd, q, f->fb_y.p, f->c.p, (int)q, st);
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
+static int fb_down(ks_factor* f, double* Xd, int64_t q, cudaStream_t st) {
+  if (f->fb_leaf.empty()) return KS_OK;
+  ks::launch_fb_down(f->fb_batch(), f->fb_begin.p, f->fb_size.p, f->fb_y.p, f->tin.p, Xd, q, (int)q, f->n_nodes > 1,
+                     st);
+  KS_CUDA(cudaGetLastError());
+  return KS_OK;
+}
+
 static void trace_mark(ks_factor* f, cudaStream_t st, const char* what) {
   Launcher L{f, st, &f->launches[1]};
   L.check(what);
@@ -1112,6 +1239,7 @@ static int solve_up(ks_factor* f, const double* Bd, int64_t q, cudaStream_t st) 
   if (q >= kGemmSolveQ && (q & 1) == 0) {  // DMMA tiles need an even q
     Launcher L{f, st, &f->launches[1]};
     if (int rc = leaf_up_gemm(f, L, Bd, (int)q)) return rc;
+    if (int rc = fb_up(f, Bd, q, st)) return rc;
     for (int lev = 0; lev < f->n_local_levels; ++lev)
       if (int rc = node_up_gemm(f, L, f->nodebatch(lev), f->levels[lev][0] == 0, (int)q)) return rc;
     KS_CUDA(cudaGetLastError());
@@ -1121,6 +1249,7 @@ static int solve_up(ks_factor* f, const double* Bd, int64_t q, cudaStream_t st) 
   f->cur_tag = -1;
   trace_mark(f, st, "start");
   ks::launch_leaf_fwd(f->leafbatch(), Bd, q, sb, st);
+  if (int rc = fb_up(f, Bd, q, st)) return rc;
   ++f->launches[1];
   trace_mark(f, st, "leaf_fwd");
   for (int lev = 0; lev < f->n_local_levels; ++lev) {
@@ -1166,6 +1295,7 @@ static int solve_down(ks_factor* f, double* Xd, int64_t q, cudaStream_t st) {
     for (int lev = f->n_local_levels - 1; lev >= 0; --lev)
       if (int rc = node_down_gemm(f, L, f->nodebatch(lev), f->levels[lev][0] == 0, (int)q)) return rc;
     if (int rc = leaf_down_gemm(f, L, Xd, (int)q)) return rc;
+    if (int rc = fb_down(f, Xd, q, st)) return rc;
     KS_CUDA(cudaGetLastError());
     return KS_OK;
   }
@@ -1178,6 +1308,7 @@ static int solve_down(ks_factor* f, double* Xd, int64_t q, cudaStream_t st) {
   }
   f->cur_tag = -1;
   ks::launch_leaf_bwd(f->leafbatch(), Xd, q, sb, f->n_nodes > 1, st);
+  if (int rc = fb_down(f, Xd, q, st)) return rc;
   ++f->launches[1];
   trace_mark(f, st, "leaf_bwd");
   KS_CUDA(cudaGetLastError());

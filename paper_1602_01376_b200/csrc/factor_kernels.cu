@@ -690,6 +690,61 @@ void launch_hager(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
   k_hager<<<nb.count, STHREADS, smem, st>>>(t, nb);
 }
 
+// LU fallback for leaves whose Cholesky failed (solver.py:125-131): the
+// augmented matrix [[A, -P^T], [P, 0]], A = K(X_leaf, X_leaf) + lam I (both
+// triangles), with the leaf's padded identity; its LU restricted to the first
+// m_pad pivots leaves the Schur complement P A^-1 P^T = H in the trailing block.
+// fb: count = failed leaves, node = their node ids, t_pad = m_pad, T = m_pad + s_pad.
+__global__ void __launch_bounds__(256) k_fb_assemble(DevTree t, NodeBatch fb, const int* begin, const int* size,
+                                                     const double* lam_p) {
+  const int k = blockIdx.z;
+  const int v = fb.node[k], b0 = begin[k], m = size[k];
+  const int TP = fb.t_pad, T = fb.T, S = T - TP;
+  double* A = fb.Aug + (int64_t)k * T * T;
+  const int r0 = blockIdx.y * GT, c0 = blockIdx.x * GT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  if (r0 < TP && c0 < TP) {
+    double sq[4][4];
+    gauss_tile<false>(t, nullptr, b0, m, nullptr, b0, m, r0, c0, sq);
+    const double den = -2.0 * t.h * t.h, lam = *lam_p;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = r0 + ty + 16 * i, c = c0 + tx + 16 * j;
+        double val;
+        if (r >= m || c >= m) val = (r == c) ? 1.0 : 0.0;
+        else val = exp(sq[i][j] / den) + (r == c ? lam : 0.0);
+        A[(int64_t)r * T + c] = val;
+      }
+    return;
+  }
+  // P blocks: rows TP.. = P (cols < TP), cols TP.. = -P^T (rows < TP), zero corner
+  const int rank = t.rank[v];
+  const double* P = t.coeff + t.coeff_off[v];
+  for (int e = threadIdx.x; e < GT * GT; e += 256) {
+    const int r = r0 + e / GT, c = c0 + e % GT;
+    if (r >= T || c >= T) continue;
+    double val = 0.0;
+    if (r >= TP && c < TP) {
+      const int i = r - TP;
+      val = (i < rank && c < m) ? P[(int64_t)i * m + c] : 0.0;
+    } else if (r < TP && c >= TP) {
+      const int i = c - TP;
+      val = (i < rank && r < m) ? -P[(int64_t)i * m + r] : 0.0;
+    }
+    A[(int64_t)r * T + c] = val;
+  }
+  (void)S;
+}
+
+void launch_fb_assemble(const DevTree& t, const NodeBatch& fb, const int* begin, const int* size, const double* lam,
+                        cudaStream_t st) {
+  const int nt = (fb.T + GT - 1) / GT;
+  dim3 g(nt, nt, fb.count);
+  k_fb_assemble<<<g, 256, 0, st>>>(t, fb, begin, size, lam);
+}
+
 // Composed row interchanges of each node's LU: (Pi v)[i] = v[pm[i]], from the
 // LAPACK-style swap sequence (linalg.py:250-253). One warp per node.
 __global__ void k_compose_perm(NodeBatch nb) {

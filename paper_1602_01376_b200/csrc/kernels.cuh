@@ -63,6 +63,12 @@ void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncol
 void launch_hager(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
 void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st);
 void launch_compose_perm(const NodeBatch& nb, cudaStream_t st);
+void launch_fb_assemble(const DevTree& t, const NodeBatch& fb, const int* begin, const int* size, const double* lam,
+                        cudaStream_t st);
+void launch_fb_up(const NodeBatch& fb, const int* begin, const int* size, const double* B, int64_t ldb, double* Y,
+                  double* c, int q, cudaStream_t st);
+void launch_fb_down(const NodeBatch& fb, const int* begin, const int* size, const double* Y, const double* tin,
+                    double* X, int64_t ldx, int q, bool has_tin, cudaStream_t st);
 // leaf LU fallback (NotSPD leaves): augmented [[A, P^T], [-P, 0]]
 void launch_leaf_aug_init(const DevTree& t, const LeafBatch& lb, const NodeBatch& fb, double lam,
                           cudaStream_t st);

@@ -216,6 +216,89 @@ void launch_leaf_bwd(const LeafBatch& lb, double* X, int64_t ldx, const SolveBuf
   });
 }
 
+// ---------------------------------------------------------------------------
+// LU-fallback leaves (augmented [[A, -P^T], [P, 0]] factors, see k_fb_assemble):
+//   up   y = L^-1 Pi b_leaf,  c = L21aug y           (= P A^-1 b)
+//   down x = U^-1 (y + U12aug t)                     (= A^-1 (b - P^T t))
+// ---------------------------------------------------------------------------
+template <int QC>
+__global__ void __launch_bounds__(STHREADS) k_fb_up(NodeBatch fb, const int* begin, const int* size, const double* B,
+                                                     int64_t ldb, double* Y, double* c, int q, int q0) {
+  extern __shared__ double sm[];
+  const int TP = fb.t_pad, T = fb.T, S = T - TP;
+  double* w = sm;            // TP x QC
+  double* x = sm + TP * QC;  // TP x QC
+  __shared__ double D[SB][SB + 1];
+  const int k = blockIdx.x;
+  const int b0 = begin[k], m = size[k], v = fb.node[k];
+  for (int e = threadIdx.x; e < TP * QC; e += STHREADS) {
+    const int r = e / QC;
+    w[e] = (r < m) ? B[(int64_t)(b0 + r) * ldb + q0 + e % QC] : 0.0;
+  }
+  __syncthreads();
+  const int* pm = fb.pm + (int64_t)k * TP;
+  for (int e = threadIdx.x; e < TP * QC; e += STHREADS) x[e] = w[pm[e / QC] * QC + e % QC];
+  __syncthreads();
+  const double* A = fb.Aug + (int64_t)k * T * T;
+  cta_trsv_rows<QC, false, true>(A, T, TP, x, D);
+  double* y = Y + (int64_t)k * TP * q;
+  for (int e = threadIdx.x; e < TP * QC; e += STHREADS) y[(e / QC) * q + q0 + e % QC] = x[e];
+  if (S > 0) cta_gemv_rows<QC>(A + (int64_t)TP * T, T, S, TP, x, c + (int64_t)v * S * q + q0, q, false);
+}
+
+template <int QC>
+__global__ void __launch_bounds__(STHREADS) k_fb_down(NodeBatch fb, const int* begin, const int* size, const double* Y,
+                                                       const double* tin, double* X, int64_t ldx, int q, int q0,
+                                                       int has_tin) {
+  extern __shared__ double sm[];
+  const int TP = fb.t_pad, T = fb.T, S = T - TP;
+  double* u = sm;            // TP x QC
+  double* tv = sm + TP * QC;  // S x QC
+  __shared__ double D[SB][SB + 1];
+  const int k = blockIdx.x;
+  const int b0 = begin[k], m = size[k], v = fb.node[k];
+  const double* y = Y + (int64_t)k * TP * q;
+  for (int e = threadIdx.x; e < TP * QC; e += STHREADS) u[e] = y[(e / QC) * q + q0 + e % QC];
+  if (has_tin)
+    for (int e = threadIdx.x; e < S * QC; e += STHREADS) tv[e] = tin[((int64_t)v * S + e / QC) * q + q0 + e % QC];
+  __syncthreads();
+  const double* A = fb.Aug + (int64_t)k * T * T;
+  if (has_tin && S > 0) {
+    cta_gemv_rows<QC>(A + TP, T, TP, S, tv, u, QC, true);
+    __syncthreads();
+  }
+  cta_trsv_rows<QC, true, false>(A, T, TP, u, D);
+  for (int e = threadIdx.x; e < m * QC; e += STHREADS) X[(int64_t)(b0 + e / QC) * ldx + q0 + e % QC] = u[e];
+}
+
+void launch_fb_up(const NodeBatch& fb, const int* begin, const int* size, const double* B, int64_t ldb, double* Y,
+                  double* c, int q, cudaStream_t st) {
+  for_chunks(q, [&](int q0, int qc) {
+    const size_t smem = (size_t)2 * fb.t_pad * qc * sizeof(double);
+#define KS_CASE(QC)                                                                             \
+  if (qc == QC) {                                                                               \
+    set_smem(k_fb_up<QC>, smem);                                                                \
+    k_fb_up<QC><<<fb.count, STHREADS, smem, st>>>(fb, begin, size, B, ldb, Y, c, q, q0);        \
+  }
+    KS_CASE(1) KS_CASE(2) KS_CASE(4)
+#undef KS_CASE
+  });
+}
+
+void launch_fb_down(const NodeBatch& fb, const int* begin, const int* size, const double* Y, const double* tin,
+                    double* X, int64_t ldx, int q, bool has_tin, cudaStream_t st) {
+  for_chunks(q, [&](int q0, int qc) {
+    const size_t smem = ((size_t)fb.t_pad + (fb.T - fb.t_pad)) * qc * sizeof(double);
+#define KS_CASE(QC)                                                                                          \
+  if (qc == QC) {                                                                                            \
+    set_smem(k_fb_down<QC>, smem);                                                                           \
+    k_fb_down<QC><<<fb.count, STHREADS, smem, st>>>(fb, begin, size, Y, tin, X, ldx, q, q0, has_tin ? 1 : 0); \
+  }
+    KS_CASE(1) KS_CASE(2) KS_CASE(4)
+#undef KS_CASE
+  });
+}
+
 // Levels with many nodes keep one CTA per node (enough CTAs to saturate HBM);
 // levels with few nodes use an 8-CTA cluster per node (solve_cluster.cu).
 constexpr int kClusterMaxNodes = 128;

@@ -102,3 +102,29 @@ def test_multi_rhs_paths_match_oracle(gpu_factors, case, q):
     of = O.factorize(O.Problem(g), float(g["lam"]))
     X_ref = O.solve_many_telescoping(of, B)
     assert rel(X, X_ref) <= 1e-10, rel(X, X_ref)
+
+
+@pytest.mark.parametrize("case", ["cfg1", "ragged", "single", "cfg3s", "cfg5s"])
+def test_leaf_lu_fallback_path(golden, case, monkeypatch):
+    """The Cholesky -> LU fallback (solver.py:125-131) forced on every leaf
+    (KS_FORCE_LEAF_LU=1): the LU path yields the same H, solution and
+    diagnostics as the reference (which used Cholesky on these SPD blocks),
+    with every leaf listed in diagnostics['fallback_nodes']."""
+    import paper_1602_01376_b200 as ks
+    g = golden(case)
+    monkeypatch.setenv("KS_FORCE_LEAF_LU", "1")
+    hf = ks.factorize(g, float(g["lam"]))
+    monkeypatch.delenv("KS_FORCE_LEAF_LU")
+    leaves = [v for v in range(g["node_begin"].size) if g["node_left"][v] < 0]
+    assert hf.diagnostics["fallback_nodes"] == leaves
+    assert hf.diagnostics["cholesky_fallbacks"] == len(leaves)
+    u = ks.solve_many(hf, g["b"])
+    assert rel(u, g["u"]) <= TOL.get(case, 1e-10), rel(u, g["u"])
+    for i, v in enumerate(g["H_nodes"]):
+        H = g["H"][g["H_off"][i]:g["H_off"][i + 1]]
+        assert rel(hf.node_h(int(v)).ravel(), H) <= 1e-11, int(v)
+    B = np.random.default_rng(1).standard_normal((g["coords"].shape[0], 8))
+    from oracle import ks_oracle as O
+    X_ref = O.solve_many_telescoping(O.factorize(O.Problem(g), float(g["lam"])), B)
+    assert rel(ks.solve_many(hf, B), X_ref) <= 1e-10
+    hf.close()
