@@ -137,11 +137,17 @@ int64_t ks_last_launches(const ks_factor* f, int which /* 0 factor, 1 solve */);
  * (m_pad, s_pad, t_pad, T, R, q_cap, n_internal, n_leaves). */
 int ks_debug_copy(const ks_factor* f, int which, int64_t index, double* out, int64_t count);
 int ks_debug_layout(const ks_factor* f, int64_t* out8);
+/* Raw device address of an internal buffer (ids as ks_debug_copy; 6 = H), probes only. */
+int64_t ks_debug_ptr(const ks_factor* f, int which);
 
 /* Test hook: the library's batched DMMA GEMM on strided device batches. */
 int ks_test_gemm(int M, int N, int K, int batch, int tri, const double* A, const double* B, double* C,
                  int64_t lda, int64_t sa, int64_t ldb, int64_t sb, int64_t ldc, int64_t sc, double alpha, double beta,
                  int ta, int tb, void* stream);
+
+int ks_test_gemm_cidx(int M, int N, int K, int batch, const double* A, const double* B, double* C, const int* cidx,
+                      int64_t lda, int64_t sa, int64_t ldb, int64_t sb, int64_t ldc, int64_t sc, int ta, int tb,
+                      void* stream);
 
 void ks_destroy(ks_factor* f);
 

@@ -76,8 +76,10 @@ SIGNATURES = {
     "ks_last_launches": (C.c_int64, [C.c_void_p, C.c_int]),
     "ks_debug_copy": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, _f64p, C.c_int64]),
     "ks_debug_layout": (C.c_int, [C.c_void_p, _i64p]),
+    "ks_debug_ptr": (C.c_int64, [C.c_void_p, C.c_int]),
     "ks_test_gemm": (C.c_int, [C.c_int] * 5 + [C.c_void_p] * 3 + [C.c_int64] * 6
                      + [C.c_double, C.c_double, C.c_int, C.c_int, C.c_void_p]),
+    "ks_test_gemm_cidx": (C.c_int, [C.c_int] * 4 + [C.c_void_p] * 4 + [C.c_int64] * 6 + [C.c_int, C.c_int, C.c_void_p]),
     "ks_destroy": (None, [C.c_void_p]),
     "ks_last_error": (C.c_int, [C.c_char_p, C.c_int64]),
     "ks_version": (C.c_char_p, []),

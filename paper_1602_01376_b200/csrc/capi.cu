@@ -88,6 +88,7 @@ struct ks_factor {
   DBuf<double> coeff;
   DBuf<int> leaf_node, leaf_begin, leaf_size, leaf_info;
   DBuf<int> int_node, int_left, int_right, int_info, piv, moves, pm;
+  DBuf<double> lu_scratch;
   DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
   // solve scratch
   DBuf<double> z, c, tin, y, wtmp, bdev, xdev;
@@ -140,6 +141,7 @@ struct ks_factor {
     nb.info = fb_info.p;
     nb.moves = fb_moves.p;
     nb.pm = fb_pm.p;
+    nb.scratch = nullptr;
     return nb;
   }
   // profiling
@@ -201,12 +203,13 @@ struct ks_factor {
     nb.info = int_info.p + first;
     nb.moves = moves.p + (int64_t)first * (2 * 64 + 1);
     nb.pm = pm.p + (int64_t)first * t_pad;
+    nb.scratch = lu_scratch.p + (int64_t)first * 32 * 64;
     return nb;
   }
   void release_all() {
     coords.release(); xx.release(); rank_d.release(); skel_pos.release(); skel_off.release(); coeff_off.release();
     coeff.release(); leaf_node.release(); leaf_begin.release(); leaf_size.release(); leaf_info.release();
-    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release();
+    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release(); lu_scratch.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
     norm1.release(); cond.release(); z.release(); c.release(); tin.release(); y.release();
     fb_aug.release(); fb_y.release(); fb_norm1.release(); fb_cond.release(); fb_piv.release(); fb_info.release();
@@ -271,11 +274,11 @@ struct Launcher {
     if (e != cudaSuccess) return fail(KS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
     return KS_OK;
   }
-  int gemm(const GemmArgs& g, bool ta, bool tb) {
+  int gemm(const GemmArgs& g, bool ta, bool tb, const char* name = "gemm") {
     ++*count;
     cudaError_t e = ks::gemm(g, ta, tb, st);
     if (e != cudaSuccess) return fail(KS_ERR_CUDA, "gemm %dx%dx%d: %s", g.M, g.N, g.K, cudaGetErrorString(e));
-    return check("gemm");
+    return check(name);
   }
 };
 
@@ -295,30 +298,45 @@ int trsm_ul(Launcher& L, const ks::NodeBatch& nb, int r0, int w, int c0, int nco
   Operand A{nb.Aug + (int64_t)(r0 + h) * nb.T + r0, nb.T, TT, nullptr};
   Operand B{nb.Aug + (int64_t)r0 * nb.T + c0, nb.T, TT, nullptr};
   OperandW C{nb.Aug + (int64_t)(r0 + h) * nb.T + c0, nb.T, TT, nullptr};
-  rc = L.gemm(mk(w - h, ncols, h, nb.count, A, B, C, -1.0, 1.0), false, false);
+  rc = L.gemm(mk(w - h, ncols, h, nb.count, A, B, C, -1.0, 1.0), false, false, "trsm_gemm");
   if (rc) return rc;
   return trsm_ul(L, nb, r0 + h, w - h, c0, ncols);
 }
 
+// The fused TRSM+update merge (k_lu_merge) is opt-in: measured slower than the
+// separate trsm_ul + rlu_gemm launches at config 3 (90.3 vs 86.7 ms).
+bool fused_merge_off() {
+  const char* e = std::getenv("KS_FUSED_MERGE");
+  return !(e && e[0] == '1');
+}
+
 // Recursive LU of columns [c0, c0+w) over rows [c0, T), pivots among rows < t_pad.
-int rlu(Launcher& L, const ks::NodeBatch& nb, int c0, int w, int pw) {
+int rlu(Launcher& L, const ks::NodeBatch& nb, int c0, int w, int pw, int* pend) {
   if (w <= pw) {
-    ks::launch_lu_panel(nb, c0, w, L.st);  // panel LU + its row interchanges everywhere else
+    ks::launch_lu_panel(nb, c0, w, L.st, pend);  // panel LU + its row interchanges everywhere else
+    pend[2] = 0;                                   // the pending U12 block (if any) is in place now
     *L.count += 1;
     return L.check("lu_panel");
   }
   const int h = (int)roundup(w / 2, pw);
-  int rc = rlu(L, nb, c0, h, pw);
+  int rc = rlu(L, nb, c0, h, pw, pend);
   if (rc) return rc;
+  if ((h == 16 || h == 32) && w - h <= 64 && !fused_merge_off() && nb.scratch) {
+    ks::launch_lu_merge(nb, c0, h, w, L.st);  // TRSM + trailing GEMM in one launch
+    ++*L.count;
+    if ((rc = L.check("lu_merge"))) return rc;
+    pend[0] = c0; pend[1] = c0 + h; pend[2] = h; pend[3] = w - h;  // U12 -> next panel kernel
+    return rlu(L, nb, c0 + h, w - h, pw, pend);
+  }
   rc = trsm_ul(L, nb, c0, h, c0 + h, w - h);
   if (rc) return rc;
   const int64_t TT = (int64_t)nb.T * nb.T;
   Operand A{nb.Aug + (int64_t)(c0 + h) * nb.T + c0, nb.T, TT, nullptr};
   Operand B{nb.Aug + (int64_t)c0 * nb.T + c0 + h, nb.T, TT, nullptr};
   OperandW C{nb.Aug + (int64_t)(c0 + h) * nb.T + c0 + h, nb.T, TT, nullptr};
-  rc = L.gemm(mk(nb.T - c0 - h, w - h, h, nb.count, A, B, C, -1.0, 1.0), false, false);
+  rc = L.gemm(mk(nb.T - c0 - h, w - h, h, nb.count, A, B, C, -1.0, 1.0), false, false, "rlu_gemm");
   if (rc) return rc;
-  return rlu(L, nb, c0 + h, w - h, pw);
+  return rlu(L, nb, c0 + h, w - h, pw, pend);
 }
 
 struct PhaseTimer {
@@ -560,6 +578,7 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     KS_CUDA(f->piv.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
     KS_CUDA(f->moves.alloc((size_t)std::max(f->n_int, 1) * (2 * 64 + 1)));
     KS_CUDA(f->pm.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
+    KS_CUDA(f->lu_scratch.alloc((size_t)std::max(f->n_int, 1) * 32 * 64));
     KS_CUDA(f->leafA.alloc(nl * (size_t)f->R * f->m_pad));
     KS_CUDA(f->inv.alloc(nl * (size_t)f->m_pad * 64));
     KS_CUDA(f->hbuf.alloc((size_t)nn * f->s_pad * f->s_pad + 1));
@@ -623,7 +642,7 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
       Operand A{leafA + (int64_t)j0 * M, M, AS, nullptr};
       Operand B{leafA + (int64_t)j0 * M, M, AS, nullptr};
       OperandW C{leafA + (int64_t)j0 * M + j0, M, AS, nullptr};
-      int rc = L.gemm(mk(R - j0, 64, j0, nl, A, B, C, -1.0, 1.0), false, true);
+      int rc = L.gemm(mk(R - j0, 64, j0, nl, A, B, C, -1.0, 1.0), false, true, "leaf_update");
       if (rc) return rc;
     }
     ks::launch_potrf64(lb, j0, inv, info, st);
@@ -633,16 +652,20 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
       Operand A{leafA + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
       Operand B{inv + (int64_t)(j0 / 64) * 64 * 64, 64, (int64_t)M * 64, nullptr};
       OperandW C{leafA + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
-      int rc = L.gemm(mk(R - j0 - 64, 64, 64, nl, A, B, C, 1.0, 0.0), false, true);
+      int rc = L.gemm(mk(R - j0 - 64, 64, 64, nl, A, B, C, 1.0, 0.0), false, true, "leaf_trsm");
       if (rc) return rc;
     }
   }
   if (S > 0 && f->n_int > 0) {
     Operand A{leafA + (int64_t)M * M, M, AS, nullptr};
     OperandW C{f->hbuf.p, S, (int64_t)S * S, lb.node};
-    int rc = L.gemm(mk(S, S, M, nl, A, A, C, 1.0, 0.0), false, true);
+    // SYRK: lower-triangular tiles only, then mirrored (H exactly symmetric, so
+    // the reference's 0.5 (H + H^T) is the identity on it)
+    GemmArgs g = mk(S, S, M, nl, A, A, C, 1.0, 0.0);
+    g.tri = 1;
+    int rc = L.gemm(g, false, true, "leaf_syrk");
     if (rc) return rc;
-    ks::launch_sym_h(f->hbuf.p, (int64_t)S * S, lb.node, nl, S, st);
+    ks::launch_mirror_lower(f->hbuf.p, (int64_t)S * S, lb.node, nl, S, st);
     ++L.count[0];
     if (int rc = L.check("sym_h")) return rc;
   }
@@ -651,6 +674,15 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
 }
 
 static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1);
+
+// node groups per phase (KS_GROUPS, default 2; tracing forces 1 so per-launch
+// events stay on one stream)
+static int n_groups() {
+  if (trace_on()) return 1;
+  const char* e = std::getenv("KS_GROUPS");
+  const int g = e ? std::atoi(e) : ks_factor::kGroups;
+  return std::max(1, std::min(g, ks_factor::kGroups));
+}
 
 static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   Launcher L{f, st, &f->launches[0]};
@@ -688,7 +720,7 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   // ---- left-looking Cholesky of the trapezoid (64-column panels) and the
   // SYRK H = L21 L21^T, leaves split into independent groups on their own streams
   {
-    const int G = (nl >= 2 * 64) ? ks_factor::kGroups : 1;
+    const int G = (nl >= 2 * 64) ? n_groups() : 1;
     if (G > 1) {
       KS_CUDA(cudaEventRecord(f->gfork, st));
       for (int g = 0; g < G; ++g) KS_CUDA(cudaStreamWaitEvent(f->gst[g], f->gfork, 0));
@@ -747,7 +779,8 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
     ++L.count[0];
     if (int rc2 = L.check("colnorm1")) return rc2;
     // LU of the Z columns with pivots restricted to Z's rows
-    rc = rlu(L, nb, 0, TP, f->pw);
+    int pend[4] = {0, 0, 0, 0};
+    rc = rlu(L, nb, 0, TP, f->pw, pend);
     if (rc) return rc;
     // U12 = L^-1 Pi P^T and the Schur complement H = P G Z^-1 P^T
     rc = trsm_ul(L, nb, 0, TP, TP, S);
@@ -783,6 +816,7 @@ static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt, int T,
   s.info = nb.info + off;
   s.moves = nb.moves + (int64_t)off * (2 * 64 + 1);
   s.pm = nb.pm + (int64_t)off * TP;
+  s.scratch = nb.scratch + (int64_t)off * 32 * 64;
   return s;
 }
 
@@ -799,7 +833,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
     f->cur_tag = (int)lev;
     const ks::NodeBatch nb = f->nodebatch((int)lev);
     const bool is_root_level = (f->levels[lev][0] == 0);
-    const int G = (nb.count >= 64) ? ks_factor::kGroups : 1;
+    const int G = (nb.count >= 64) ? n_groups() : 1;
     if (G == 1) {
       if (int rc = enqueue_level_body(f, L, nb, is_root_level)) return rc;
     } else {
@@ -885,7 +919,8 @@ static int factor_fallback_leaves(ks_factor* f, cudaStream_t st) {
   Launcher L{f, st, &f->launches[0]};
   KS_CUDA(cudaMemsetAsync(f->fb_info.p, 0, sizeof(int) * nf, st));
   ks::launch_fb_assemble(f->devtree(), fb, f->fb_begin.p, f->fb_size.p, f->lam_dev.p, st);
-  int rc = rlu(L, fb, 0, M, T <= 1024 ? 16 : 8);
+  int pend[4] = {0, 0, 0, 0};
+  int rc = rlu(L, fb, 0, M, T <= 1024 ? 16 : 8, pend);
   if (rc) return rc;
   if (S > 0) {
     if ((rc = trsm_ul(L, fb, 0, M, M, S))) return rc;
@@ -1535,6 +1570,22 @@ int ks_debug_copy(const ks_factor* f, int which, int64_t index, double* out, int
   return KS_OK;
 }
 
+// Raw device address of an internal buffer (same ids as ks_debug_copy), for probes.
+int64_t ks_debug_ptr(const ks_factor* f, int which) {
+  if (!f) return 0;
+  switch (which) {
+    case 0: return (int64_t)f->z.p;
+    case 1: return (int64_t)f->c.p;
+    case 2: return (int64_t)f->tin.p;
+    case 3: return (int64_t)f->y.p;
+    case 4: return (int64_t)f->aug.p;
+    case 5: return (int64_t)f->leafA.p;
+    case 6: return (int64_t)f->hbuf.p;
+    case 7: return (int64_t)f->leaf_node.p;
+    default: return 0;
+  }
+}
+
 int ks_debug_layout(const ks_factor* f, int64_t* out8) {
   if (!f || !out8) return fail(KS_ERR_INVALID, "null argument");
   out8[0] = f->m_pad; out8[1] = f->s_pad; out8[2] = f->t_pad; out8[3] = f->T;
@@ -1576,9 +1627,20 @@ int ks_get_level_ms(const ks_factor* f, double* ms, int cap) {
 int ks_test_gemm(int M, int N, int K, int batch, int tri, const double* A, const double* B, double* C,
                  int64_t lda, int64_t sa, int64_t ldb, int64_t sb, int64_t ldc, int64_t sc, double alpha, double beta,
                  int ta, int tb, void* stream) {
+  // tri >= 2 is a probe hook: C batches indexed through the int array at address (tri - 2)... not used
   ks::GemmArgs g = mk(M, N, K, batch, Operand{A, lda, sa, nullptr}, Operand{B, ldb, sb, nullptr},
                       OperandW{C, ldc, sc, nullptr}, alpha, beta);
   g.tri = tri;
+  cudaError_t e = ks::gemm(g, ta != 0, tb != 0, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(KS_ERR_CUDA, "gemm: %s", cudaGetErrorString(e));
+  return KS_OK;
+}
+
+int ks_test_gemm_cidx(int M, int N, int K, int batch, const double* A, const double* B, double* C, const int* cidx,
+                      int64_t lda, int64_t sa, int64_t ldb, int64_t sb, int64_t ldc, int64_t sc, int ta, int tb,
+                      void* stream) {
+  ks::GemmArgs g = mk(M, N, K, batch, Operand{A, lda, sa, nullptr}, Operand{B, ldb, sb, nullptr},
+                      OperandW{C, ldc, sc, cidx}, 1.0, 0.0);
   cudaError_t e = ks::gemm(g, ta != 0, tb != 0, (cudaStream_t)stream);
   if (e != cudaSuccess) return fail(KS_ERR_CUDA, "gemm: %s", cudaGetErrorString(e));
   return KS_OK;

@@ -127,55 +127,79 @@ __global__ void __launch_bounds__(256) k_potrf64(LeafBatch lb, int j0, double* i
   double(*a)[65] = reinterpret_cast<double(*)[65]>(potrf_sm);
   double(*x)[65] = reinterpret_cast<double(*)[65]>(potrf_sm + 64 * 65);
   __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  for (int e = threadIdx.x; e < 64 * 64; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    a[r][c] = (c <= r) ? A[r * ld + c] : 0.0;
+  {  // all 16 loads per thread in flight
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = threadIdx.x + u * 256, r = e >> 6, c = e & 63;
+      v[u] = (c <= r) ? A[r * ld + c] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = threadIdx.x + u * 256, r = e >> 6, c = e & 63;
+      a[r][c] = v[u];
+      x[r][c] = (r == c) ? 1.0 : 0.0;
+    }
   }
+  if (threadIdx.x == 0) bad = 0x7fffffff;
   __syncthreads();
-  for (int k = 0; k < 64; ++k) {
-    if (threadIdx.x == 0) {
-      const double p = a[k][k];
-      if (!(p > 0.0) || !isfinite(p)) {
-        if (!bad) bad = j0 + k + 1;
-        a[k][k] = 1.0;
-      } else {
-        a[k][k] = sqrt(p);
-      }
-    }
-    __syncthreads();
-    const double dk = a[k][k];
-    for (int i = k + 1 + threadIdx.x; i < 64; i += 256) a[i][k] /= dk;
-    __syncthreads();
-    // trailing update of the lower triangle: a[i][j] -= a[i][k] a[j][k], k < j <= i
-    const int rem = 63 - k;
-    for (int e = threadIdx.x; e < rem * rem; e += 256) {
-      const int i = k + 1 + e / rem, j = k + 1 + e % rem;
-      if (j <= i) a[i][j] = fma(-a[i][k], a[j][k], a[i][j]);
+  // symmetric right-looking elimination, one barrier per column:
+  //   a[i][j] -= a[i][k] a[j][k] / p_k  (k < j <= i),  p_k = a[k][k] at step k;
+  // afterwards L[k][k] = sqrt(p_k), L[i][k] = a[i][k] / sqrt(p_k)
+  // (_cholesky, linalg.py:185-196; a non-positive p_k is NotSPDError, :190-192)
+  for (int k = 0; k < 63; ++k) {
+    double p = a[k][k];
+    if (!(p > 0.0) || !isfinite(p)) p = 1.0;  // recorded below; keep the block finite
+    const double rp = 1.0 / p;
+    // 16 x 16 thread grid over the trailing lower triangle, no index division
+    const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
+    for (int i = k + 1 + ti; i < 64; i += 16) {
+      const double li = a[i][k] * rp;
+      for (int j = k + 1 + tj; j <= i; j += 16) a[i][j] = fma(-li, a[j][k], a[i][j]);
     }
     __syncthreads();
   }
-  // inverse of the lower factor, one column per thread (columns independent)
   if (threadIdx.x < 64) {
-    const int j = threadIdx.x;
-    for (int i = 0; i < 64; ++i) x[i][j] = 0.0;
-    x[j][j] = 1.0 / a[j][j];
-    for (int i = j + 1; i < 64; ++i) {
-      double s = 0.0;
-      for (int k = j; k < i; ++k) s = fma(a[i][k], x[k][j], s);
-      x[i][j] = -s / a[i][i];
-    }
+    const double p = a[threadIdx.x][threadIdx.x];
+    if (!(p > 0.0) || !isfinite(p)) atomicMin(&bad, (int)threadIdx.x);
   }
   __syncthreads();
-  // every panel's inverse is kept: [leaf][panel][64][64] (the multi-RHS solve
-  // applies the diagonal blocks as GEMMs)
+  for (int e = threadIdx.x; e < 64 * 64; e += 256) {  // scale columns (diagonal last)
+    const int r = e >> 6, c = e & 63;
+    if (c >= r) continue;
+    double p = a[c][c];
+    if (!(p > 0.0) || !isfinite(p)) p = 1.0;
+    a[r][c] = a[r][c] / sqrt(p);
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    double p = a[threadIdx.x][threadIdx.x];
+    if (!(p > 0.0) || !isfinite(p)) p = 1.0;
+    a[threadIdx.x][threadIdx.x] = sqrt(p);
+  }
+  __syncthreads();
+  // X = L^-1 right-looking: rows below k lose L[i][k] X[k] / L[k][k], then row
+  // k is scaled; one barrier per step
+  for (int k = 0; k < 64; ++k) {
+    const double rk = 1.0 / a[k][k];
+    const int cols = k + 1;
+    const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
+    for (int i = k + 1 + ti; i < 64; i += 16) {
+      const double li = a[i][k] * rk;
+      for (int j = tj; j < cols; j += 16) x[i][j] = fma(-li, x[k][j], x[i][j]);
+    }
+    __syncthreads();
+    if (threadIdx.x < cols) x[k][threadIdx.x] *= rk;
+  }
+  __syncthreads();
   double* iv = inv + ((int64_t)leaf * (lb.m_pad / 64) + j0 / 64) * 64 * 64;
+#pragma unroll 4
   for (int e = threadIdx.x; e < 64 * 64; e += 256) {
     const int r = e >> 6, c = e & 63;
     A[r * ld + c] = (c <= r) ? a[r][c] : 0.0;
     iv[e] = x[r][c];
   }
-  if (threadIdx.x == 0 && bad && info[leaf] == 0) info[leaf] = bad;
+  if (threadIdx.x == 0 && bad != 0x7fffffff && info[leaf] == 0) info[leaf] = j0 + bad + 1;
 }
 
 void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStream_t st) {
@@ -200,6 +224,22 @@ __global__ void k_sym_h(double* H, int64_t stride, const int* idx, int s) {
       h[(int64_t)j * s + i] = v;
     }
   }
+}
+
+// Upper triangle := lower triangle (SYRK computed on lower tiles only).
+__global__ void k_mirror_lower(double* H, int64_t stride, const int* idx, int s) {
+  double* h = H + (int64_t)idx[blockIdx.y] * stride;
+  const int64_t total = (int64_t)s * s;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / s), j = (int)(e % s);
+    if (j > i) h[e] = h[(int64_t)j * s + i];
+  }
+}
+
+void launch_mirror_lower(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st) {
+  if (count <= 0 || s_pad <= 0) return;
+  dim3 g(32, count);
+  k_mirror_lower<<<g, 256, 0, st>>>(H, h_stride, node_idx, s_pad);
 }
 
 void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st) {
@@ -333,11 +373,18 @@ void launch_colnorm1(const DevTree&, const NodeBatch& nb, cudaStream_t st) {
 // smallest logical position, as np.argmax does.
 // --------------------------------------------------------------------------
 template <int W, int RPT, int NT>
-__global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0) {
+__global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, int pc0, int ph, int pcols) {
   constexpr int NW = NT / 32;
   const int k = blockIdx.x;
   const int T = nb.T;
   double* A = nb.Aug + (int64_t)k * T * T;
+  if (ph > 0) {  // U12 of the preceding fused merge (k_lu_merge), disjoint from this panel
+    const double* sc = nb.scratch + (int64_t)k * 32 * 64;
+    for (int e = threadIdx.x; e < ph * pcols; e += NT) {
+      const int i = e / pcols, j = e % pcols;
+      A[(int64_t)(pr0 + i) * T + pc0 + j] = sc[i * 64 + j];
+    }
+  }
   const int rows = T - c0;
   const int plim = nb.t_pad - c0;  // eligible pivot rows: physical (= original) local rows < plim
   extern __shared__ double fin[];  // rows x W finished values (column kk written at step kk)
@@ -484,34 +531,36 @@ __global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0) {
 }
 
 template <int W, int RPT, int NT>
-static void launch_panel(const NodeBatch& nb, int c0, cudaStream_t st) {
+static void launch_panel(const NodeBatch& nb, int c0, cudaStream_t st, const int* pend) {
   const size_t smem = (size_t)(nb.T - c0) * W * sizeof(double);
   static size_t set = 0;
   if (smem > set) {
     cudaFuncSetAttribute(k_lu_panel<W, RPT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set = smem;
   }
-  k_lu_panel<W, RPT, NT><<<nb.count, NT, smem, st>>>(nb, c0);
+  k_lu_panel<W, RPT, NT><<<nb.count, NT, smem, st>>>(nb, c0, pend[0], pend[1], pend[2], pend[3]);
 }
 
 template <int W>
-static void launch_panel_w(const NodeBatch& nb, int c0, cudaStream_t st) {
+static void launch_panel_w(const NodeBatch& nb, int c0, cudaStream_t st, const int* pend) {
   const int rows = nb.T - c0;
   // 256 threads x (up to 3 rows x 16 columns) in registers up to 768 rows;
   // 512 threads beyond
-  if (W == 16 && rows <= 256) launch_panel<W, 1, 256>(nb, c0, st);
-  else if (W == 16 && rows <= 512) launch_panel<W, 2, 256>(nb, c0, st);
-  else if (W == 16 && rows <= 768) launch_panel<W, 3, 256>(nb, c0, st);
-  else if (rows <= 1024) launch_panel<W, 2, 512>(nb, c0, st);
+  if (W == 16 && rows <= 256) launch_panel<W, 1, 256>(nb, c0, st, pend);
+  else if (W == 16 && rows <= 512) launch_panel<W, 2, 256>(nb, c0, st, pend);
+  else if (W == 16 && rows <= 768) launch_panel<W, 3, 256>(nb, c0, st, pend);
+  else if (rows <= 1024) launch_panel<W, 2, 512>(nb, c0, st, pend);
   else if constexpr (W <= 8) {
-    if (rows <= 1536) launch_panel<W, 3, 512>(nb, c0, st);
-    else launch_panel<W, 4, 512>(nb, c0, st);
+    if (rows <= 1536) launch_panel<W, 3, 512>(nb, c0, st, pend);
+    else launch_panel<W, 4, 512>(nb, c0, st, pend);
   }
 }
 
-void launch_lu_panel(const NodeBatch& nb, int c0, int w, cudaStream_t st) {
-  if (w == 16) launch_panel_w<16>(nb, c0, st);
-  else launch_panel_w<8>(nb, c0, st);
+void launch_lu_panel(const NodeBatch& nb, int c0, int w, cudaStream_t st, const int* pend) {
+  static const int none[4] = {0, 0, 0, 0};
+  if (!pend) pend = none;
+  if (w == 16) launch_panel_w<16>(nb, c0, st, pend);
+  else launch_panel_w<8>(nb, c0, st, pend);
 }
 
 // Apply the panel's row interchanges (swaps[c0..c0+w)) to every column outside
@@ -778,6 +827,115 @@ __global__ void k_extract_h(NodeBatch nb, double* H, int64_t stride) {
 void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st) {
   dim3 g(32, nb.count);
   k_extract_h<<<g, 256, 0, st>>>(nb, H, h_stride);
+}
+
+}  // namespace ks
+
+namespace ks {
+
+// ---------------------------------------------------------------------------
+// Fused recursive-LU merge for a left block of width H <= 32 (rlu in capi.cu):
+//   U12 = L11^-1 A12   (L11 unit lower H x H at (c0, c0), A12 = rows [c0, c0+H),
+//                       columns [c0+H, c0+w))
+//   A22 -= L21 U12      (rows [c0+H, T), same columns)
+// One CTA per (64-column tile, 64-row tile, node): every CTA solves its U12
+// tile in shared memory (row tile 0 writes it back), then the DMMA update.
+// Replaces a TRSM launch plus a GEMM launch per merge.
+// ---------------------------------------------------------------------------
+template <int H>
+__global__ void __launch_bounds__(128) k_lu_merge(NodeBatch nb, int c0, int w) {
+  constexpr int BM = 64, BN = 64;
+  constexpr int A_LD = H + 4, B_LD = BN + 4;
+  __shared__ double Ls[H][H + 1];
+  __shared__ __align__(16) double Us[H][B_LD];
+  __shared__ __align__(16) double As[BM][A_LD];
+  const int k = blockIdx.z;
+  const int T = nb.T;
+  double* A = nb.Aug + (int64_t)k * T * T;
+  const int n0 = c0 + H + blockIdx.x * BN;  // first column of the tile
+  const int m0 = c0 + H + blockIdx.y * BM;  // first row of the A22 tile
+  const int ncol = min(BN, c0 + w - n0);
+  const int mrow = min(BM, T - m0);
+  // L21 tile (rows m0.., cols c0..c0+H) through cp.async
+  for (int e = threadIdx.x; e < BM * (H / 2); e += 128) {
+    const int r = e / (H / 2), cc = (e % (H / 2)) * 2;
+    const bool ok = r < mrow;
+    cp_async16(&As[r][cc], ok ? A + (int64_t)(m0 + r) * T + c0 + cc : A, ok ? 16 : 0);
+  }
+  cp_async_commit();
+  for (int e = threadIdx.x; e < H * H; e += 128) Ls[e / H][e % H] = A[(int64_t)(c0 + e / H) * T + c0 + e % H];
+  for (int e = threadIdx.x; e < H * BN; e += 128) {
+    const int i = e / BN, j = e % BN;
+    Us[i][j] = (j < ncol) ? A[(int64_t)(c0 + i) * T + n0 + j] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < BN) {  // forward substitution, one column per thread
+    const int j = threadIdx.x;
+    for (int i = 1; i < H; ++i) {
+      double s0 = 0.0, s1 = 0.0;
+      int kk = 0;
+      for (; kk + 1 < i; kk += 2) {
+        s0 = fma(Ls[i][kk], Us[kk][j], s0);
+        s1 = fma(Ls[i][kk + 1], Us[kk + 1][j], s1);
+      }
+      if (kk < i) s0 = fma(Ls[i][kk], Us[kk][j], s0);
+      Us[i][j] -= s0 + s1;
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // U12 cannot overwrite A12 here (other row tiles may still read A12): it goes
+  // to the node's scratch and the next panel kernel of this node copies it in
+  if (blockIdx.y == 0) {
+    double* sc = nb.scratch + (int64_t)k * 32 * 64;
+    for (int e = threadIdx.x; e < H * BN; e += 128) {
+      const int i = e / BN, j = e % BN;
+      if (j < ncol) sc[i * 64 + blockIdx.x * BN + j] = Us[i][j];
+    }
+  }
+  if (mrow <= 0) return;
+  // DMMA: 4 warps as 2 x 2, warp tile 32 x 32
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm0 = (warp >> 1) * 32, wn0 = (warp & 1) * 32;
+  const int gq = lane >> 2, tq = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < H; kk += 4) {
+    double af[4], bf[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) af[i] = As[wm0 + i * 8 + gq][kk + tq];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bf[j] = Us[kk + tq][wn0 + j * 8 + gq];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = wm0 + i * 8 + gq;
+    if (r >= mrow) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = wn0 + j * 8 + 2 * tq;
+      if (c >= ncol) continue;
+      double2* p = reinterpret_cast<double2*>(A + (int64_t)(m0 + r) * T + n0 + c);
+      double2 v = *p;
+      v.x -= acc[i][j][0];
+      v.y -= acc[i][j][1];
+      *p = v;
+    }
+  }
+}
+
+void launch_lu_merge(const NodeBatch& nb, int c0, int h, int w, cudaStream_t st) {
+  dim3 g((w - h + 63) / 64, (nb.T - c0 - h + 63) / 64, nb.count);
+  if (h == 16) k_lu_merge<16><<<g, 128, 0, st>>>(nb, c0, w);
+  else k_lu_merge<32><<<g, 128, 0, st>>>(nb, c0, w);
 }
 
 }  // namespace ks

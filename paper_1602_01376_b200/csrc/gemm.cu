@@ -1,4 +1,6 @@
 // Tile-shape selection and instantiation of the batched DMMA GEMM.
+#include <cstdlib>
+
 #include "gemm.cuh"
 
 namespace ks {
@@ -20,20 +22,40 @@ cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+static int variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("KS_GEMM_VARIANT");  // tile-shape experiments (tools/gemm_probe.py)
+    v = e ? std::atoi(e) : 0;
+  }
+  return v;
+}
+
 template <bool TA, bool TB>
 cudaError_t dispatch(const GemmArgs& g, cudaStream_t st) {
+  switch (variant()) {
+    case 1: return launch<128, 64, 2, 2, TA, TB, 3>(g, st);
+    case 2: return launch<128, 64, 4, 2, TA, TB, 4>(g, st);
+    case 3: return launch<128, 128, 2, 4, TA, TB, 4>(g, st);
+    case 4: return launch<128, 128, 4, 2, TA, TB, 3>(g, st);
+    case 5: return launch<64, 64, 2, 2, TA, TB, 4>(g, st);
+    default: break;
+  }
   // Large output tiles when there is enough work to fill the 148 SMs with
   // them; otherwise narrower tiles (N <= 64 panels, small per-node blocks).
-  const long tiles128 = (long)((g.M + 127) / 128) * ((g.N + 127) / 128) * g.batch;
+  // measured on B200 with tools/gemm_variants.py: N <= 64 panels keep 128x64
+  // tiles (8 warps, 32x32 warp tiles); wider outputs use 64x32 warp tiles
+  // (128x64 CTA tiles) when K is long and 64x64 tiles with 4 stages otherwise
   if (g.N <= 16) return launch<128, 16, 4, 1, TA, TB, 3>(g, st);
   if (g.N <= 32) return launch<128, 32, 4, 1, TA, TB, 3>(g, st);
   if (g.N <= 64) {
     if (g.M >= 128 && (long)((g.M + 127) / 128) * g.batch >= 2 * 148)
       return launch<128, 64, 4, 2, TA, TB, 3>(g, st);
-    return launch<64, 64, 2, 2, TA, TB, 3>(g, st);
+    return launch<64, 64, 2, 2, TA, TB, 4>(g, st);
   }
-  if (tiles128 >= 148) return launch<128, 128, 2, 4, TA, TB, 3>(g, st);
-  return launch<64, 64, 2, 2, TA, TB, 3>(g, st);
+  const long tiles = (long)((g.M + 127) / 128) * ((g.N + 63) / 64) * g.batch;
+  if (g.K >= 512 && tiles >= 2 * 148) return launch<128, 64, 2, 2, TA, TB, 3>(g, st);
+  return launch<64, 64, 2, 2, TA, TB, 4>(g, st);
 }
 
 }  // namespace

@@ -45,6 +45,7 @@ struct NodeBatch {
   int* info;            // count (LU: first zero pivot column + 1)
   int* moves;           // count x (1 + 2*64): rows moved by the last LU panel
   int* pm;              // count x t_pad: composed row interchanges, (Pi v)[i] = v[pm[i]]
+  double* scratch;      // count x 32 x 64: U12 of the last fused LU merge
 };
 
 // --- factor launchers (factor_kernels.cu) ---
@@ -54,15 +55,18 @@ void launch_leaf_copy_p(const DevTree& t, const LeafBatch& lb, cudaStream_t st);
 void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, const double* lam, cudaStream_t st);
 void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStream_t st);
 void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st);
+void launch_mirror_lower(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st);
 void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
 void launch_aug_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
 void launch_colnorm1(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
-void launch_lu_panel(const NodeBatch& nb, int c0, int w, cudaStream_t st);
+// pend (may be null): {row0, col0, rows, cols} of a U12 block waiting in nb.scratch
+void launch_lu_panel(const NodeBatch& nb, int c0, int w, cudaStream_t st, const int* pend = nullptr);
 void launch_lu_swap(const NodeBatch& nb, int c0, int w, cudaStream_t st);
 void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncols, cudaStream_t st);
 void launch_hager(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
 void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st);
 void launch_compose_perm(const NodeBatch& nb, cudaStream_t st);
+void launch_lu_merge(const NodeBatch& nb, int c0, int h, int w, cudaStream_t st);
 void launch_fb_assemble(const DevTree& t, const NodeBatch& fb, const int* begin, const int* size, const double* lam,
                         cudaStream_t st);
 void launch_fb_up(const NodeBatch& fb, const int* begin, const int* size, const double* B, int64_t ldb, double* Y,
