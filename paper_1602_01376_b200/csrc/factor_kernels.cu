@@ -365,16 +365,19 @@ void launch_colnorm1(const DevTree&, const NodeBatch& nb, cudaStream_t st) {
 // --------------------------------------------------------------------------
 // LU with partial pivoting restricted to rows < t_pad (linalg.py:199-213 on
 // the Z block; the -PG rows are eliminated but never chosen as pivots).
-// Base panel: W columns [c0, c0+W), rows [c0, T), staged column-major in smem.
-// Rows are never moved inside the panel: each thread owns up to RPT physical
-// rows and tracks their LOGICAL position (the row-interchange sequence of the
-// reference, swaps[k] = p), so a column step needs two barriers: one after
-// the pivot search, one after the rank-1 update. Ties in |pivot| go to the
-// smallest logical position, as np.argmax does.
+// Base panel: W columns [c0, c0+W), rows [c0, T), held in registers (each
+// thread owns up to RPT physical rows). Rows are never moved inside the panel:
+// each thread tracks its rows' LOGICAL positions (the row-interchange sequence
+// of the reference, swaps[k] = p). The column loop is fully unrolled, so the
+// finished L/U values simply stay in their registers; one barrier per column.
+// Pivot search: |v| >= 0 compares like its bit pattern, so the warp maximum is
+// three redux ops (hi word, lo word, then the smallest logical position among
+// the maxima: np.argmax's first-occurrence rule).
 // --------------------------------------------------------------------------
 template <int W, int RPT, int NT>
 __global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, int pc0, int ph, int pcols) {
   constexpr int NW = NT / 32;
+  constexpr int NONE = 0x7fffffff;
   const int k = blockIdx.x;
   const int T = nb.T;
   double* A = nb.Aug + (int64_t)k * T * T;
@@ -387,13 +390,11 @@ __global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, 
   }
   const int rows = T - c0;
   const int plim = nb.t_pad - c0;  // eligible pivot rows: physical (= original) local rows < plim
-  extern __shared__ double fin[];  // rows x W finished values (column kk written at step kk)
   // per-warp candidate pivot rows, double buffered by column parity
   __shared__ __align__(16) double cand[2][NW][W];
   __shared__ double wv[2][NW];
   __shared__ int wp[2][NW], wr[2][NW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // a[i][0] is always the current column: after each step the window rotates left
   double a[RPT][W];
   int pos[RPT];
   bool done[RPT];
@@ -412,35 +413,33 @@ __global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, 
   }
   int* info = nb.info + k;
   int* piv = nb.piv + (int64_t)k * nb.t_pad + c0;
-#pragma unroll 1
+#pragma unroll
   for (int kk = 0; kk < W; ++kk) {
     const int buf = kk & 1;
-    // 1) pivot search in registers; warp max by shuffles, ties to the smallest
-    //    logical position through a warp min-reduction (np.argmax semantics)
-    double bv = -1.0;
-    int bp = 0x7fffffff, bi = -1;
+    // 1) this thread's best eligible row (no candidate: value 0, position NONE)
+    double bv = 0.0;
+    int bp = NONE, bi = -1;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int r = threadIdx.x + i * NT;
-      if (r < plim && !done[i]) {
-        const double v = fabs(a[i][0]);
-        if (v > bv || (v == bv && pos[i] < bp)) { bv = v; bp = pos[i]; bi = i; }
-      }
+      const double v = fabs(a[i][kk]);
+      if (r < plim && !done[i] && (v > bv || (v == bv && pos[i] < bp))) { bv = v; bp = pos[i]; bi = i; }
     }
-    double wmax = bv;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-    const int wpos = (int)__reduce_min_sync(0xffffffffu, (unsigned)(bv == wmax ? bp : 0x7fffffff));
-    if (bv == wmax && bp == wpos && bi >= 0) {  // the winning lane publishes its row
+    const unsigned hi = (unsigned)__double2hiint(bv), lo = (unsigned)__double2loint(bv);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    const bool top = (hi == mh && lo == ml);
+    const int mp = (int)__reduce_min_sync(0xffffffffu, top ? (unsigned)bp : (unsigned)NONE);
+    if (top && bp == mp && bi >= 0) {  // the warp's winning lane publishes its row
 #pragma unroll
       for (int i = 0; i < RPT; ++i)
         if (i == bi) {
 #pragma unroll
-          for (int j = 0; j < W; ++j) cand[buf][warp][j] = a[i][j];
+          for (int j = kk; j < W; ++j) cand[buf][warp][j] = a[i][j];
           wr[buf][warp] = threadIdx.x + i * NT;
         }
     }
-    if (lane == 0) { wv[buf][warp] = wmax; wp[buf][warp] = wpos; }
+    if (lane == 0) { wv[buf][warp] = __hiloint2double((int)mh, (int)ml); wp[buf][warp] = mp; }
     __syncthreads();
     int ww = 0;
     bv = wv[buf][0];
@@ -457,49 +456,30 @@ __global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, 
       if (singular && *info == 0) *info = c0 + kk + 1;  // linalg.py:205-206
       piv[kk] = c0 + (singular ? kk : bp);
     }
-    double prow[W];
-#pragma unroll
-    for (int j = 0; j < W; ++j) prow[j] = singular ? (j == 0 ? 1.0 : 0.0) : cand[buf][ww][j];
-    const double rcp = 1.0 / prow[0];
+    const double p0 = singular ? 1.0 : cand[buf][ww][kk];
+    const double rcp = 1.0 / p0;
     // 2) logical swap kk <-> bp, eliminate every other remaining row (linalg.py:209-212)
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int r = threadIdx.x + i * NT;
-      if (!done[i]) {
-        bool piv_row = false;
-        if (!singular) {
-          if (r == br) { pos[i] = kk; piv_row = true; }
-          else if (pos[i] == kk) pos[i] = bp;
-        } else if (pos[i] == kk) {
-          piv_row = true;
-        }
-        if (piv_row) {  // U row: its values from column kk on are final
-          done[i] = true;
+      const bool is_piv = !done[i] && (singular ? pos[i] == kk : r == br);
+      if (!singular && !done[i]) pos[i] = (r == br) ? kk : (pos[i] == kk ? bp : pos[i]);
+      const bool keep = done[i] || is_piv;  // U rows: values from column kk on are final
+      done[i] = keep;
+      const double l = keep ? 0.0 : a[i][kk] * rcp;
+      if (!keep) a[i][kk] = l;
 #pragma unroll
-          for (int j = 0; j < W; ++j)
-            if (j < W - kk) fin[r * W + kk + j] = a[i][j];
-        } else {
-          const double l = a[i][0] * rcp;
-          fin[r * W + kk] = l;
-#pragma unroll
-          for (int j = 1; j < W; ++j) a[i][j] = fma(-l, prow[j], a[i][j]);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < W - 1; ++j) a[i][j] = a[i][j + 1];
-      a[i][W - 1] = 0.0;
+      for (int j = kk + 1; j < W; ++j) a[i][j] = fma(-l, singular ? 0.0 : cand[buf][ww][j], a[i][j]);
     }
   }
-  __syncthreads();
   // panel rows back to their logical positions
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     const int r = threadIdx.x + i * NT;
     if (r >= rows) continue;
     double2* dst = reinterpret_cast<double2*>(A + (int64_t)(c0 + pos[i]) * T + c0);
-    const double2* f2 = reinterpret_cast<const double2*>(fin + r * W);
 #pragma unroll
-    for (int j = 0; j < W / 2; ++j) dst[j] = f2[j];
+    for (int j = 0; j < W / 2; ++j) dst[j] = make_double2(a[i][2 * j], a[i][2 * j + 1]);
   }
   // the same row interchanges for every column outside the panel: at most 2W
   // rows moved; the list goes through shared memory, all loads before stores
@@ -512,33 +492,34 @@ __global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, 
     const int r = threadIdx.x + i * NT;
     if (r < rows && pos[i] != r) {
       const int slot = atomicAdd(&nmove, 1);
-      msrc[slot] = c0 + r;
-      mdst[slot] = c0 + pos[i];
+      msrc[slot] = (c0 + r) * T;
+      mdst[slot] = (c0 + pos[i]) * T;
     }
   }
   __syncthreads();
   const int nm = nmove;
-  for (int col = threadIdx.x; col < T; col += NT) {
-    if (col >= c0 && col < c0 + W) continue;
+  if (nm == 0) return;
+  int so[2 * W], sd[2 * W];
+#pragma unroll
+  for (int m = 0; m < 2 * W; ++m) {
+    so[m] = m < nm ? msrc[m] : 0;
+    sd[m] = m < nm ? mdst[m] : 0;
+  }
+  for (int col = threadIdx.x; col < T - W; col += NT) {
+    const int cc = col < c0 ? col : col + W;
     double v[2 * W];
 #pragma unroll
     for (int m = 0; m < 2 * W; ++m)
-      if (m < nm) v[m] = A[(int64_t)msrc[m] * T + col];
+      if (m < nm) v[m] = A[so[m] + cc];
 #pragma unroll
     for (int m = 0; m < 2 * W; ++m)
-      if (m < nm) A[(int64_t)mdst[m] * T + col] = v[m];
+      if (m < nm) A[sd[m] + cc] = v[m];
   }
 }
 
 template <int W, int RPT, int NT>
 static void launch_panel(const NodeBatch& nb, int c0, cudaStream_t st, const int* pend) {
-  const size_t smem = (size_t)(nb.T - c0) * W * sizeof(double);
-  static size_t set = 0;
-  if (smem > set) {
-    cudaFuncSetAttribute(k_lu_panel<W, RPT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    set = smem;
-  }
-  k_lu_panel<W, RPT, NT><<<nb.count, NT, smem, st>>>(nb, c0, pend[0], pend[1], pend[2], pend[3]);
+  k_lu_panel<W, RPT, NT><<<nb.count, NT, 0, st>>>(nb, c0, pend[0], pend[1], pend[2], pend[3]);
 }
 
 template <int W>
