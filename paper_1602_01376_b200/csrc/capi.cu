@@ -89,6 +89,7 @@ struct ks_factor {
   DBuf<int> leaf_node, leaf_begin, leaf_size, leaf_info;
   DBuf<int> int_node, int_left, int_right, int_info, piv, moves, pm;
   DBuf<double> lu_scratch;
+  DBuf<double> dinv;  // condition estimator: diagonal-block inverses of every node's Z factors
   DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
   // solve scratch
   DBuf<double> z, c, tin, y, wtmp, bdev, xdev;
@@ -209,7 +210,7 @@ struct ks_factor {
   void release_all() {
     coords.release(); xx.release(); rank_d.release(); skel_pos.release(); skel_off.release(); coeff_off.release();
     coeff.release(); leaf_node.release(); leaf_begin.release(); leaf_size.release(); leaf_info.release();
-    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release(); lu_scratch.release();
+    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release(); lu_scratch.release(); dinv.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
     norm1.release(); cond.release(); z.release(); c.release(); tin.release(); y.release();
     fb_aug.release(); fb_y.release(); fb_norm1.release(); fb_cond.release(); fb_piv.release(); fb_info.release();
@@ -579,6 +580,7 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     KS_CUDA(f->moves.alloc((size_t)std::max(f->n_int, 1) * (2 * 64 + 1)));
     KS_CUDA(f->pm.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
     KS_CUDA(f->lu_scratch.alloc((size_t)std::max(f->n_int, 1) * 32 * 64));
+    KS_CUDA(f->dinv.alloc((size_t)std::max(f->n_int, 1) * 2 * f->t_pad * 16));
     KS_CUDA(f->leafA.alloc(nl * (size_t)f->R * f->m_pad));
     KS_CUDA(f->inv.alloc(nl * (size_t)f->m_pad * 64));
     KS_CUDA(f->hbuf.alloc((size_t)nn * f->s_pad * f->s_pad + 1));
@@ -822,18 +824,46 @@ static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt, int T,
 
 // Internal levels [lev0, lev1) of the plan (deepest first); wide levels split
 // into node groups on the group streams. Condition estimates run on the side
-// stream (they only feed diagnostics), joined at the end.
+// stream (they only feed diagnostics), joined at the end. The estimates of the
+// wide (HBM-heavy) levels wait for the first narrow level, whose latency-bound
+// launches leave most SMs idle, instead of competing with the next wide level.
 static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1) {
   const ks::DevTree dt = f->devtree();
   auto mark = [&](cudaEvent_t e) -> int {
     if (f->profiling) KS_CUDA(cudaEventRecord(e, st));
     return KS_OK;
   };
+  std::vector<int> deferred;  // levels whose estimate is not launched yet
+  auto flush = [&]() -> int {
+    if (deferred.empty()) return KS_OK;
+    if (trace_on()) {  // inline, so the trace times each estimate
+      for (int lv : deferred) {
+        f->cur_tag = lv;
+        ks::launch_hager(dt, f->nodebatch(lv), f->dinv.p, st);
+        L.count[0] += ks::hager_launches(f->nodebatch(lv));
+        if (int rc = L.check("hager")) return rc;
+      }
+      deferred.clear();
+      return KS_OK;
+    }
+    KS_CUDA(cudaEventRecord(f->ev_fork, st));
+    KS_CUDA(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
+    for (int lv : deferred) {
+      ks::launch_hager(dt, f->nodebatch(lv), f->dinv.p, f->side);
+      L.count[0] += ks::hager_launches(f->nodebatch(lv));
+    }
+    deferred.clear();
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+  };
   for (int lev = lev0; lev < lev1; ++lev) {
     f->cur_tag = (int)lev;
     const ks::NodeBatch nb = f->nodebatch((int)lev);
     const bool is_root_level = (f->levels[lev][0] == 0);
-    const int G = (nb.count >= 64) ? n_groups() : 1;
+    const bool wide = nb.count >= 64;
+    if (!wide)
+      if (int rc = flush()) return rc;
+    const int G = wide ? n_groups() : 1;
     if (G == 1) {
       if (int rc = enqueue_level_body(f, L, nb, is_root_level)) return rc;
     } else {
@@ -848,14 +878,13 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
         KS_CUDA(cudaStreamWaitEvent(st, f->gjoin[g], 0));
       }
     }
-    // condition estimate off the critical path (it only feeds diagnostics)
-    KS_CUDA(cudaEventRecord(f->ev_fork, st));
-    KS_CUDA(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
-    ks::launch_hager(dt, nb, f->side);
-    ++L.count[0];
-    KS_CUDA(cudaGetLastError());
+    // condition estimate off the critical path
+    deferred.push_back(lev);
+    if (!wide)
+      if (int rc = flush()) return rc;
     if (int rc2 = mark(f->ev_level[lev])) return rc2;
   }
+  if (int rc = flush()) return rc;
   KS_CUDA(cudaEventRecord(f->ev_join, f->side));
   KS_CUDA(cudaStreamWaitEvent(st, f->ev_join, 0));
   return KS_OK;

@@ -365,19 +365,32 @@ void launch_colnorm1(const DevTree&, const NodeBatch& nb, cudaStream_t st) {
 // --------------------------------------------------------------------------
 // LU with partial pivoting restricted to rows < t_pad (linalg.py:199-213 on
 // the Z block; the -PG rows are eliminated but never chosen as pivots).
-// Base panel: W columns [c0, c0+W), rows [c0, T), held in registers (each
-// thread owns up to RPT physical rows). Rows are never moved inside the panel:
-// each thread tracks its rows' LOGICAL positions (the row-interchange sequence
-// of the reference, swaps[k] = p). The column loop is fully unrolled, so the
-// finished L/U values simply stay in their registers; one barrier per column.
-// Pivot search: |v| >= 0 compares like its bit pattern, so the warp maximum is
+// Base panel: W columns [c0, c0+W), rows [c0, T), held in registers (each of
+// the NT threads owns up to RPT physical rows). Rows are never moved inside
+// the panel: each thread tracks its rows' LOGICAL positions (the
+// row-interchange sequence of the reference, swaps[k] = p). Columns go in
+// unrolled blocks of CB; after a block its finished values go to shared
+// memory and the register window shifts left by CB (compact code: the i-cache
+// is what limits a fully unrolled panel). One barrier per column.
+// Pivot search: |v| >= 0 compares like its bit pattern, so a warp maximum is
 // three redux ops (hi word, lo word, then the smallest logical position among
-// the maxima: np.argmax's first-occurrence rule).
+// the maxima: np.argmax's first-occurrence rule), within and across warps.
 // --------------------------------------------------------------------------
+__device__ __forceinline__ void warp_argmax(double v, int p, unsigned& mh, unsigned& ml, int& mp, bool& top) {
+  const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
+  mh = __reduce_max_sync(0xffffffffu, hi);
+  ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  top = (hi == mh && lo == ml);
+  mp = (int)__reduce_min_sync(0xffffffffu, top ? (unsigned)p : 0x7fffffffu);
+}
+
 template <int W, int RPT, int NT>
 __global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, int pc0, int ph, int pcols) {
   constexpr int NW = NT / 32;
   constexpr int NONE = 0x7fffffff;
+  constexpr int CB = 4;       // columns per unrolled block
+  constexpr int FS = W + 2;   // finished-value row stride (16 B aligned, conflict-free 16 B stores)
+  static_assert(NW <= 32 && W % CB == 0, "panel shape");
   const int k = blockIdx.x;
   const int T = nb.T;
   double* A = nb.Aug + (int64_t)k * T * T;
@@ -390,8 +403,8 @@ __global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, 
   }
   const int rows = T - c0;
   const int plim = nb.t_pad - c0;  // eligible pivot rows: physical (= original) local rows < plim
-  // per-warp candidate pivot rows, double buffered by column parity
-  __shared__ __align__(16) double cand[2][NW][W];
+  extern __shared__ __align__(16) double fin[];  // rows x FS finished values
+  __shared__ __align__(16) double cand[2][NW][W];  // per-warp candidate pivot rows, by column parity
   __shared__ double wv[2][NW];
   __shared__ int wp[2][NW], wr[2][NW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -413,73 +426,90 @@ __global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, 
   }
   int* info = nb.info + k;
   int* piv = nb.piv + (int64_t)k * nb.t_pad + c0;
+#pragma unroll 1
+  for (int kb = 0; kb < W; kb += CB) {
 #pragma unroll
-  for (int kk = 0; kk < W; ++kk) {
-    const int buf = kk & 1;
-    // 1) this thread's best eligible row (no candidate: value 0, position NONE)
-    double bv = 0.0;
-    int bp = NONE, bi = -1;
+    for (int c = 0; c < CB; ++c) {
+      const int kk = kb + c;  // panel column; c is its slot in the register window
+      const int buf = c & 1;
+      // 1) this thread's best eligible row (none: value 0, position NONE)
+      double bv = 0.0;
+      int bp = NONE, bi = -1;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int r = threadIdx.x + i * NT;
+        const double v = fabs(a[i][c]);
+        if (r < plim && !done[i] && (v > bv || (v == bv && pos[i] < bp))) { bv = v; bp = pos[i]; bi = i; }
+      }
+      unsigned mh, ml;
+      int mp;
+      bool top;
+      warp_argmax(bv, bp, mh, ml, mp, top);
+      if (top && bp == mp && bi >= 0) {  // the warp's winning lane publishes its row
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+          if (i == bi) {
+#pragma unroll
+            for (int j = c; j < W; ++j) cand[buf][warp][j] = a[i][j];
+            wr[buf][warp] = threadIdx.x + i * NT;
+          }
+      }
+      if (lane == 0) { wv[buf][warp] = __hiloint2double((int)mh, (int)ml); wp[buf][warp] = mp; }
+      __syncthreads();
+      // 2) across warps, lane-parallel
+      {
+        const double v = lane < NW ? wv[buf][lane] : 0.0;
+        const int p = lane < NW ? wp[buf][lane] : NONE;
+        warp_argmax(v, p, mh, ml, mp, top);
+        bv = __hiloint2double((int)mh, (int)ml);
+        bp = mp;
+      }
+      const bool singular = !(bv > 0.0);
+      const int ww = singular ? 0 : __ffs(__ballot_sync(0xffffffffu, lane < NW && wp[buf][lane < NW ? lane : 0] == bp &&
+                                                                   wv[buf][lane < NW ? lane : 0] == bv)) - 1;
+      const int br = singular ? -1 : wr[buf][ww];
+      if (threadIdx.x == 0) {
+        if (singular && *info == 0) *info = c0 + kk + 1;  // linalg.py:205-206
+        piv[kk] = c0 + (singular ? kk : bp);
+      }
+      const double rcp = 1.0 / (singular ? 1.0 : cand[buf][ww][c]);
+      // 3) logical swap kk <-> bp, eliminate every other remaining row (linalg.py:209-212)
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int r = threadIdx.x + i * NT;
+        const bool is_piv = !done[i] && (singular ? pos[i] == kk : r == br);
+        if (!singular && !done[i]) pos[i] = (r == br) ? kk : (pos[i] == kk ? bp : pos[i]);
+        const bool keep = done[i] || is_piv;  // U rows: values from column kk on are final
+        done[i] = keep;
+        const double l = keep ? 0.0 : a[i][c] * rcp;
+        if (!keep) a[i][c] = l;
+#pragma unroll
+        for (int j = c + 1; j < W; ++j) a[i][j] = fma(-l, singular ? 0.0 : cand[buf][ww][j], a[i][j]);
+      }
+    }
+    // block finished: flush its CB columns, shift the window
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int r = threadIdx.x + i * NT;
-      const double v = fabs(a[i][kk]);
-      if (r < plim && !done[i] && (v > bv || (v == bv && pos[i] < bp))) { bv = v; bp = pos[i]; bi = i; }
-    }
-    const unsigned hi = (unsigned)__double2hiint(bv), lo = (unsigned)__double2loint(bv);
-    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
-    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-    const bool top = (hi == mh && lo == ml);
-    const int mp = (int)__reduce_min_sync(0xffffffffu, top ? (unsigned)bp : (unsigned)NONE);
-    if (top && bp == mp && bi >= 0) {  // the warp's winning lane publishes its row
+      if (r < rows) {
+        double2* f2 = reinterpret_cast<double2*>(fin + r * FS + kb);
 #pragma unroll
-      for (int i = 0; i < RPT; ++i)
-        if (i == bi) {
+        for (int j = 0; j < CB / 2; ++j) f2[j] = make_double2(a[i][2 * j], a[i][2 * j + 1]);
+      }
 #pragma unroll
-          for (int j = kk; j < W; ++j) cand[buf][warp][j] = a[i][j];
-          wr[buf][warp] = threadIdx.x + i * NT;
-        }
-    }
-    if (lane == 0) { wv[buf][warp] = __hiloint2double((int)mh, (int)ml); wp[buf][warp] = mp; }
-    __syncthreads();
-    int ww = 0;
-    bv = wv[buf][0];
-    bp = wp[buf][0];
-#pragma unroll
-    for (int w = 1; w < NW; ++w) {
-      const double v = wv[buf][w];
-      const int p = wp[buf][w];
-      if (v > bv || (v == bv && p < bp)) { bv = v; bp = p; ww = w; }
-    }
-    const bool singular = !(bv > 0.0);
-    const int br = singular ? -1 : wr[buf][ww];
-    if (threadIdx.x == 0) {
-      if (singular && *info == 0) *info = c0 + kk + 1;  // linalg.py:205-206
-      piv[kk] = c0 + (singular ? kk : bp);
-    }
-    const double p0 = singular ? 1.0 : cand[buf][ww][kk];
-    const double rcp = 1.0 / p0;
-    // 2) logical swap kk <-> bp, eliminate every other remaining row (linalg.py:209-212)
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int r = threadIdx.x + i * NT;
-      const bool is_piv = !done[i] && (singular ? pos[i] == kk : r == br);
-      if (!singular && !done[i]) pos[i] = (r == br) ? kk : (pos[i] == kk ? bp : pos[i]);
-      const bool keep = done[i] || is_piv;  // U rows: values from column kk on are final
-      done[i] = keep;
-      const double l = keep ? 0.0 : a[i][kk] * rcp;
-      if (!keep) a[i][kk] = l;
-#pragma unroll
-      for (int j = kk + 1; j < W; ++j) a[i][j] = fma(-l, singular ? 0.0 : cand[buf][ww][j], a[i][j]);
+      for (int j = 0; j < W; ++j) a[i][j] = (j + CB < W) ? a[i][j + CB] : 0.0;
     }
   }
+  __syncthreads();
   // panel rows back to their logical positions
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     const int r = threadIdx.x + i * NT;
     if (r >= rows) continue;
     double2* dst = reinterpret_cast<double2*>(A + (int64_t)(c0 + pos[i]) * T + c0);
+    const double2* f2 = reinterpret_cast<const double2*>(fin + r * FS);
 #pragma unroll
-    for (int j = 0; j < W / 2; ++j) dst[j] = make_double2(a[i][2 * j], a[i][2 * j + 1]);
+    for (int j = 0; j < W / 2; ++j) dst[j] = f2[j];
   }
   // the same row interchanges for every column outside the panel: at most 2W
   // rows moved; the list goes through shared memory, all loads before stores
@@ -498,38 +528,39 @@ __global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, 
   }
   __syncthreads();
   const int nm = nmove;
-  if (nm == 0) return;
-  int so[2 * W], sd[2 * W];
-#pragma unroll
-  for (int m = 0; m < 2 * W; ++m) {
-    so[m] = m < nm ? msrc[m] : 0;
-    sd[m] = m < nm ? mdst[m] : 0;
-  }
-  for (int col = threadIdx.x; col < T - W; col += NT) {
-    const int cc = col < c0 ? col : col + W;
-    double v[2 * W];
-#pragma unroll
-    for (int m = 0; m < 2 * W; ++m)
-      if (m < nm) v[m] = A[so[m] + cc];
-#pragma unroll
-    for (int m = 0; m < 2 * W; ++m)
-      if (m < nm) A[sd[m] + cc] = v[m];
+  // staged through the (now free) finished-value buffer, PC columns at a time
+  constexpr int PC = 256;
+  for (int cb = 0; cb < T - W; cb += PC) {
+    const int ncol = min(PC, T - W - cb);
+    for (int e = threadIdx.x; e < nm * PC; e += NT) {
+      const int m = e / PC, col = cb + e % PC;
+      if (col < cb + ncol) fin[e] = A[msrc[m] + (col < c0 ? col : col + W)];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nm * PC; e += NT) {
+      const int m = e / PC, col = cb + e % PC;
+      if (col < cb + ncol) A[mdst[m] + (col < c0 ? col : col + W)] = fin[e];
+    }
+    __syncthreads();
   }
 }
 
 template <int W, int RPT, int NT>
 static void launch_panel(const NodeBatch& nb, int c0, cudaStream_t st, const int* pend) {
-  k_lu_panel<W, RPT, NT><<<nb.count, NT, 0, st>>>(nb, c0, pend[0], pend[1], pend[2], pend[3]);
+  const size_t smem = (size_t)std::max((nb.T - c0) * (W + 2), 2 * W * 256) * sizeof(double);
+  static size_t set = 0;
+  if (smem > set) {
+    cudaFuncSetAttribute(k_lu_panel<W, RPT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = smem;
+  }
+  k_lu_panel<W, RPT, NT><<<nb.count, NT, smem, st>>>(nb, c0, pend[0], pend[1], pend[2], pend[3]);
 }
 
 template <int W>
 static void launch_panel_w(const NodeBatch& nb, int c0, cudaStream_t st, const int* pend) {
+  // 512 threads (16 warps hide the per-column latency), rows in registers
   const int rows = nb.T - c0;
-  // 256 threads x (up to 3 rows x 16 columns) in registers up to 768 rows;
-  // 512 threads beyond
-  if (W == 16 && rows <= 256) launch_panel<W, 1, 256>(nb, c0, st, pend);
-  else if (W == 16 && rows <= 512) launch_panel<W, 2, 256>(nb, c0, st, pend);
-  else if (W == 16 && rows <= 768) launch_panel<W, 3, 256>(nb, c0, st, pend);
+  if (rows <= 512) launch_panel<W, 1, 512>(nb, c0, st, pend);
   else if (rows <= 1024) launch_panel<W, 2, 512>(nb, c0, st, pend);
   else if constexpr (W <= 8) {
     if (rows <= 1536) launch_panel<W, 3, 512>(nb, c0, st, pend);
@@ -710,14 +741,246 @@ __global__ void __launch_bounds__(STHREADS) k_hager(DevTree t, NodeBatch nb) {
   if (threadIdx.x == 0) nb.cond[k] = isfinite(est) ? nb.norm1[k] * est : INFINITY;
 }
 
-void launch_hager(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
-  const size_t smem = (3 * (size_t)nb.t_pad + SWARPS * 32) * sizeof(double) + nb.t_pad * sizeof(int);
+static void launch_hager_blocked(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (3 * nb.t_pad + SWARPS * 32) + sizeof(int) * nb.t_pad;
   static size_t set = 0;
   if (smem > set) {
     cudaFuncSetAttribute(k_hager, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set = smem;
   }
   k_hager<<<nb.count, STHREADS, smem, st>>>(t, nb);
+}
+
+// --------------------------------------------------------------------------
+// The same estimate with thread-owned vectors (t_pad <= 1024): thread i owns
+// entry i of every vector. A triangular solve walks SB-row blocks; the
+// coefficients coupling the next block to each thread's entry are loaded one
+// step ahead, the diagonal block goes through its inverse (precomputed by
+// k_diag_inv, staged in shared memory) as an SB-wide shuffle GEMV, so a block
+// step is a handful of dependent operations and one barrier.
+// --------------------------------------------------------------------------
+enum { SOLVE_L = 0, SOLVE_U = 1, SOLVE_UT = 2, SOLVE_LT = 3 };
+
+// inverses of the SB x SB diagonal blocks of unit-lower L (which 0) and upper
+// U (which 1) of every node's Z factors: dinv[node][which][b][s][t]
+template <int SB>
+__global__ void __launch_bounds__(256) k_diag_inv(NodeBatch nb, double* dinv) {
+  const int k = blockIdx.x, which = blockIdx.y;
+  const int TP = nb.t_pad, T = nb.T;
+  const double* A = nb.Aug + (int64_t)k * T * T;
+  double* out = dinv + ((int64_t)(nb.first + k) * 2 + which) * TP * SB;
+  for (int task = threadIdx.x; task < TP; task += 256) {
+    const int b = task / SB, j = task % SB;  // column j of block b's inverse
+    const int r0 = b * SB;
+    double x[SB];
+    if (which == 0) {
+#pragma unroll
+      for (int s2 = 0; s2 < SB; ++s2) {
+        double v = (s2 == j) ? 1.0 : 0.0;
+#pragma unroll
+        for (int t2 = 0; t2 < s2; ++t2)
+          if (t2 >= j) v = fma(-A[(int64_t)(r0 + s2) * T + r0 + t2], x[t2], v);
+        x[s2] = (s2 < j) ? 0.0 : v;
+      }
+    } else {
+#pragma unroll
+      for (int s2 = SB - 1; s2 >= 0; --s2) {
+        double v = (s2 == j) ? 1.0 : 0.0;
+#pragma unroll
+        for (int t2 = s2 + 1; t2 < SB; ++t2)
+          if (t2 <= j) v = fma(-A[(int64_t)(r0 + s2) * T + r0 + t2], x[t2], v);
+        x[s2] = (s2 > j) ? 0.0 : v / A[(int64_t)(r0 + s2) * T + r0 + s2];
+      }
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < SB; ++s2) out[(int64_t)b * SB * SB + s2 * SB + j] = x[s2];
+  }
+}
+
+// v (thread i's entry) <- M^-1 v for M = L (unit lower), U, U^T or L^T of the
+// packed factors in A (rows of length lda); di: the matching diagonal-block
+// inverses in shared memory; xs: a shared broadcast buffer (n entries).
+template <int SB, int NT, int MODE>
+__device__ __forceinline__ double own_solve(const double* __restrict__ A, int64_t lda, int n, const double* di, double v,
+                            double* xs) {
+  constexpr bool ASC = (MODE == SOLVE_L || MODE == SOLVE_UT);
+  constexpr bool TRANS = (MODE == SOLVE_UT || MODE == SOLVE_LT);
+  const int i = threadIdx.x, lane = i & 31;
+  const bool own = i < n;
+  const int nblk = n / SB;
+  double cur[SB], nxt[SB];
+  auto load = [&](int b, double (&c)[SB]) {
+    const int r0 = b * SB;
+    const bool need = own && (ASC ? i >= r0 + SB : i < r0);  // solved after block b
+    if (TRANS) {
+      const double* p = A + (int64_t)r0 * lda + (own ? i : 0);
+#pragma unroll
+      for (int j = 0; j < SB; ++j, p += lda) c[j] = need ? __ldg(p) : 0.0;
+    } else {
+      const double2* p = reinterpret_cast<const double2*>(A + (int64_t)(own ? i : 0) * lda + r0);
+#pragma unroll
+      for (int j = 0; j < SB / 2; ++j) {
+        const double2 u = need ? __ldg(p + j) : make_double2(0.0, 0.0);
+        c[2 * j] = u.x;
+        c[2 * j + 1] = u.y;
+      }
+    }
+  };
+  load(ASC ? 0 : nblk - 1, cur);
+  __syncthreads();  // xs may still be read by the caller's previous phase
+#pragma unroll 1
+  for (int step = 0; step < nblk; ++step) {
+    const int b = ASC ? step : nblk - 1 - step;
+    if (step + 1 < nblk) load(ASC ? b + 1 : b - 1, nxt);
+    const int r0 = b * SB;
+    if ((i >> 5) == (r0 >> 5)) {  // the warp holding block b: x_b = D_b^-1 v_b
+      const int base = r0 & 31, s2 = lane - base;
+      const bool inb = own && s2 >= 0 && s2 < SB;
+      const double* d = di + (int64_t)b * SB * SB;
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+      for (int t2 = 0; t2 < SB; t2 += 2) {
+        const double v0 = __shfl_sync(0xffffffffu, v, base + t2);
+        const double v1 = __shfl_sync(0xffffffffu, v, base + t2 + 1);
+        if (inb) {
+          acc0 = fma(TRANS ? d[t2 * SB + s2] : d[s2 * SB + t2], v0, acc0);
+          acc1 = fma(TRANS ? d[(t2 + 1) * SB + s2] : d[s2 * SB + t2 + 1], v1, acc1);
+        }
+      }
+      if (inb) {
+        v = acc0 + acc1;
+        xs[i] = v;
+      }
+    }
+    __syncthreads();
+    const bool after = own && (ASC ? i >= r0 + SB : i < r0);
+    if (after) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < SB; j += 2) {
+        s0 = fma(cur[j], xs[r0 + j], s0);
+        s1 = fma(cur[j + 1], xs[r0 + j + 1], s1);
+      }
+      v -= s0 + s1;
+    }
+#pragma unroll
+    for (int j = 0; j < SB; ++j) cur[j] = nxt[j];
+  }
+  return v;
+}
+
+template <int NT>
+__device__ __forceinline__ double nt_sum(double v, double* red) {
+  constexpr int NWp = NT / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < NWp; ++w) s += red[w];
+  return s;
+}
+
+template <int NT>
+__device__ __forceinline__ void nt_argmax(double& bv, int& bi, double* red, int* redi) {
+  constexpr int NWp = NT / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  }
+  __syncthreads();
+  if (lane == 0) { red[warp] = bv; redi[warp] = bi; }
+  __syncthreads();
+  bv = red[0];
+  bi = redi[0];
+#pragma unroll
+  for (int w = 1; w < NWp; ++w)
+    if (red[w] > bv || (red[w] == bv && redi[w] < bi)) { bv = red[w]; bi = redi[w]; }
+}
+
+template <int SB, int NT>
+__global__ void __launch_bounds__(NT, 1) k_hager_own(DevTree t, NodeBatch nb, const double* dinv) {
+  extern __shared__ __align__(16) double hs[];
+  const int k = blockIdx.x;
+  const int TP = nb.t_pad, S = nb.s_pad, T = nb.T;
+  const int sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]];
+  const int n = sl + sr;
+  if (n == 0) {
+    if (threadIdx.x == 0) nb.cond[k] = 0.0;
+    return;
+  }
+  double* dL = hs;                 // TP x SB
+  double* dU = hs + TP * SB;       // TP x SB
+  double* xs = dU + TP * SB;       // TP
+  double* red = xs + TP;           // NT / 32
+  int* redi = reinterpret_cast<int*>(red + NT / 32);
+  int* pm = redi + NT / 32;        // TP: composed swaps, (Pi v)[i] = v[pm[i]]
+  const double* A = nb.Aug + (int64_t)k * T * T;
+  {
+    const double2* src = reinterpret_cast<const double2*>(dinv + (int64_t)(nb.first + k) * 2 * TP * SB);
+    double2* dst = reinterpret_cast<double2*>(hs);
+    for (int e = threadIdx.x; e < TP * SB; e += NT) dst[e] = src[e];
+    for (int e = threadIdx.x; e < TP; e += NT) pm[e] = nb.pm[(int64_t)k * TP + e];
+  }
+  const int i = threadIdx.x;
+  const bool own = i < TP;
+  const bool real = own && (i < S ? (i < sl) : (i - S < sr));
+  const int ref = i < S ? i : sl + (i - S);  // reference index order
+  double x = real ? 1.0 / n : 0.0;
+  double est = 0.0;
+  __syncthreads();
+  for (int it = 0; it < 5; ++it) {
+    // y = Z^-1 x   (dense_solve: swaps, unit L, U)
+    if (own) xs[i] = x;
+    __syncthreads();
+    double y = own ? xs[pm[i]] : 0.0;
+    y = own_solve<SB, NT, SOLVE_L>(A, T, TP, dL, y, xs);
+    y = own_solve<SB, NT, SOLVE_U>(A, T, TP, dU, y, xs);
+    est = nt_sum<NT>(real ? fabs(y) : 0.0, red);
+    // z = Z^-T sign(y)   (solve_transposed: U^T, unit L^T, undo swaps)
+    double w = real ? (y >= 0.0 ? 1.0 : -1.0) : 0.0;
+    w = own_solve<SB, NT, SOLVE_UT>(A, T, TP, dU, w, xs);
+    w = own_solve<SB, NT, SOLVE_LT>(A, T, TP, dL, w, xs);
+    __syncthreads();
+    if (own) xs[pm[i]] = w;
+    __syncthreads();
+    const double z = own ? xs[i] : 0.0;
+    // j = argmax |z| (first in reference order on ties), z . x
+    double bv = real ? fabs(z) : -1.0;
+    int bi = real ? ref : 0x7fffffff;
+    nt_argmax<NT>(bv, bi, red, redi);
+    const double dot = nt_sum<NT>(real ? z * x : 0.0, red);
+    if (bv <= dot) break;
+    const int jp = bi < sl ? bi : S + (bi - sl);
+    x = (i == jp) ? 1.0 : 0.0;
+  }
+  if (threadIdx.x == 0) nb.cond[k] = isfinite(est) ? nb.norm1[k] * est : INFINITY;
+}
+
+template <int SB, int NT>
+static void launch_hager_own(const DevTree& t, const NodeBatch& nb, double* dinv, cudaStream_t st) {
+  dim3 g(nb.count, 2);
+  k_diag_inv<SB><<<g, 256, 0, st>>>(nb, dinv);
+  const size_t smem = sizeof(double) * (2 * (size_t)nb.t_pad * SB + nb.t_pad + 2 * NT / 32) + sizeof(int) * nb.t_pad;
+  static size_t set = 0;
+  if (smem > set) {
+    cudaFuncSetAttribute(k_hager_own<SB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = smem;
+  }
+  k_hager_own<SB, NT><<<nb.count, NT, smem, st>>>(t, nb, dinv);
+}
+
+int hager_launches(const NodeBatch& nb) { return nb.t_pad <= 1024 ? 2 : 1; }
+
+void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, cudaStream_t st) {
+  if (nb.t_pad <= 512) launch_hager_own<8, 512>(t, nb, dinv, st);
+  else if (nb.t_pad <= 1024) launch_hager_own<8, 1024>(t, nb, dinv, st);
+  else launch_hager_blocked(t, nb, st);
 }
 
 // LU fallback for leaves whose Cholesky failed (solver.py:125-131): the
