@@ -822,6 +822,12 @@ static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt, int T,
   return s;
 }
 
+// SMs the overlapped condition estimates may occupy (of 148); KS_HAGER_CTAS overrides
+static int hager_ctas() {
+  const char* e = std::getenv("KS_HAGER_CTAS");
+  return e ? std::max(1, std::atoi(e)) : 96;
+}
+
 // Internal levels [lev0, lev1) of the plan (deepest first); wide levels split
 // into node groups on the group streams. Condition estimates run on the side
 // stream (they only feed diagnostics), joined at the end. The estimates of the
@@ -839,7 +845,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
     if (trace_on()) {  // inline, so the trace times each estimate
       for (int lv : deferred) {
         f->cur_tag = lv;
-        ks::launch_hager(dt, f->nodebatch(lv), f->dinv.p, st);
+        ks::launch_hager(dt, f->nodebatch(lv), f->dinv.p, 1 << 30, st);
         L.count[0] += ks::hager_launches(f->nodebatch(lv));
         if (int rc = L.check("hager")) return rc;
       }
@@ -849,7 +855,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
     KS_CUDA(cudaEventRecord(f->ev_fork, st));
     KS_CUDA(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
     for (int lv : deferred) {
-      ks::launch_hager(dt, f->nodebatch(lv), f->dinv.p, f->side);
+      ks::launch_hager(dt, f->nodebatch(lv), f->dinv.p, hager_ctas(), f->side);
       L.count[0] += ks::hager_launches(f->nodebatch(lv));
     }
     deferred.clear();

@@ -906,13 +906,16 @@ __device__ __forceinline__ void nt_argmax(double& bv, int& bi, double* red, int*
 template <int SB, int NT>
 __global__ void __launch_bounds__(NT, 1) k_hager_own(DevTree t, NodeBatch nb, const double* dinv) {
   extern __shared__ __align__(16) double hs[];
-  const int k = blockIdx.x;
+  // persistent over nodes: the grid may be smaller than the batch so that the
+  // estimate leaves SMs free for the factorization it overlaps
+  for (int k = blockIdx.x; k < nb.count; k += gridDim.x) {
+  __syncthreads();
   const int TP = nb.t_pad, S = nb.s_pad, T = nb.T;
   const int sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]];
   const int n = sl + sr;
   if (n == 0) {
     if (threadIdx.x == 0) nb.cond[k] = 0.0;
-    return;
+    continue;
   }
   double* dL = hs;                 // TP x SB
   double* dU = hs + TP * SB;       // TP x SB
@@ -960,10 +963,11 @@ __global__ void __launch_bounds__(NT, 1) k_hager_own(DevTree t, NodeBatch nb, co
     x = (i == jp) ? 1.0 : 0.0;
   }
   if (threadIdx.x == 0) nb.cond[k] = isfinite(est) ? nb.norm1[k] * est : INFINITY;
+  }
 }
 
 template <int SB, int NT>
-static void launch_hager_own(const DevTree& t, const NodeBatch& nb, double* dinv, cudaStream_t st) {
+static void launch_hager_own(const DevTree& t, const NodeBatch& nb, double* dinv, int max_ctas, cudaStream_t st) {
   dim3 g(nb.count, 2);
   k_diag_inv<SB><<<g, 256, 0, st>>>(nb, dinv);
   const size_t smem = sizeof(double) * (2 * (size_t)nb.t_pad * SB + nb.t_pad + 2 * NT / 32) + sizeof(int) * nb.t_pad;
@@ -972,14 +976,14 @@ static void launch_hager_own(const DevTree& t, const NodeBatch& nb, double* dinv
     cudaFuncSetAttribute(k_hager_own<SB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set = smem;
   }
-  k_hager_own<SB, NT><<<nb.count, NT, smem, st>>>(t, nb, dinv);
+  k_hager_own<SB, NT><<<std::min(nb.count, max_ctas), NT, smem, st>>>(t, nb, dinv);
 }
 
 int hager_launches(const NodeBatch& nb) { return nb.t_pad <= 1024 ? 2 : 1; }
 
-void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, cudaStream_t st) {
-  if (nb.t_pad <= 512) launch_hager_own<8, 512>(t, nb, dinv, st);
-  else if (nb.t_pad <= 1024) launch_hager_own<8, 1024>(t, nb, dinv, st);
+void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, int max_ctas, cudaStream_t st) {
+  if (nb.t_pad <= 512) launch_hager_own<8, 512>(t, nb, dinv, max_ctas, st);
+  else if (nb.t_pad <= 1024) launch_hager_own<8, 1024>(t, nb, dinv, max_ctas, st);
   else launch_hager_blocked(t, nb, st);
 }
 

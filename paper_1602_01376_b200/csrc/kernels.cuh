@@ -64,7 +64,8 @@ void launch_lu_panel(const NodeBatch& nb, int c0, int w, cudaStream_t st, const 
 void launch_lu_swap(const NodeBatch& nb, int c0, int w, cudaStream_t st);
 void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncols, cudaStream_t st);
 // dinv: scratch for the diagonal-block inverses, 2 x t_pad x 16 doubles per internal node
-void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, cudaStream_t st);
+// max_ctas bounds the estimator's grid (it loops over the batch's nodes)
+void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, int max_ctas, cudaStream_t st);
 int hager_launches(const NodeBatch& nb);
 void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st);
 void launch_compose_perm(const NodeBatch& nb, cudaStream_t st);
