@@ -230,6 +230,7 @@ GemmArgs mk(int M, int N, int K, int batch, Operand A, Operand B, OperandW C, do
   g.M = M; g.N = N; g.K = K; g.batch = batch;
   g.A = A; g.B = B; g.C = C;
   g.alpha = alpha; g.beta = beta; g.tri = 0;
+  g.E = Operand{nullptr, 0, 0, nullptr};
   return g;
 }
 
@@ -624,6 +625,12 @@ int ks_create_shard(const ks_problem* p, int device, int64_t shard_root, ks_fact
 // Leaves [l0, l1): left-looking Cholesky of the (m+s) x m trapezoids in 64-column
 // panels (panel update GEMM, 64x64 POTRF + inverse, panel TRSM as GEMM with the
 // inverse), then H = L21 L21^T (solver.py:123-135).
+// KS_UNFUSED_LEAF_TRSM=1: separate update and TRSM GEMMs per leaf panel (A/B check)
+static bool unfused_leaf_trsm() {
+  const char* e = std::getenv("KS_UNFUSED_LEAF_TRSM");
+  return e && e[0] == '1';
+}
+
 static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
   const ks::LeafBatch all = f->leafbatch();
   ks::LeafBatch lb = all;
@@ -639,23 +646,37 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
   double* inv = f->inv.p + (int64_t)l0 * M * 64;
   int* info = f->leaf_info.p + l0;
   cudaStream_t st = L.st;
+  const bool fused = !unfused_leaf_trsm();
   for (int j0 = 0; j0 < M; j0 += 64) {
-    if (j0 > 0) {
+    const Operand Einv{inv + (int64_t)(j0 / 64) * 64 * 64, 64, (int64_t)M * 64, nullptr};
+    if (j0 > 0) {  // left-looking update of the panel (all rows, or just its diagonal block)
       Operand A{leafA + (int64_t)j0 * M, M, AS, nullptr};
       Operand B{leafA + (int64_t)j0 * M, M, AS, nullptr};
       OperandW C{leafA + (int64_t)j0 * M + j0, M, AS, nullptr};
-      int rc = L.gemm(mk(R - j0, 64, j0, nl, A, B, C, -1.0, 1.0), false, true, "leaf_update");
+      int rc = L.gemm(mk(fused ? 64 : R - j0, 64, j0, nl, A, B, C, -1.0, 1.0), false, true,
+                      fused ? "leaf_update_diag" : "leaf_update");
       if (rc) return rc;
     }
     ks::launch_potrf64(lb, j0, inv, info, st);
     ++L.count[0];
     if (int rc = L.check("potrf64")) return rc;
     if (R - j0 - 64 > 0) {
-      Operand A{leafA + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
-      Operand B{inv + (int64_t)(j0 / 64) * 64 * 64, 64, (int64_t)M * 64, nullptr};
       OperandW C{leafA + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
-      int rc = L.gemm(mk(R - j0 - 64, 64, 64, nl, A, B, C, 1.0, 0.0), false, true, "leaf_trsm");
-      if (rc) return rc;
+      if (fused && j0 > 0) {
+        // rows below the diagonal block: update and TRSM (x L_jj^-T) in one GEMM
+        Operand A{leafA + (int64_t)(j0 + 64) * M, M, AS, nullptr};
+        Operand B{leafA + (int64_t)j0 * M, M, AS, nullptr};
+        GemmArgs g = mk(R - j0 - 64, 64, j0, nl, A, B, C, -1.0, 1.0);
+        g.E = Einv;
+        ++L.count[0];
+        cudaError_t e = ks::gemm_update_trsm(g, st);
+        if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf update+trsm gemm: %s", cudaGetErrorString(e));
+        if (int rc = L.check("leaf_update_trsm")) return rc;
+      } else {
+        Operand A{leafA + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
+        int rc = L.gemm(mk(R - j0 - 64, 64, 64, nl, A, Einv, C, 1.0, 0.0), false, true, "leaf_trsm");
+        if (rc) return rc;
+      }
     }
   }
   if (S > 0 && f->n_int > 0) {

@@ -11,14 +11,15 @@ template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES, int EPI 
 cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, WM, WN, TA, TB, STAGES>;
   auto kern = k_gemm<BM, BN, WM, WN, TA, TB, STAGES, EPI>;
+  constexpr size_t smem = (EPI == 2 && Cfg::SMEM_EPI2 > Cfg::SMEM) ? Cfg::SMEM_EPI2 : Cfg::SMEM;
   static bool attr = false;  // per instantiation; set before first launch
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.batch);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(g);
+  kern<<<grid, Cfg::THREADS, smem, st>>>(g);
   return cudaGetLastError();
 }
 
@@ -66,6 +67,12 @@ cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st) {
   t.tri = 1;
   // K = d is small and the exp epilogue dominates: small tiles, 2 stages, many warps per SM
   return launch<64, 64, 2, 2, false, true, 2, 1>(t, st);
+}
+
+cudaError_t gemm_update_trsm(const GemmArgs& g, cudaStream_t st) {
+  if (g.M <= 0 || g.batch <= 0) return cudaSuccess;
+  if (g.N != 64 || (g.K & 1) || g.K <= 0 || ((g.A.ld | g.B.ld | g.C.ld | g.E.ld) & 1)) return cudaErrorInvalidValue;
+  return launch<128, 64, 4, 2, false, true, 3, 2>(g, st);
 }
 
 cudaError_t gemm(const GemmArgs& g, bool ta, bool tb, cudaStream_t st) {

@@ -24,6 +24,10 @@ namespace ks {
 //      / (-2 h h)) for r > c, 1 + lam on the diagonal (r == c: distance exactly 0,
 //      kernel exactly 1, solver.py:124), identity on padded rows/columns
 //      (r or c >= size[b]) and 0 above the diagonal.
+//   2  panel TRSM folded into a panel update (N == BN == 64):
+//      C = (alpha*AB + beta*C) * E^T, E[b] a 64 x 64 block (the inverse of the
+//      panel's diagonal Cholesky factor): the updated tile is staged in shared
+//      memory and multiplied on the tensor pipe before it is stored.
 struct GaussEpi {
   const double* xx;   // squared norms of the points, tree order
   const int* begin;   // per batch: first point of the leaf
@@ -39,6 +43,7 @@ struct GemmArgs {
   double alpha, beta;
   int tri;  // 1: skip CTA tiles strictly above the diagonal of C
   GaussEpi ge;
+  Operand E;  // EPI == 2: right factor of the epilogue product
 };
 
 template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
@@ -51,6 +56,9 @@ struct GemmCfg {
   static constexpr int B_ROWS = TB ? BN : BK, B_COLS = TB ? BK : BN, B_LD = B_COLS + 4;
   static constexpr int A_STAGE = A_ROWS * A_LD, B_STAGE = B_ROWS * B_LD;
   static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+  // EPI == 2 reuses the pipeline buffers for the staged tile and E
+  static constexpr int T_LD = BN + 4;
+  static constexpr size_t SMEM_EPI2 = (size_t)(BM + BN) * T_LD * sizeof(double);
   static_assert(A_LD % 16 == 4 && B_LD % 16 == 4, "conflict-free fragment loads need ld = 4 mod 16");
 };
 
@@ -148,6 +156,58 @@ __global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
   cp_async_wait<0>();
 
   const double alpha = g.alpha, beta = g.beta;
+  if constexpr (EPI == 2) {
+    constexpr int TL = Cfg::T_LD;
+    static_assert(TL % 16 == 4, "conflict-free fragment loads");
+    __syncthreads();  // every warp is done with the pipeline buffers
+    double* Ts = smem;            // BM x BN updated tile
+    double* Es = smem + BM * TL;  // BN x BN, E[c][k]
+    const double* E = g.E.at(b);
+    for (int e = threadIdx.x; e < BN * BN / 2; e += Cfg::THREADS) {
+      const int r = e / (BN / 2), c = (e % (BN / 2)) * 2;
+      *reinterpret_cast<double2*>(Es + r * TL + c) = *reinterpret_cast<const double2*>(E + (int64_t)r * g.E.ld + c);
+    }
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; ++i) {
+      const int rl = wm0 + i * 8 + gq, r = m0 + rl;
+#pragma unroll
+      for (int j = 0; j < Cfg::NT; ++j) {
+        const int cl = wn0 + j * 8 + 2 * tq;
+        double2 v = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+        if (beta != 0.0 && r < g.M) {
+          const double2 ov = *reinterpret_cast<const double2*>(C + (int64_t)r * g.C.ld + n0 + cl);
+          v.x = fma(beta, ov.x, v.x);
+          v.y = fma(beta, ov.y, v.y);
+        }
+        *reinterpret_cast<double2*>(Ts + rl * TL + cl) = v;
+        acc[i][j][0] = acc[i][j][1] = 0.0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BN; kk += 4) {
+      double af[Cfg::MT], bf[Cfg::NT];
+#pragma unroll
+      for (int i = 0; i < Cfg::MT; ++i) af[i] = Ts[(wm0 + i * 8 + gq) * TL + kk + tq];
+#pragma unroll
+      for (int j = 0; j < Cfg::NT; ++j) bf[j] = Es[(wn0 + j * 8 + gq) * TL + kk + tq];
+#pragma unroll
+      for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; ++i) {
+      const int r = m0 + wm0 + i * 8 + gq;
+      if (r >= g.M) continue;
+#pragma unroll
+      for (int j = 0; j < Cfg::NT; ++j) {
+        const int c = n0 + wn0 + j * 8 + 2 * tq;
+        *reinterpret_cast<double2*>(C + (int64_t)r * g.C.ld + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    }
+    return;
+  }
   double den = 0.0, lam = 0.0;
   int bsz = 0, bbeg = 0;
   if (EPI == 1) {
@@ -203,5 +263,7 @@ cudaError_t gemm(const GemmArgs& g, bool ta, bool tb, cudaStream_t st);
 // Leaf Gaussian blocks through the Gram GEMM with the EPI == 1 epilogue
 // (lower-triangular tiles only).
 cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st);
+// Panel update with the panel TRSM folded in (EPI == 2): N must be 64, op(B) = B^T.
+cudaError_t gemm_update_trsm(const GemmArgs& g, cudaStream_t st);
 
 }  // namespace ks
