@@ -105,6 +105,12 @@ int ks_shard_info(const ks_factor* f, int64_t* out, int64_t cap);
  * ||(K~ + lam I) X - B|| at any size. Needs a factorized (unsharded) handle. */
 int ks_matvec(ks_factor* f, const double* W, double* Y, int64_t q, void* stream);
 
+/* out[j] = sum_i exp(-|x_test_j - x_train_i|^2 / (2 h^2)) w_i: the dense, exact
+ * cross-kernel matvec of krr_predict (solver.py:273-301). Coordinates row-major
+ * (n x d), any order; host or device pointers. No handle needed. */
+int ks_kernel_matvec(const double* x_test, int64_t n_test, const double* x_train, int64_t n_train, int64_t d,
+                     double bandwidth, const double* w, double* out, int device, void* stream);
+
 int ks_get_diag(const ks_factor* f, ks_diag* out);
 /* Fill up to cap (node id, Z condition estimate) pairs, ascending node id. */
 int64_t ks_get_z_cond(const ks_factor* f, int64_t* nodes, double* conds, int64_t cap);

@@ -509,3 +509,31 @@ def hss_matvec(prob: Problem, w: np.ndarray) -> np.ndarray:
         out[seg] = kernel_block(prob.coords, ids, ids, prob.h) @ w[seg]
         out[seg] += prob.coeff(v).T @ totals[v]
     return out
+
+
+# --------------------------------------------------------------------------
+# KRR front ends, solver.py:240-301
+# --------------------------------------------------------------------------
+def krr_weights(prob: Problem, lam: float, y: np.ndarray) -> np.ndarray:
+    """krr_fit after tree + compress (solver.py:264-270): solve in tree order,
+    weights back in original order."""
+    of = factorize(prob, lam)
+    w_perm = solve_many_telescoping(of, np.asarray(y, dtype=np.float64)[prob.perm][:, None])[:, 0]
+    w = np.empty_like(w_perm)
+    w[prob.perm] = w_perm
+    return w
+
+
+def krr_predict(x_train: np.ndarray, w: np.ndarray, h: float, x_test: np.ndarray) -> np.ndarray:
+    """sum_i k(x_test_j, x_train_i) w_i, dense (solver.py:273-301): the same
+    merged-point-set kernel_block over row blocks of the test set."""
+    if x_test.shape[0] == 0:
+        return np.empty(0)
+    merged = np.vstack([x_test, x_train])
+    train_cols = x_test.shape[0] + np.arange(x_train.shape[0])
+    out = np.empty(x_test.shape[0])
+    step = max(1, (1 << 24) // max(x_train.shape[0], 1))
+    for start in range(0, x_test.shape[0], step):
+        stop = min(start + step, x_test.shape[0])
+        out[start:stop] = kernel_block(merged, np.arange(start, stop), train_cols, h) @ w
+    return out

@@ -16,6 +16,7 @@ from .errors import (
     SingularMatrixError,
 )
 from .problem import Problem, as_problem, from_arrays, from_compressed_kernel
+from .krr import krr_fit, krr_predict
 from .solver import GpuHierFactor, factorize, hss_matvec, solve, solve_many
 
 HierFactor = GpuHierFactor
@@ -35,6 +36,8 @@ __all__ = [
     "from_arrays",
     "from_compressed_kernel",
     "hss_matvec",
+    "krr_fit",
+    "krr_predict",
     "solve",
     "solve_many",
 ]

@@ -63,6 +63,8 @@ SIGNATURES = {
     "ks_node_exchange": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
     "ks_shard_info": (C.c_int, [C.c_void_p, _i64p, C.c_int64]),
     "ks_matvec": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "ks_kernel_matvec": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p,
+                                   C.c_void_p, C.c_int, C.c_void_p]),
     "ks_get_diag": (C.c_int, [C.c_void_p, C.POINTER(KsDiag)]),
     "ks_get_z_cond": (C.c_int64, [C.c_void_p, _i64p, _f64p, C.c_int64]),
     "ks_get_fallback_nodes": (C.c_int64, [C.c_void_p, _i64p, C.c_int64]),

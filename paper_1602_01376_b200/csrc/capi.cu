@@ -1544,6 +1544,65 @@ int ks_matvec(ks_factor* f, const double* W, double* Y, int64_t q, void* stream)
   return KS_OK;
 }
 
+int ks_kernel_matvec(const double* x_test, int64_t n_test, const double* x_train, int64_t n_train, int64_t d,
+                     double bandwidth, const double* w, double* out, int device, void* stream) {
+  if (n_test < 0 || n_train < 0 || d < 1) return fail(KS_ERR_INVALID, "bad sizes");
+  if (!(bandwidth > 0.0) || !std::isfinite(bandwidth))
+    return fail(KS_ERR_INVALID, "gaussian kernel needs bandwidth > 0, got %g", bandwidth);
+  if (n_test == 0) return KS_OK;
+  if (!x_test || !out || (n_train > 0 && (!x_train || !w))) return fail(KS_ERR_INVALID, "null argument");
+  KS_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool odev = is_device_ptr(out);
+  if (n_train == 0) {
+    if (odev) KS_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * n_test, st));
+    else std::fill(out, out + n_test, 0.0);
+    return KS_OK;
+  }
+  // coordinates padded to an even dimension (16-byte cp.async rows), norms, weights
+  const int64_t dp = d + (d & 1);
+  DBuf<double> xt, xr, xx, yy, wd, part, od;
+  KS_CUDA(xt.alloc((size_t)n_test * dp));
+  KS_CUDA(xr.alloc((size_t)n_train * dp));
+  KS_CUDA(xx.alloc((size_t)n_test));
+  KS_CUDA(yy.alloc((size_t)n_train));
+  KS_CUDA(wd.alloc((size_t)n_train));
+  if (dp != d) {
+    KS_CUDA(cudaMemsetAsync(xt.p, 0, sizeof(double) * n_test * dp, st));
+    KS_CUDA(cudaMemsetAsync(xr.p, 0, sizeof(double) * n_train * dp, st));
+  }
+  KS_CUDA(cudaMemcpy2DAsync(xt.p, sizeof(double) * dp, x_test, sizeof(double) * d, sizeof(double) * d, n_test,
+                            cudaMemcpyDefault, st));
+  KS_CUDA(cudaMemcpy2DAsync(xr.p, sizeof(double) * dp, x_train, sizeof(double) * d, sizeof(double) * d, n_train,
+                            cudaMemcpyDefault, st));
+  KS_CUDA(cudaMemcpyAsync(wd.p, w, sizeof(double) * n_train, cudaMemcpyDefault, st));
+  ks::launch_row_sqnorms(xt.p, n_test, dp, xx.p, st);
+  ks::launch_row_sqnorms(xr.p, n_train, dp, yy.p, st);
+  double* outd = out;
+  if (!odev) {
+    KS_CUDA(od.alloc((size_t)n_test));
+    outd = od.p;
+  }
+  // test rows in blocks so that the partial sums stay within ~256 MB
+  const int64_t tiles = (n_train + 63) / 64;
+  const int64_t rows_blk = std::max<int64_t>(64, std::min<int64_t>(n_test, (int64_t(1) << 25) / tiles / 64 * 64));
+  KS_CUDA(part.alloc((size_t)tiles * std::min(rows_blk, n_test)));
+  for (int64_t r0 = 0; r0 < n_test; r0 += rows_blk) {
+    const int m = (int)std::min(rows_blk, n_test - r0);
+    GemmArgs g = mk(m, (int)n_train, (int)dp, 1, Operand{xt.p + r0 * dp, dp, 0, nullptr},
+                    Operand{xr.p, dp, 0, nullptr}, OperandW{nullptr, 0, 0, nullptr}, 1.0, 0.0);
+    g.ke = ks::KrrEpi{xx.p + r0, yy.p, wd.p, part.p, 1.0 / (-2.0 * bandwidth * bandwidth)};
+    int nt = 0;
+    cudaError_t e = ks::gemm_krr(g, &nt, st);
+    if (e != cudaSuccess) return fail(KS_ERR_CUDA, "kernel matvec gemm: %s", cudaGetErrorString(e));
+    ks::launch_sum_partials(part.p, nt, m, outd + r0, st);
+  }
+  KS_CUDA(cudaGetLastError());
+  if (!odev) KS_CUDA(cudaMemcpyAsync(out, outd, sizeof(double) * n_test, cudaMemcpyDeviceToHost, st));
+  KS_CUDA(cudaStreamSynchronize(st));  // buffers are released on return
+  return KS_OK;
+}
+
 int ks_get_diag(const ks_factor* f, ks_diag* out) {
   if (!f || !out) return fail(KS_ERR_INVALID, "null argument");
   out->cholesky_fallbacks = (int64_t)f->fallback.size();

@@ -75,6 +75,13 @@ cudaError_t gemm_update_trsm(const GemmArgs& g, cudaStream_t st) {
   return launch<128, 64, 4, 2, false, true, 3, 2>(g, st);
 }
 
+cudaError_t gemm_krr(const GemmArgs& g, int* tiles, cudaStream_t st) {
+  *tiles = (g.N + 63) / 64;
+  if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+  if ((g.K & 1) || g.K <= 0 || ((g.A.ld | g.B.ld) & 1)) return cudaErrorInvalidValue;
+  return launch<64, 64, 2, 2, false, true, 3, 3>(g, st);
+}
+
 cudaError_t gemm(const GemmArgs& g, bool ta, bool tb, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
   if ((g.M | g.N | g.K) & 1) return cudaErrorInvalidValue;

@@ -36,6 +36,17 @@ struct GaussEpi {
   double h;
 };
 
+//   3  dense Gaussian cross-kernel matvec (krr_predict, solver.py:273-301):
+//      per row r of the tile, sum_c exp(max(xx_r + yy_c - 2G, 0) / (-2 h h)) w_c
+//      over the tile's valid columns -> partial[blockIdx.x][r] (no C written).
+struct KrrEpi {
+  const double* xx;  // squared norms of the test points (rows)
+  const double* yy;  // squared norms of the training points (columns)
+  const double* w;   // weights (columns)
+  double* partial;   // n_col_tiles x M
+  double den;        // 1 / (-2 h h)
+};
+
 struct GemmArgs {
   int M, N, K, batch;
   Operand A, B;
@@ -44,6 +55,7 @@ struct GemmArgs {
   int tri;  // 1: skip CTA tiles strictly above the diagonal of C
   GaussEpi ge;
   Operand E;  // EPI == 2: right factor of the epilogue product
+  KrrEpi ke;  // EPI == 3
 };
 
 template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
@@ -208,6 +220,40 @@ __global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
     }
     return;
   }
+  if constexpr (EPI == 3) {
+    __syncthreads();  // pipeline buffers become the cross-warp row reduction
+    double* red = smem;  // BM x WN
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; ++i) {
+      const int rl = wm0 + i * 8 + gq, r = m0 + rl;
+      const double xr = (r < g.M) ? g.ke.xx[r] : 0.0;
+      double sacc = 0.0;
+#pragma unroll
+      for (int j = 0; j < Cfg::NT; ++j) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c = n0 + wn0 + j * 8 + 2 * tq + u;
+          if (r < g.M && c < g.N) {
+            const double sq = fmax(xr + g.ke.yy[c] - 2.0 * acc[i][j][u], 0.0);
+            sacc = fma(exp(sq * g.ke.den), g.ke.w[c], sacc);
+          }
+        }
+      }
+      sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+      sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+      if (tq == 0) red[rl * WN + (warp % WN)] = sacc;
+    }
+    __syncthreads();
+    for (int rl = threadIdx.x; rl < BM; rl += Cfg::THREADS) {
+      const int r = m0 + rl;
+      if (r >= g.M) continue;
+      double s = 0.0;
+#pragma unroll
+      for (int w2 = 0; w2 < WN; ++w2) s += red[rl * WN + w2];
+      g.ke.partial[(int64_t)blockIdx.x * g.M + r] = s;
+    }
+    return;
+  }
   double den = 0.0, lam = 0.0;
   int bsz = 0, bbeg = 0;
   if (EPI == 1) {
@@ -265,5 +311,8 @@ cudaError_t gemm(const GemmArgs& g, bool ta, bool tb, cudaStream_t st);
 cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st);
 // Panel update with the panel TRSM folded in (EPI == 2): N must be 64, op(B) = B^T.
 cudaError_t gemm_update_trsm(const GemmArgs& g, cudaStream_t st);
+// Gaussian cross-kernel row sums (EPI == 3), op(B) = B^T: partial sums per
+// 64-column tile; returns the number of column tiles through *tiles.
+cudaError_t gemm_krr(const GemmArgs& g, int* tiles, cudaStream_t st);
 
 }  // namespace ks

@@ -51,6 +51,8 @@ struct NodeBatch {
 // --- factor launchers (factor_kernels.cu) ---
 void launch_gather_rows(const double* src, const int64_t* perm, int64_t n, int64_t d, double* dst, cudaStream_t st);
 void launch_row_sqnorms(const double* X, int64_t n, int64_t d, double* out, cudaStream_t st);
+// out[r] = sum_{t < tiles} partial[t * n + r], t ascending (deterministic)
+void launch_sum_partials(const double* partial, int tiles, int n, double* out, cudaStream_t st);
 void launch_leaf_copy_p(const DevTree& t, const LeafBatch& lb, cudaStream_t st);
 void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, const double* lam, cudaStream_t st);
 void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStream_t st);

@@ -235,4 +235,18 @@ void launch_mv_leaf(const DevTree& t, const LeafBatch& lb, const double* W, int6
   KS_QC(k_mv_leaf, grid, 256, 0, t, lb, W, ldw, tot, Y, S, q, q0, has_tot ? 1 : 0);
 }
 
+// krr_predict partial sums (EPI 3 of the DMMA GEMM) summed over column tiles
+__global__ void k_sum_partials(const double* partial, int tiles, int n, double* out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double s = 0.0;
+  for (int t = 0; t < tiles; ++t) s += partial[(int64_t)t * n + r];
+  out[r] = s;
+}
+
+void launch_sum_partials(const double* partial, int tiles, int n, double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_sum_partials<<<(n + 255) / 256, 256, 0, st>>>(partial, tiles, n, out);
+}
+
 }  // namespace ks

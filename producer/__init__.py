@@ -41,6 +41,23 @@ def make_operator(cfg: Config, device: str = "cuda", verbose: bool = False, samp
     return out
 
 
+def make_operator_from_points(coords: np.ndarray, leaf_size: int, h: float, max_rank: int = 256, tol: float = 1e-5,
+                              n_neighbors: int = 32, seed: int = 0, device: str = "cuda",
+                              sampling: str = "knn") -> dict:
+    """Operator inputs for given points (krr_fit's GPU producer): the bit-exact
+    tree restatement and the GPU skeletonization, CompressParams defaults
+    (compress.py:41-69) unless overridden."""
+    from .skeletons import skeletonize
+
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    tree = build_tree(coords, leaf_size)
+    sk = skeletonize(coords, tree, h, max_rank, tol, n_neighbors, seed, device, sampling)
+    out = {"coords": coords, "h": np.float64(h)}
+    out.update(tree)
+    out.update(sk)
+    return out
+
+
 def make_rhs(cfg: Config, perm: np.ndarray, q: int) -> np.ndarray:
     """(n, q) right-hand side in TREE order (cli.py:270-272 convention)."""
     return gen_rhs(cfg, q).reshape(cfg.n, q)[perm]
