@@ -8,7 +8,7 @@ LIB := paper_1602_01376_b200/libinvaskit.so
 
 all: $(LIB)
 
-build/%.o: paper_1602_01376_b200/csrc/%.cu $(wildcard paper_1602_01376_b200/csrc/*.cuh) include/invaskit.h
+build/%.o: paper_1602_01376_b200/csrc/%.cu $(wildcard paper_1602_01376_b200/csrc/*.cuh paper_1602_01376_b200/csrc/*.h) include/invaskit.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 

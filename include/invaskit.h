@@ -40,6 +40,7 @@ extern "C" {
 #define KS_ERR_ILL_COND 4     /* IllConditionedError(node, cond) (errors.py:29-39, solver.py:150-152) */
 #define KS_ERR_CUDA 5         /* device / runtime failure */
 #define KS_ERR_UNSUPPORTED 6  /* shape outside what the kernels handle */
+#define KS_ERR_IO 7           /* file missing, truncated or not in the KSINVASK container format */
 
 typedef struct ks_problem {
   int64_t n;                  /* points */
@@ -111,7 +112,26 @@ int ks_matvec(ks_factor* f, const double* W, double* Y, int64_t q, void* stream)
 int ks_kernel_matvec(const double* x_test, int64_t n_test, const double* x_train, int64_t n_train, int64_t d,
                      double bandwidth, const double* w, double* out, int device, void* stream);
 
+/* ---- persistence (operator inputs and factors; container layout in
+ * paper_1602_01376_b200/csrc/container.h). The reference persists
+ * only points (points.py:65-129, restated in paper_1602_01376_b200/persist.py);
+ * these cache the compression output and the factorization across runs. ---- */
+/* Write the operator inputs (coords, tree, skeletons, P, h) with a fingerprint. */
+int ks_save_problem(const ks_problem* prob, const char* path);
+/* Read them back; the arrays live in host memory owned by *owner until
+ * ks_free_problem(*owner). A fingerprint mismatch (corruption) is KS_ERR_IO. */
+int ks_load_problem(const char* path, ks_problem* out, void** owner);
+int ks_free_problem(void* owner);
+/* Save a factorized (unsharded) handle: factor buffers, lam, diagnostics and
+ * the fingerprint of `prob`, the operator it was created from. */
+int ks_save_factor(const ks_factor* f, const ks_problem* prob, const char* path);
+/* Recreate a factorized handle on `device` from `prob` and a factor file;
+ * KS_ERR_INVALID if the file was saved for a different operator. */
+int ks_load_factor(const char* path, const ks_problem* prob, int device, ks_factor** out);
+
 int ks_get_diag(const ks_factor* f, ks_diag* out);
+/* lam of the last factorization (HierFactor.lam, solver.py:77-89). */
+int ks_get_lam(const ks_factor* f, double* lam);
 /* Fill up to cap (node id, Z condition estimate) pairs, ascending node id. */
 int64_t ks_get_z_cond(const ks_factor* f, int64_t* nodes, double* conds, int64_t cap);
 /* Fill up to cap leaf node ids that fell back from Cholesky to LU. */

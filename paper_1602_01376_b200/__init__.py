@@ -8,6 +8,7 @@ reference compression, and the factor/solve runs in libinvaskit.so
 """
 
 from .errors import (
+    DataFormatError,
     DeviceError,
     IllConditionedError,
     InvalidArgumentError,
@@ -17,11 +18,13 @@ from .errors import (
 )
 from .problem import Problem, as_problem, from_arrays, from_compressed_kernel
 from .krr import krr_fit, krr_predict
+from .persist import load_factor, load_operator, load_points, save_factor, save_operator, save_points
 from .solver import GpuHierFactor, factorize, hss_matvec, solve, solve_many
 
 HierFactor = GpuHierFactor
 
 __all__ = [
+    "DataFormatError",
     "DeviceError",
     "GpuHierFactor",
     "HierFactor",
@@ -38,6 +41,12 @@ __all__ = [
     "hss_matvec",
     "krr_fit",
     "krr_predict",
+    "load_factor",
+    "load_operator",
+    "load_points",
+    "save_factor",
+    "save_operator",
+    "save_points",
     "solve",
     "solve_many",
 ]

@@ -13,7 +13,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libinvaskit.so")
 
-KS_OK, KS_ERR_INVALID, KS_ERR_NOT_SPD, KS_ERR_SINGULAR, KS_ERR_ILL_COND, KS_ERR_CUDA, KS_ERR_UNSUPPORTED = range(7)
+(KS_OK, KS_ERR_INVALID, KS_ERR_NOT_SPD, KS_ERR_SINGULAR, KS_ERR_ILL_COND, KS_ERR_CUDA, KS_ERR_UNSUPPORTED,
+ KS_ERR_IO) = range(8)
 
 _i64p = C.POINTER(C.c_int64)
 _f64p = C.POINTER(C.c_double)
@@ -65,7 +66,13 @@ SIGNATURES = {
     "ks_matvec": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "ks_kernel_matvec": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p,
                                    C.c_void_p, C.c_int, C.c_void_p]),
+    "ks_save_problem": (C.c_int, [C.POINTER(KsProblem), C.c_char_p]),
+    "ks_load_problem": (C.c_int, [C.c_char_p, C.POINTER(KsProblem), C.POINTER(C.c_void_p)]),
+    "ks_free_problem": (C.c_int, [C.c_void_p]),
+    "ks_save_factor": (C.c_int, [C.c_void_p, C.POINTER(KsProblem), C.c_char_p]),
+    "ks_load_factor": (C.c_int, [C.c_char_p, C.POINTER(KsProblem), C.c_int, C.POINTER(C.c_void_p)]),
     "ks_get_diag": (C.c_int, [C.c_void_p, C.POINTER(KsDiag)]),
+    "ks_get_lam": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "ks_get_z_cond": (C.c_int64, [C.c_void_p, _i64p, _f64p, C.c_int64]),
     "ks_get_fallback_nodes": (C.c_int64, [C.c_void_p, _i64p, C.c_int64]),
     "ks_get_node_h": (C.c_int, [C.c_void_p, C.c_int64, _f64p]),

@@ -29,7 +29,7 @@ def _coords(points) -> np.ndarray:
 
 
 def _bandwidth(spec) -> float:
-    name = getattr(spec, "name", "gaussian")
+    name = getattr(spec, "family", "gaussian")
     if name != "gaussian":  # the GPU path implements the Gaussian kernel (kernels.py:29-59)
         raise InvalidArgumentError(f"unsupported kernel {name!r}: the B200 path implements 'gaussian'")
     h = float(getattr(spec, "bandwidth", spec))

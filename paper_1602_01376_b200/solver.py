@@ -20,8 +20,10 @@ import os
 import numpy as np
 
 from . import _lib
-from ._lib import KS_ERR_CUDA, KS_ERR_ILL_COND, KS_ERR_INVALID, KS_ERR_NOT_SPD, KS_ERR_SINGULAR, KS_ERR_UNSUPPORTED, KsDiag
+from ._lib import (KS_ERR_CUDA, KS_ERR_ILL_COND, KS_ERR_INVALID, KS_ERR_IO, KS_ERR_NOT_SPD, KS_ERR_SINGULAR,
+                   KS_ERR_UNSUPPORTED, KsDiag)
 from .errors import (
+    DataFormatError,
     DeviceError,
     IllConditionedError,
     InvalidArgumentError,
@@ -50,6 +52,8 @@ def _raise(rc: int, handle=None):
         raise DeviceError(msg)
     if rc == KS_ERR_UNSUPPORTED:
         raise InvalidArgumentError(msg)
+    if rc == KS_ERR_IO:
+        raise DataFormatError(msg)
     raise KernelSolveError(f"libinvaskit error {rc}: {msg}")
 
 
