@@ -343,8 +343,8 @@ def run_ours(args) -> None:
         "factor_ms": ms_fac,
         "solve_ms": ms_sol,
         f"solve_ms_q{q32}": ms_sol_q,
-        "factor_phase_ms_eager": {"leaf_assemble": ph[0], "leaf_cholesky": ph[1], "leaf_syrk": ph[2],
-                            "internal_levels": ph[3], "total": ph[4]} if ph else None,
+        "factor_phase_ms_eager": {"leaves": ph[0] + ph[1] + ph[2], "internal_levels": ph[3],
+                                  "total": ph[4]} if ph else None,
         "level_ms": levels_ms,
         "yardstick": {"factor_tflop": F / 1e12, "solve_gb_q1": B_solve / 1e9},
         "roofline": {"bound": "tensor", "achieved": F / (ms_fac * 1e-3) / 1e12, "peak": fp64_peak,

@@ -6,8 +6,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <string>
 #include <type_traits>
+#include <thread>
 #include <vector>
 
 #include "../../include/invaskit.h"
@@ -115,6 +117,12 @@ struct ks_factor {
   int64_t n_factorizations = 0;
   DBuf<double> lam_dev;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // uploads started by ks_create, consumed by the first factorization
+  static constexpr int kLeafChunks = 4;
+  cudaStream_t upl = nullptr;
+  cudaEvent_t ev_up_coords = nullptr, ev_up_all = nullptr, ev_up_leaf[kLeafChunks] = {};
+  std::vector<cudaEvent_t> ev_up_level;
+  bool upload_pending = false;
   // diagnostics
   std::vector<int> leaf_info_h, int_info_h;
   std::vector<double> cond_h;
@@ -401,7 +409,23 @@ int ks_last_error(char* buf, int64_t len) {
 
 const char* ks_version(void) { return "libinvaskit 0.1 sm_100a (DMMA fp64, telescoping solve)"; }
 
+static double host_ms() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+}
+
+static bool host_timing() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("KS_HOST_TIMING");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor** out) {
+  const double t_start = host_ms();
   if (!p || !out) return fail(KS_ERR_INVALID, "null argument");
   *out = nullptr;
   if (p->n < 1 || p->d < 1 || p->n_nodes < 1) return fail(KS_ERR_INVALID, "empty problem");
@@ -515,15 +539,15 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
   f->pw = (f->T <= 1024) ? 16 : 8;
   if (f->T > 2048) { delete f; return fail(KS_ERR_UNSUPPORTED, "skeleton rank %lld too large (max 682)", (long long)s_max); }
 
-  // host-side checks and small tables (large arrays go to the device directly)
+  const double t_plan = host_ms();
+  // the permutation first: the device gather of the points trusts it
   std::vector<int64_t> pos(p->n, -1);
   for (int64_t i = 0; i < p->n; ++i) {
     const int64_t id = p->perm[i];
     if (id < 0 || id >= p->n || pos[id] >= 0) return bad("perm is not a permutation");
     pos[id] = i;
   }
-  for (int64_t i = 0, e = p->n * p->d; i < e; ++i)
-    if (!std::isfinite(p->coords[i])) return bad("coords contain non-finite values");
+  const size_t nl = f->leaf_nodes.size();
   const int64_t nsk = p->skel_off[nn];
   std::vector<int> sp((size_t)nsk);
   for (int64_t i = 0; i < nsk; ++i) {
@@ -546,38 +570,23 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     ileft.push_back((int)f->left[v]);
     iright.push_back((int)f->right[v]);
   }
-  const size_t nl = f->leaf_nodes.size();
-  auto up = [&]() -> int {
-    {  // points to tree order on the device: coords_tree[i] = coords[perm[i]]
-      DBuf<double> orig;
-      DBuf<int64_t> pm;
-      KS_CUDA(orig.alloc((size_t)p->n * p->d));
-      KS_CUDA(pm.alloc((size_t)p->n));
-      KS_CUDA(f->coords.alloc((size_t)(p->n + f->m_pad) * p->d));
-      KS_CUDA(cudaMemset(f->coords.p + (size_t)p->n * p->d, 0, sizeof(double) * f->m_pad * p->d));
-      KS_CUDA(cudaMemcpy(orig.p, p->coords, sizeof(double) * p->n * p->d, cudaMemcpyHostToDevice));
-      KS_CUDA(cudaMemcpy(pm.p, p->perm, sizeof(int64_t) * p->n, cudaMemcpyHostToDevice));
-      ks::launch_gather_rows(orig.p, pm.p, p->n, p->d, f->coords.p, nullptr);
-      KS_CUDA(f->xx.alloc((size_t)p->n + f->m_pad));
-      ks::launch_row_sqnorms(f->coords.p, p->n + f->m_pad, p->d, f->xx.p, nullptr);
-      KS_CUDA(cudaDeviceSynchronize());
-      orig.release();
-      pm.release();
-    }
-    KS_CUDA(f->rank_d.upload(rk));
-    KS_CUDA(f->skel_pos.upload(sp));
-    KS_CUDA(f->skel_off.upload(so));
-    KS_CUDA(f->coeff_off.upload(co));
-    KS_CUDA(f->coeff.alloc((size_t)p->coeff_off[nn]));
-    if (p->coeff_off[nn] > 0)
-      KS_CUDA(cudaMemcpy(f->coeff.p, p->coeff, sizeof(double) * p->coeff_off[nn], cudaMemcpyHostToDevice));
-    KS_CUDA(f->leaf_node.upload(ln));
-    KS_CUDA(f->leaf_begin.upload(lbg));
-    KS_CUDA(f->leaf_size.upload(lsz));
+  // From here on the handle owns device memory and streams: errors go through ks_destroy.
+  auto abort_create = [&](int rc) {
+    ks_destroy(f);
+    return rc;
+  };
+  auto alloc_all = [&]() -> int {
+    KS_CUDA(f->rank_d.alloc(rk.size()));
+    KS_CUDA(f->skel_pos.alloc(sp.size()));
+    KS_CUDA(f->skel_off.alloc(so.size()));
+    KS_CUDA(f->coeff_off.alloc(co.size()));
+    KS_CUDA(f->leaf_node.alloc(ln.size()));
+    KS_CUDA(f->leaf_begin.alloc(lbg.size()));
+    KS_CUDA(f->leaf_size.alloc(lsz.size()));
     KS_CUDA(f->leaf_info.alloc(nl));
-    KS_CUDA(f->int_node.upload(inode));
-    KS_CUDA(f->int_left.upload(ileft));
-    KS_CUDA(f->int_right.upload(iright));
+    KS_CUDA(f->int_node.alloc(inode.size()));
+    KS_CUDA(f->int_left.alloc(ileft.size()));
+    KS_CUDA(f->int_right.alloc(iright.size()));
     KS_CUDA(f->int_info.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->piv.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
     KS_CUDA(f->moves.alloc((size_t)std::max(f->n_int, 1) * (2 * 64 + 1)));
@@ -592,6 +601,9 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     KS_CUDA(f->pn.alloc((size_t)f->n_int * f->s_pad * f->t_pad + 1));
     KS_CUDA(f->norm1.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->cond.alloc(std::max(f->n_int, 1)));
+    KS_CUDA(f->coords.alloc((size_t)(p->n + f->m_pad) * p->d));
+    KS_CUDA(f->xx.alloc((size_t)p->n + f->m_pad));
+    KS_CUDA(f->coeff.alloc((size_t)p->coeff_off[nn]));
     KS_CUDA(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
     KS_CUDA(cudaStreamCreateWithFlags(&f->cap, cudaStreamNonBlocking));
     for (auto& g : f->gst) KS_CUDA(cudaStreamCreateWithFlags(&g, cudaStreamNonBlocking));
@@ -605,12 +617,109 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_join, cudaEventDisableTiming));
     return KS_OK;
   };
-  int rc = up();
-  if (rc) {
-    f->release_all();
-    delete f;
-    return rc;
+  if (int rc = alloc_all()) return abort_create(rc);
+  const double t_alloc = host_ms();
+  // ---- asynchronous uploads on the upload stream, in the order the first
+  // factorization consumes them; the point-coordinate check overlaps the DMA.
+  // Points: tree order on the device (coords_tree[i] = coords[perm[i]]) + norms.
+  auto start_uploads = [&]() -> int {
+    KS_CUDA(cudaStreamCreateWithFlags(&f->upl, cudaStreamNonBlocking));
+    KS_CUDA(cudaEventCreateWithFlags(&f->ev_up_coords, cudaEventDisableTiming));
+    KS_CUDA(cudaEventCreateWithFlags(&f->ev_up_all, cudaEventDisableTiming));
+    for (auto& e : f->ev_up_leaf) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    f->ev_up_level.resize(f->levels.size());
+    for (auto& e : f->ev_up_level) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaStream_t u = f->upl;
+    // the small tables first (pageable sources: staged before the call returns)
+    auto put = [&](auto& buf, const auto& v) -> int {
+      if (!v.empty()) KS_CUDA(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, u));
+      return KS_OK;
+    };
+    if (int rc = put(f->rank_d, rk)) return rc;
+    if (int rc = put(f->skel_pos, sp)) return rc;
+    if (int rc = put(f->skel_off, so)) return rc;
+    if (int rc = put(f->coeff_off, co)) return rc;
+    if (int rc = put(f->leaf_node, ln)) return rc;
+    if (int rc = put(f->leaf_begin, lbg)) return rc;
+    if (int rc = put(f->leaf_size, lsz)) return rc;
+    if (int rc = put(f->int_node, inode)) return rc;
+    if (int rc = put(f->int_left, ileft)) return rc;
+    if (int rc = put(f->int_right, iright)) return rc;
+    double* orig = nullptr;
+    int64_t* pmd = nullptr;
+    KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&orig), sizeof(double) * p->n * p->d, u));
+    KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pmd), sizeof(int64_t) * p->n, u));
+    KS_CUDA(cudaMemsetAsync(f->coords.p + (size_t)p->n * p->d, 0, sizeof(double) * f->m_pad * p->d, u));
+    KS_CUDA(cudaMemcpyAsync(orig, p->coords, sizeof(double) * p->n * p->d, cudaMemcpyHostToDevice, u));
+    KS_CUDA(cudaMemcpyAsync(pmd, p->perm, sizeof(int64_t) * p->n, cudaMemcpyHostToDevice, u));
+    ks::launch_gather_rows(orig, pmd, p->n, p->d, f->coords.p, u);
+    ks::launch_row_sqnorms(f->coords.p, p->n + f->m_pad, p->d, f->xx.p, u);
+    KS_CUDA(cudaFreeAsync(orig, u));
+    KS_CUDA(cudaFreeAsync(pmd, u));
+    KS_CUDA(cudaEventRecord(f->ev_up_coords, u));
+    // P blocks: leaves in leaf order (a milestone event per leaf quarter), then
+    // internal nodes level by level, deepest first (an event per level), then
+    // whatever this handle does not factor; contiguous ranges are coalesced
+    std::vector<char> sent(nn, 0);
+    int64_t r0 = -1, r1 = -1;
+    auto flush = [&]() -> int {
+      if (r1 > r0) KS_CUDA(cudaMemcpyAsync(f->coeff.p + r0, p->coeff + r0, sizeof(double) * (r1 - r0),
+                                           cudaMemcpyHostToDevice, u));
+      r0 = r1 = -1;
+      return KS_OK;
+    };
+    auto add = [&](int64_t v) -> int {
+      sent[v] = 1;
+      const int64_t a0 = p->coeff_off[v], a1 = p->coeff_off[v + 1];
+      if (a1 <= a0) return KS_OK;
+      if (a0 == r1) { r1 = a1; return KS_OK; }
+      if (int rc = flush()) return rc;
+      r0 = a0;
+      r1 = a1;
+      return KS_OK;
+    };
+    for (int c = 0; c < ks_factor::kLeafChunks; ++c) {
+      const size_t l0 = nl * c / ks_factor::kLeafChunks, l1 = nl * (c + 1) / ks_factor::kLeafChunks;
+      for (size_t li = l0; li < l1; ++li)
+        if (int rc = add(f->leaf_nodes[li])) return rc;
+      if (int rc = flush()) return rc;
+      KS_CUDA(cudaEventRecord(f->ev_up_leaf[c], u));
+    }
+    for (size_t lev = 0; lev < f->levels.size(); ++lev) {
+      for (int v : f->levels[lev])
+        if (int rc = add(v)) return rc;
+      if (int rc = flush()) return rc;
+      KS_CUDA(cudaEventRecord(f->ev_up_level[lev], u));
+    }
+    for (int64_t v = 0; v < nn; ++v)
+      if (!sent[v])
+        if (int rc = add(v)) return rc;
+    if (int rc = flush()) return rc;
+    KS_CUDA(cudaEventRecord(f->ev_up_all, u));
+    f->upload_pending = true;
+    return KS_OK;
+  };
+  if (int rc = start_uploads()) return abort_create(rc);
+  const double t_issue = host_ms();
+  // ---- host checks while the copies run: point coordinates on worker threads
+  {
+    const int64_t total = p->n * p->d;
+    const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(8, total / (1 << 20)));
+    std::vector<char> ok(nth, 1);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nth; ++t)
+      th.emplace_back([&, t]() {
+        const int64_t a = total * t / nth, b = total * (t + 1) / nth;
+        for (int64_t i = a; i < b; ++i)
+          if (!std::isfinite(p->coords[i])) { ok[t] = 0; return; }
+      });
+    for (auto& x : th) x.join();
+    for (char c : ok)
+      if (!c) return abort_create(fail(KS_ERR_INVALID, "coords contain non-finite values"));
   }
+  if (host_timing())
+    std::fprintf(stderr, "[ks_create] plan %.1f tables+alloc %.1f issue %.1f checks %.1f ms (uploads in flight)\n",
+                 t_plan - t_start, t_alloc - t_plan, t_issue - t_alloc, host_ms() - t_issue);
   *out = f;
   return KS_OK;
 }
@@ -627,6 +736,35 @@ int ks_create_shard(const ks_problem* p, int device, int64_t shard_root, ks_fact
 // Leaves [l0, l1): left-looking Cholesky of the (m+s) x m trapezoids in 64-column
 // panels (panel update GEMM, 64x64 POTRF + inverse, panel TRSM as GEMM with the
 // inverse), then H = L21 L21^T (solver.py:123-135).
+// Leaves [l0, l1): K(X_leaf, X_leaf) + lam I (lower triangle) and the P rows of
+// the trapezoid [[A], [P]].
+static int enqueue_leaf_assemble(ks_factor* f, Launcher& L, int l0, int l1) {
+  if (l1 <= l0) return KS_OK;
+  const ks::DevTree dt = f->devtree();
+  const ks::LeafBatch all = f->leafbatch();
+  ks::LeafBatch lb = all;
+  lb.count = l1 - l0;
+  lb.node = all.node + l0;
+  lb.begin = all.begin + l0;
+  lb.size = all.size + l0;
+  lb.A = all.A + (int64_t)l0 * all.a_stride;
+  const int M = f->m_pad;
+  if ((f->d & 1) == 0) {
+    // a DMMA Gram GEMM with the Gaussian epilogue
+    GemmArgs g = mk(M, M, (int)f->d, lb.count, Operand{f->coords.p, f->d, f->d, lb.begin},
+                    Operand{f->coords.p, f->d, f->d, lb.begin}, OperandW{lb.A, M, lb.a_stride, nullptr}, 1.0, 0.0);
+    g.ge = ks::GaussEpi{f->xx.p, lb.begin, lb.size, f->lam_dev.p, f->h};
+    ++L.count[0];
+    cudaError_t e = ks::gemm_gauss(g, L.st);
+    if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf gauss gemm: %s", cudaGetErrorString(e));
+    ks::launch_leaf_copy_p(dt, lb, L.st);
+  } else {
+    ks::launch_leaf_assemble(dt, lb, f->lam_dev.p, L.st);
+  }
+  L.count[0] += 1;
+  return L.check("leaf_assemble");
+}
+
 // KS_UNFUSED_LEAF_TRSM=1: separate update and TRSM GEMMs per leaf panel (A/B check)
 static bool unfused_leaf_trsm() {
   const char* e = std::getenv("KS_UNFUSED_LEAF_TRSM");
@@ -723,27 +861,12 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   if (int rc = mark(f->ev_phase[0])) return rc;
   KS_CUDA(cudaMemsetAsync(f->leaf_info.p, 0, sizeof(int) * nl, st));
   if (f->n_int) KS_CUDA(cudaMemsetAsync(f->int_info.p, 0, sizeof(int) * f->n_int, st));
-  // ---- leaves: assemble [[K + lam I], [P]] ----
+  // ---- leaves: assemble [[K + lam I], [P]] and factor, leaves split into
+  // independent groups on their own streams; on the first factorization each
+  // group waits only for the uploads of its own P blocks
+  if (f->upload_pending) KS_CUDA(cudaStreamWaitEvent(st, f->ev_up_coords, 0));
   if (int rc = L.check("start")) return rc;
-  if ((f->d & 1) == 0) {
-    // K(X_leaf, X_leaf) + lam I as a DMMA Gram GEMM with the Gaussian epilogue
-    GemmArgs g = mk(M, M, (int)f->d, nl, Operand{f->coords.p, f->d, f->d, f->leaf_begin.p},
-                    Operand{f->coords.p, f->d, f->d, f->leaf_begin.p}, OperandW{f->leafA.p, M, lb.a_stride, nullptr},
-                    1.0, 0.0);
-    g.ge = ks::GaussEpi{f->xx.p, f->leaf_begin.p, f->leaf_size.p, f->lam_dev.p, f->h};
-    ++L.count[0];
-    cudaError_t e = ks::gemm_gauss(g, st);
-    if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf gauss gemm: %s", cudaGetErrorString(e));
-    ks::launch_leaf_copy_p(dt, lb, st);
-  } else {
-    ks::launch_leaf_assemble(dt, lb, f->lam_dev.p, st);
-  }
-  L.count[0] += 1;
-  if (int rc = L.check("leaf_assemble")) return rc;
-  KS_CUDA(cudaGetLastError());
   if (int rc = mark(f->ev_phase[1])) return rc;
-  // ---- left-looking Cholesky of the trapezoid (64-column panels) and the
-  // SYRK H = L21 L21^T, leaves split into independent groups on their own streams
   {
     const int G = (nl >= 2 * 64) ? n_groups() : 1;
     if (G > 1) {
@@ -753,7 +876,13 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
     for (int g = 0; g < G; ++g) {
       const int l0 = (int)((int64_t)nl * g / G), l1 = (int)((int64_t)nl * (g + 1) / G);
       cudaStream_t gs = (G > 1) ? f->gst[g] : st;
+      if (f->upload_pending && l1 > l0) {
+        int c = 0;  // the upload chunk holding this group's last leaf
+        while ((int64_t)nl * (c + 1) / ks_factor::kLeafChunks <= l1 - 1) ++c;
+        KS_CUDA(cudaStreamWaitEvent(gs, f->ev_up_leaf[c], 0));
+      }
       Launcher Lg{f, gs, &f->launches[0]};
+      if (int rc = enqueue_leaf_assemble(f, Lg, l0, l1)) return rc;
       if (int rc = enqueue_leaf_chol(f, Lg, l0, l1)) return rc;
     }
     if (G > 1)
@@ -887,6 +1016,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
   };
   for (int lev = lev0; lev < lev1; ++lev) {
     f->cur_tag = (int)lev;
+    if (f->upload_pending) KS_CUDA(cudaStreamWaitEvent(st, f->ev_up_level[lev], 0));
     const ks::NodeBatch nb = f->nodebatch((int)lev);
     const bool is_root_level = (f->levels[lev][0] == 0);
     const bool wide = nb.count >= 64;
@@ -1032,6 +1162,10 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
   // (KS_GRAPH=1, default), always (2) or never (0); tracing runs eagerly.
   const int gm = (trace_on() || debug_sync() || f->profiling) ? 0 : graph_mode();
   const bool use_graph = gm == 2 || (gm == 1 && f->n_factorizations > 0);
+  if (use_graph && f->upload_pending) {  // a graph does not capture waits on the upload stream
+    KS_CUDA(cudaStreamSynchronize(f->upl));
+    f->upload_pending = false;
+  }
   if (use_graph) {
     if (!f->graph_exec || f->graph_profiling != f->profiling) {
       if (f->graph_exec) { cudaGraphExecDestroy(f->graph_exec); f->graph_exec = nullptr; }
@@ -1051,6 +1185,10 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
   } else {
     int rc = enqueue_factorization(f, st);
     if (rc) return rc;
+    if (f->upload_pending) {  // everything after this point sees every upload
+      KS_CUDA(cudaStreamWaitEvent(st, f->ev_up_all, 0));
+      f->upload_pending = false;
+    }
   }
   ++f->n_factorizations;
   // leaf Cholesky failures (NotSPD) -> LU fallback for those leaves (solver.py:125-131)
@@ -2006,6 +2144,11 @@ int ks_load_factor(const char* path, const ks_problem* p, int device, ks_factor*
     return fail(KS_ERR_INVALID, "%s: the factor was computed for a different operator", path);
   ks_factor* f = nullptr;
   if (int rc = create_impl(p, device, 0, &f)) return rc;
+  if (cudaStreamSynchronize(f->upl) != cudaSuccess) {  // no factorization will wait for the uploads
+    ks_destroy(f);
+    return fail(KS_ERR_CUDA, "upload failed");
+  }
+  f->upload_pending = false;
   auto bad = [&](int rc) {
     ks_destroy(f);
     return rc;
@@ -2073,6 +2216,13 @@ void ks_destroy(ks_factor* f) {
   f->lam_dev.release();
   if (f->ev_fork) cudaEventDestroy(f->ev_fork);
   if (f->ev_join) cudaEventDestroy(f->ev_join);
+  if (f->upl) cudaStreamDestroy(f->upl);
+  if (f->ev_up_coords) cudaEventDestroy(f->ev_up_coords);
+  if (f->ev_up_all) cudaEventDestroy(f->ev_up_all);
+  for (auto e : f->ev_up_leaf)
+    if (e) cudaEventDestroy(e);
+  for (auto e : f->ev_up_level)
+    if (e) cudaEventDestroy(e);
   delete f;
 }
 
