@@ -302,10 +302,18 @@ def run_ours(args) -> None:
     u = X.cpu().numpy()
     del X, XQ
     # e2e through the public API from pinned host memory
+    # what the JSON line needs from the device-resident factor, then release it
+    # (and torch's cached blocks) so the public-API calls below run as a user's would
+    dev_bytes = hf.device_bytes()
+    max_zc = max(hf.diagnostics["z_cond"].values())
+    n_fallbacks = hf.diagnostics["cholesky_fallbacks"]
+    hf.close()
+    del hf, B1, BQ
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     pin, h2d = _pinned_problem(torch, op)
     pin_prob = ks.from_arrays(pin)
     b_pin = torch.from_numpy(b1).pin_memory().numpy()
-    hf_keep = hf
     e2e_fac, e2e_sol = [], []
     for i in range(max(2, min(args.steps, 3))):
         torch.cuda.synchronize()
@@ -339,7 +347,7 @@ def run_ours(args) -> None:
         "data": "synthetic (config-3 recipe points from the reference RNG; tree restated bit-exactly; skeletons/P by a GPU restatement of the reference ID with kNN-guided sampling)",
         "config": {"workload": f"{cfg.name} factor+solve q=1", "n": cfg.n, "d": cfg.d, "leaf": cfg.leaf_size,
                    "rank": cfg.max_rank, "h": cfg.h, "lambda": cfg.lam, "q": 1,
-                   "l2": "inputs larger than L2 (factor working set %.1f GB)" % (hf_keep.device_bytes() / 1e9)},
+                   "l2": "inputs larger than L2 (factor working set %.1f GB)" % (dev_bytes / 1e9)},
         "factor_ms": ms_fac,
         "solve_ms": ms_sol,
         f"solve_ms_q{q32}": ms_sol_q,
@@ -361,8 +369,7 @@ def run_ours(args) -> None:
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "producer_s": t_prod,
-        "diagnostics": {"max_z_cond": max(hf_keep.diagnostics["z_cond"].values()),
-                        "cholesky_fallbacks": hf_keep.diagnostics["cholesky_fallbacks"]},
+        "diagnostics": {"max_z_cond": max_zc, "cholesky_fallbacks": n_fallbacks},
     }
     if cpu is not None:
         line["cpu_baseline"] = {"value": cpu["factor_tflops"], "unit": "TFLOP/s", "cores": cpu["cores"], "kind": "port",

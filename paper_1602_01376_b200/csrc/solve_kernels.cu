@@ -21,7 +21,7 @@ namespace ks {
 // leaf up: z = L^-1 b, c = L21 z
 // ---------------------------------------------------------------------------
 template <int QC>
-__global__ void __launch_bounds__(STHREADS) k_leaf_fwd(LeafBatch lb, const double* B, int64_t ldb, SolveBufs sb,
+__global__ void __launch_bounds__(STHREADS, 8) k_leaf_fwd(LeafBatch lb, const double* B, int64_t ldb, SolveBufs sb,
                                                         int q0) {
   extern __shared__ double x[];  // m_pad x QC
   __shared__ double D[SB][SB + 1];
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(STHREADS) k_leaf_fwd(LeafBatch lb, const doubl
 // leaf down: x = L^-T (z - L21^T t)
 // ---------------------------------------------------------------------------
 template <int QC>
-__global__ void __launch_bounds__(STHREADS) k_leaf_bwd(LeafBatch lb, double* X, int64_t ldx, SolveBufs sb, int q0,
+__global__ void __launch_bounds__(STHREADS, 8) k_leaf_bwd(LeafBatch lb, double* X, int64_t ldx, SolveBufs sb, int q0,
                                                         int has_tin) {
   extern __shared__ double sm[];
   double* x = sm;                       // m_pad x QC
