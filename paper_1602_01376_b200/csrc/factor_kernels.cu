@@ -119,13 +119,16 @@ void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, const double* l
 // Failure (pivot <= 0 or non-finite) records the first bad column + 1, as
 // _cholesky raises NotSPDError at linalg.py:190-192.
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_potrf64(LeafBatch lb, int j0, double* inv, int* info) {
+__global__ void __launch_bounds__(256, 6) k_potrf64(LeafBatch lb, int j0, double* inv, int* info) {
   const int leaf = blockIdx.x;
   double* A = lb.A + (int64_t)leaf * lb.a_stride + (int64_t)j0 * lb.m_pad + j0;
   const int64_t ld = lb.m_pad;
+  // one 64 x 65 tile: L in the lower triangle, X = L^-1 (also lower) stored
+  // transposed in the strict upper triangle (x[i][j] at a[j][i], i > j) with its
+  // diagonal in xd: 34 KB, so six CTAs share an SM
   extern __shared__ double potrf_sm[];
   double(*a)[65] = reinterpret_cast<double(*)[65]>(potrf_sm);
-  double(*x)[65] = reinterpret_cast<double(*)[65]>(potrf_sm + 64 * 65);
+  double* xd = potrf_sm + 64 * 65;
   __shared__ int bad;
   {  // all 16 loads per thread in flight
     double v[16];
@@ -138,8 +141,8 @@ __global__ void __launch_bounds__(256) k_potrf64(LeafBatch lb, int j0, double* i
     for (int u = 0; u < 16; ++u) {
       const int e = threadIdx.x + u * 256, r = e >> 6, c = e & 63;
       a[r][c] = v[u];
-      x[r][c] = (r == c) ? 1.0 : 0.0;
     }
+    if (threadIdx.x < 64) xd[threadIdx.x] = 1.0;
   }
   if (threadIdx.x == 0) bad = 0x7fffffff;
   __syncthreads();
@@ -179,17 +182,23 @@ __global__ void __launch_bounds__(256) k_potrf64(LeafBatch lb, int j0, double* i
   }
   __syncthreads();
   // X = L^-1 right-looking: rows below k lose L[i][k] X[k] / L[k][k], then row
-  // k is scaled; one barrier per step
+  // k is scaled; one barrier per step. x[i][j] (i > j) lives at a[j][i].
   for (int k = 0; k < 64; ++k) {
     const double rk = 1.0 / a[k][k];
     const int cols = k + 1;
     const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
     for (int i = k + 1 + ti; i < 64; i += 16) {
       const double li = a[i][k] * rk;
-      for (int j = tj; j < cols; j += 16) x[i][j] = fma(-li, x[k][j], x[i][j]);
+      for (int j = tj; j < cols; j += 16) {
+        const double xkj = (j == k) ? xd[k] : a[j][k];
+        a[j][i] = fma(-li, xkj, a[j][i]);
+      }
     }
     __syncthreads();
-    if (threadIdx.x < cols) x[k][threadIdx.x] *= rk;
+    if (threadIdx.x < cols) {
+      if (threadIdx.x == k) xd[k] *= rk;
+      else a[threadIdx.x][k] *= rk;
+    }
   }
   __syncthreads();
   double* iv = inv + ((int64_t)leaf * (lb.m_pad / 64) + j0 / 64) * 64 * 64;
@@ -197,13 +206,13 @@ __global__ void __launch_bounds__(256) k_potrf64(LeafBatch lb, int j0, double* i
   for (int e = threadIdx.x; e < 64 * 64; e += 256) {
     const int r = e >> 6, c = e & 63;
     A[r * ld + c] = (c <= r) ? a[r][c] : 0.0;
-    iv[e] = x[r][c];
+    iv[e] = (c < r) ? a[c][r] : (c == r ? xd[r] : 0.0);
   }
   if (threadIdx.x == 0 && bad != 0x7fffffff && info[leaf] == 0) info[leaf] = j0 + bad + 1;
 }
 
 void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStream_t st) {
-  constexpr size_t smem = 2 * 64 * 65 * sizeof(double);
+  constexpr size_t smem = (64 * 65 + 64) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_potrf64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -384,8 +393,8 @@ __device__ __forceinline__ void warp_argmax(double v, int p, unsigned& mh, unsig
   mp = (int)__reduce_min_sync(0xffffffffu, top ? (unsigned)p : 0x7fffffffu);
 }
 
-template <int W, int RPT, int NT>
-__global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, int pc0, int ph, int pcols) {
+template <int W, int RPT, int NT, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) k_lu_panel(NodeBatch nb, int c0, int pr0, int pc0, int ph, int pcols) {
   constexpr int NW = NT / 32;
   constexpr int NONE = 0x7fffffff;
   constexpr int CB = 4;       // columns per unrolled block
@@ -545,20 +554,22 @@ __global__ void __launch_bounds__(NT) k_lu_panel(NodeBatch nb, int c0, int pr0, 
   }
 }
 
-template <int W, int RPT, int NT>
+template <int W, int RPT, int NT, int MINB = 1>
 static void launch_panel(const NodeBatch& nb, int c0, cudaStream_t st, const int* pend) {
   const size_t smem = (size_t)std::max((nb.T - c0) * (W + 2), 2 * W * 256) * sizeof(double);
   static size_t set = 0;
   if (smem > set) {
-    cudaFuncSetAttribute(k_lu_panel<W, RPT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_lu_panel<W, RPT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set = smem;
   }
-  k_lu_panel<W, RPT, NT><<<nb.count, NT, smem, st>>>(nb, c0, pend[0], pend[1], pend[2], pend[3]);
+  k_lu_panel<W, RPT, NT, MINB><<<nb.count, NT, smem, st>>>(nb, c0, pend[0], pend[1], pend[2], pend[3]);
 }
 
 template <int W>
 static void launch_panel_w(const NodeBatch& nb, int c0, cudaStream_t st, const int* pend) {
-  // 512 threads (16 warps hide the per-column latency), rows in registers
+  // 512 threads (16 warps hide the per-column latency), rows in registers.
+  // (A 256-thread, two-CTAs-per-SM variant for batches wider than the GPU
+  // measured no better: the two node-group streams already fill the SMs.)
   const int rows = nb.T - c0;
   if (rows <= 512) launch_panel<W, 1, 512>(nb, c0, st, pend);
   else if (rows <= 1024) launch_panel<W, 2, 512>(nb, c0, st, pend);
