@@ -1,6 +1,8 @@
 // Shared device helpers for libinvaskit (sm_100a only).
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -63,5 +65,41 @@ struct OperandW {
     return ptr + (idx ? (int64_t)idx[b] : (int64_t)b) * stride;
   }
 };
+
+
+// Programmatic dependent launch: kernels of the factorization's dependent chain
+// start with pdl_wait() (a no-op unless launched with the PDL attribute) and are
+// launched through launch_pdl, so the next kernel's launch and CTA setup
+// overlap the tail of the previous one. KS_PDL=0 turns the attribute off.
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+inline bool pdl_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("KS_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 
 }  // namespace ks

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(256) k_leaf_gauss(DevTree t, LeafBatch lb, con
 
 // P rows of the leaf trapezoid (rows m_pad .. m_pad+s_pad-1), zero padded.
 __global__ void k_leaf_copy_p(DevTree t, LeafBatch lb) {
+  pdl_wait();
   const int leaf = blockIdx.y;
   const int node = lb.node[leaf], m = lb.size[leaf], r = t.rank[node];
   const double* P = t.coeff + t.coeff_off[node];
@@ -100,7 +101,7 @@ void launch_row_sqnorms(const double* X, int64_t n, int64_t d, double* out, cuda
 void launch_leaf_copy_p(const DevTree& t, const LeafBatch& lb, cudaStream_t st) {
   if (lb.s_pad > 0) {
     dim3 g2(64, lb.count);
-    k_leaf_copy_p<<<g2, 256, 0, st>>>(t, lb);
+    launch_pdl(k_leaf_copy_p, g2, dim3(256), 0, st, t, lb);
   }
 }
 
@@ -110,7 +111,7 @@ void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, const double* l
   k_leaf_gauss<<<g1, 256, 0, st>>>(t, lb, lam);
   if (lb.s_pad > 0) {
     dim3 g2(64, lb.count);
-    k_leaf_copy_p<<<g2, 256, 0, st>>>(t, lb);
+    launch_pdl(k_leaf_copy_p, g2, dim3(256), 0, st, t, lb);
   }
 }
 
@@ -120,6 +121,7 @@ void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, const double* l
 // _cholesky raises NotSPDError at linalg.py:190-192.
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(256, 6) k_potrf64(LeafBatch lb, int j0, double* inv, int* info) {
+  pdl_wait();
   const int leaf = blockIdx.x;
   double* A = lb.A + (int64_t)leaf * lb.a_stride + (int64_t)j0 * lb.m_pad + j0;
   const int64_t ld = lb.m_pad;
@@ -218,7 +220,7 @@ void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStr
     cudaFuncSetAttribute(k_potrf64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_potrf64<<<lb.count, 256, smem, st>>>(lb, j0, inv, info);
+  launch_pdl(k_potrf64, dim3(lb.count), dim3(256), smem, st, lb, j0, inv, info);
 }
 
 // In-place symmetrization H = (H + H^T)/2 (solver.py:135, :163).
@@ -237,6 +239,7 @@ __global__ void k_sym_h(double* H, int64_t stride, const int* idx, int s) {
 
 // Upper triangle := lower triangle (SYRK computed on lower tiles only).
 __global__ void k_mirror_lower(double* H, int64_t stride, const int* idx, int s) {
+  pdl_wait();
   double* h = H + (int64_t)idx[blockIdx.y] * stride;
   const int64_t total = (int64_t)s * s;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -248,7 +251,7 @@ __global__ void k_mirror_lower(double* H, int64_t stride, const int* idx, int s)
 void launch_mirror_lower(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st) {
   if (count <= 0 || s_pad <= 0) return;
   dim3 g(32, count);
-  k_mirror_lower<<<g, 256, 0, st>>>(H, h_stride, node_idx, s_pad);
+  launch_pdl(k_mirror_lower, g, dim3(256), 0, st, H, h_stride, node_idx, s_pad);
 }
 
 void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st) {
@@ -262,6 +265,7 @@ void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, i
 // --------------------------------------------------------------------------
 // Coupling B = K(S_l, S_r) (compress.py:281-283), zero padded to s_pad^2.
 __global__ void __launch_bounds__(256) k_coupling(DevTree t, NodeBatch nb) {
+  pdl_wait();
   const int k = blockIdx.z;
   const int l = nb.left[k], r = nb.right[k];
   const int sl = t.rank[l], sr = t.rank[r];
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(256) k_coupling(DevTree t, NodeBatch nb) {
 
 void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
   dim3 g(nb.s_pad / GT, nb.s_pad / GT, nb.count);
-  k_coupling<<<g, 256, 0, st>>>(t, nb);
+  launch_pdl(k_coupling, g, dim3(256), 0, st, t, nb);
 }
 
 // Identity diagonal blocks of Z, P^T (top right), zero bottom-right block, and
@@ -293,6 +297,7 @@ void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
 // (cand = [skel_l; skel_r], compress.py:213): i' < s_pad -> i' (if < s_l),
 // i' >= s_pad -> s_l + (i' - s_pad) (if < s_r).
 __global__ void k_aug_init(DevTree t, NodeBatch nb) {
+  pdl_wait();
   const int k = blockIdx.y;
   const int v = nb.node[k], l = nb.left[k], r = nb.right[k];
   const int sl = t.rank[l], sr = t.rank[r], sv = t.rank[v];
@@ -338,13 +343,14 @@ __global__ void k_aug_init(DevTree t, NodeBatch nb) {
 
 void launch_aug_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
   dim3 g(128, nb.count);
-  k_aug_init<<<g, 256, 0, st>>>(t, nb);
+  launch_pdl(k_aug_init, g, dim3(256), 0, st, t, nb);
 }
 
 // 1-norm of Z (max column abs sum, linalg.py:176), before the LU overwrites it.
 // 32 columns per CTA, rows split over 8 warps; the max over column tiles goes
 // through an integer atomicMax on the (non-negative) double's bit pattern.
 __global__ void __launch_bounds__(256) k_colnorm1(NodeBatch nb) {
+  pdl_wait();
   const int k = blockIdx.y;
   const double* A = nb.Aug + (int64_t)k * nb.T * nb.T;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -368,7 +374,7 @@ __global__ void __launch_bounds__(256) k_colnorm1(NodeBatch nb) {
 void launch_colnorm1(const DevTree&, const NodeBatch& nb, cudaStream_t st) {
   cudaMemsetAsync(nb.norm1, 0, sizeof(double) * nb.count, st);
   dim3 g((nb.t_pad + 31) / 32, nb.count);
-  k_colnorm1<<<g, 256, 0, st>>>(nb);
+  launch_pdl(k_colnorm1, g, dim3(256), 0, st, nb);
 }
 
 // --------------------------------------------------------------------------
@@ -395,6 +401,7 @@ __device__ __forceinline__ void warp_argmax(double v, int p, unsigned& mh, unsig
 
 template <int W, int RPT, int NT, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) k_lu_panel(NodeBatch nb, int c0, int pr0, int pc0, int ph, int pcols) {
+  pdl_wait();
   constexpr int NW = NT / 32;
   constexpr int NONE = 0x7fffffff;
   constexpr int CB = 4;       // columns per unrolled block
@@ -410,12 +417,17 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel(NodeBatch nb, int c0, int
       A[(int64_t)(pr0 + i) * T + pc0 + j] = sc[i * 64 + j];
     }
   }
-  const int rows = T - c0;
-  const int plim = nb.t_pad - c0;  // eligible pivot rows: physical (= original) local rows < plim
+  // the register panel holds Z's rows [c0, t_pad) only (every one a pivot
+  // candidate); the augmented rows [t_pad, T) are never pivots and are reduced
+  // afterwards with the same operations (phase 2)
+  const int rows = nb.t_pad - c0;
+  const int plim = rows;
   extern __shared__ __align__(16) double fin[];  // rows x FS finished values
   __shared__ __align__(16) double cand[2][NW][W];  // per-warp candidate pivot rows, by column parity
   __shared__ double wv[2][NW];
   __shared__ int wp[2][NW], wr[2][NW];
+  __shared__ double u11[W][W + 1];  // effective pivot rows (U of the panel), for phase 2
+  __shared__ double urcp[W];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double a[RPT][W];
   int pos[RPT];
@@ -519,6 +531,38 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel(NodeBatch nb, int c0, int
     const double2* f2 = reinterpret_cast<const double2*>(fin + r * FS);
 #pragma unroll
     for (int j = 0; j < W / 2; ++j) dst[j] = f2[j];
+    if (pos[i] < W) {  // a pivot row: U of the panel, for phase 2
+#pragma unroll
+      for (int j = 0; j < W; ++j) u11[pos[i]][j] = fin[r * FS + j];
+      urcp[pos[i]] = 1.0 / fin[r * FS + pos[i]];  // the loop's reciprocal of this pivot
+    }
+  }
+  // phase 2: the augmented rows, eliminated against the panel's pivot rows
+  // exactly as the register loop would have (same multiply and FMA order; a
+  // zero pivot column is a SingularMatrixError either way)
+  __syncthreads();
+  for (int r = threadIdx.x; r < T - nb.t_pad; r += NT) {
+    double2* row = reinterpret_cast<double2*>(A + (int64_t)(nb.t_pad + r) * T + c0);
+    // read the pivot rows through an opaque pointer: hoisting all W*W of them
+    // out of this loop would not fit in registers
+    const double* ut = &u11[0][0];
+    asm volatile("" : "+l"(ut));
+    double x[W];
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) {
+      const double2 v = row[j];
+      x[2 * j] = v.x;
+      x[2 * j + 1] = v.y;
+    }
+#pragma unroll
+    for (int kk = 0; kk < W; ++kk) {
+      const double l = x[kk] * urcp[kk];
+      x[kk] = l;
+#pragma unroll
+      for (int j = kk + 1; j < W; ++j) x[j] = fma(-l, ut[kk * (W + 1) + j], x[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) row[j] = make_double2(x[2 * j], x[2 * j + 1]);
   }
   // the same row interchanges for every column outside the panel: at most 2W
   // rows moved; the list goes through shared memory, all loads before stores
@@ -556,13 +600,14 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel(NodeBatch nb, int c0, int
 
 template <int W, int RPT, int NT, int MINB = 1>
 static void launch_panel(const NodeBatch& nb, int c0, cudaStream_t st, const int* pend) {
-  const size_t smem = (size_t)std::max((nb.T - c0) * (W + 2), 2 * W * 256) * sizeof(double);
+  const size_t smem = (size_t)std::max((nb.t_pad - c0) * (W + 2), 2 * W * 256) * sizeof(double);
   static size_t set = 0;
   if (smem > set) {
     cudaFuncSetAttribute(k_lu_panel<W, RPT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set = smem;
   }
-  k_lu_panel<W, RPT, NT, MINB><<<nb.count, NT, smem, st>>>(nb, c0, pend[0], pend[1], pend[2], pend[3]);
+  launch_pdl(k_lu_panel<W, RPT, NT, MINB>, dim3(nb.count), dim3(NT), smem, st, nb, c0, pend[0], pend[1], pend[2],
+             pend[3]);
 }
 
 template <int W>
@@ -570,7 +615,7 @@ static void launch_panel_w(const NodeBatch& nb, int c0, cudaStream_t st, const i
   // 512 threads (16 warps hide the per-column latency), rows in registers.
   // (A 256-thread, two-CTAs-per-SM variant for batches wider than the GPU
   // measured no better: the two node-group streams already fill the SMs.)
-  const int rows = nb.T - c0;
+  const int rows = nb.t_pad - c0;
   if (rows <= 512) launch_panel<W, 1, 512>(nb, c0, st, pend);
   else if (rows <= 1024) launch_panel<W, 2, 512>(nb, c0, st, pend);
   else if constexpr (W <= 8) {
@@ -616,6 +661,7 @@ void launch_lu_swap(const NodeBatch& nb, int c0, int w, cudaStream_t st) {
 // columns [c0, c0+ncols). One thread per column, x held in registers.
 template <int W>
 __global__ void __launch_bounds__(128) k_trsm_ul(NodeBatch nb, int r0, int c0, int ncols) {
+  pdl_wait();
   const int k = blockIdx.y;
   const int T = nb.T;
   double* A = nb.Aug + (int64_t)k * T * T;
@@ -652,10 +698,10 @@ __global__ void __launch_bounds__(128) k_trsm_ul(NodeBatch nb, int r0, int c0, i
 void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncols, cudaStream_t st) {
   if (ncols <= 0) return;
   dim3 g((ncols + 127) / 128, nb.count);
-  if (w == 8) k_trsm_ul<8><<<g, 128, 0, st>>>(nb, r0, c0, ncols);
-  else if (w == 16) k_trsm_ul<16><<<g, 128, 0, st>>>(nb, r0, c0, ncols);
-  else if (w == 32) k_trsm_ul<32><<<g, 128, 0, st>>>(nb, r0, c0, ncols);
-  else k_trsm_ul<64><<<g, 128, 0, st>>>(nb, r0, c0, ncols);
+  if (w == 8) launch_pdl(k_trsm_ul<8>, g, dim3(128), 0, st, nb, r0, c0, ncols);
+  else if (w == 16) launch_pdl(k_trsm_ul<16>, g, dim3(128), 0, st, nb, r0, c0, ncols);
+  else if (w == 32) launch_pdl(k_trsm_ul<32>, g, dim3(128), 0, st, nb, r0, c0, ncols);
+  else launch_pdl(k_trsm_ul<64>, g, dim3(128), 0, st, nb, r0, c0, ncols);
 }
 
 // --------------------------------------------------------------------------
@@ -1056,6 +1102,7 @@ void launch_fb_assemble(const DevTree& t, const NodeBatch& fb, const int* begin,
 // Composed row interchanges of each node's LU: (Pi v)[i] = v[pm[i]], from the
 // LAPACK-style swap sequence (linalg.py:250-253). One warp per node.
 __global__ void k_compose_perm(NodeBatch nb) {
+  pdl_wait();
   const int k = blockIdx.x;
   const int* piv = nb.piv + (int64_t)k * nb.t_pad;
   int* pm = nb.pm + (int64_t)k * nb.t_pad;
@@ -1068,10 +1115,13 @@ __global__ void k_compose_perm(NodeBatch nb) {
     }
 }
 
-void launch_compose_perm(const NodeBatch& nb, cudaStream_t st) { k_compose_perm<<<nb.count, 32, 0, st>>>(nb); }
+void launch_compose_perm(const NodeBatch& nb, cudaStream_t st) {
+  launch_pdl(k_compose_perm, dim3(nb.count), dim3(32), 0, st, nb);
+}
 
 // H = sym(trailing block) -> Hbuf[node] (solver.py:163).
 __global__ void k_extract_h(NodeBatch nb, double* H, int64_t stride) {
+  pdl_wait();
   const int k = blockIdx.y;
   const int S = nb.s_pad, T = nb.T, TP = nb.t_pad;
   const double* A = nb.Aug + (int64_t)k * T * T + (int64_t)TP * T + TP;
@@ -1085,7 +1135,7 @@ __global__ void k_extract_h(NodeBatch nb, double* H, int64_t stride) {
 
 void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st) {
   dim3 g(32, nb.count);
-  k_extract_h<<<g, 256, 0, st>>>(nb, H, h_stride);
+  launch_pdl(k_extract_h, g, dim3(256), 0, st, nb, H, h_stride);
 }
 
 }  // namespace ks

@@ -19,7 +19,7 @@ cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
     attr = true;
   }
   dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.batch);
-  kern<<<grid, Cfg::THREADS, smem, st>>>(g);
+  launch_pdl(kern, grid, dim3(Cfg::THREADS), smem, st, g);
   return cudaGetLastError();
 }
 

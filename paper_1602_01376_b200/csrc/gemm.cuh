@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
   using Cfg = GemmCfg<BM, BN, WM, WN, TA, TB, STAGES>;
   constexpr int BK = Cfg::BK;
   extern __shared__ __align__(16) double smem[];
+  pdl_wait();
   double* As = smem;
   double* Bs = smem + STAGES * Cfg::A_STAGE;
 
