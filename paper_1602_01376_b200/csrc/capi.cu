@@ -534,9 +534,15 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
   f->t_pad = 2 * f->s_pad;
   f->T = 3 * f->s_pad;
   f->R = f->m_pad + f->s_pad;
-  // LU panel width: the panel rows live in registers (16 columns up to 1024
-  // rows, 8 columns up to 2048)
+  // LU panel width: the panel's Z rows live in registers (16 columns up to 1024
+  // rows, 8 beyond). KS_PANEL_W=32 selects 32-column panels where t_pad <= 512
+  // (measured no faster at config 3: 75.7 vs 75.5 ms); 8 forces narrow panels.
   f->pw = (f->T <= 1024) ? 16 : 8;
+  if (const char* e = std::getenv("KS_PANEL_W")) {
+    const int w = std::atoi(e);
+    if (w == 32 && f->t_pad <= 512) f->pw = 32;
+    else if (w == 8) f->pw = 8;
+  }
   if (f->T > 2048) { delete f; return fail(KS_ERR_UNSUPPORTED, "skeleton rank %lld too large (max 682)", (long long)s_max); }
 
   const double t_plan = host_ms();

@@ -616,18 +616,23 @@ static void launch_panel_w(const NodeBatch& nb, int c0, cudaStream_t st, const i
   // (A 256-thread, two-CTAs-per-SM variant for batches wider than the GPU
   // measured no better: the two node-group streams already fill the SMs.)
   const int rows = nb.t_pad - c0;
-  if (rows <= 512) launch_panel<W, 1, 512>(nb, c0, st, pend);
-  else if (rows <= 1024) launch_panel<W, 2, 512>(nb, c0, st, pend);
-  else if constexpr (W <= 8) {
-    if (rows <= 1536) launch_panel<W, 3, 512>(nb, c0, st, pend);
-    else launch_panel<W, 4, 512>(nb, c0, st, pend);
+  if constexpr (W == 32) {  // 32 columns in registers: one row per thread, t_pad <= 512
+    launch_panel<W, 1, 512>(nb, c0, st, pend);
+  } else {
+    if (rows <= 512) launch_panel<W, 1, 512>(nb, c0, st, pend);
+    else if (rows <= 1024) launch_panel<W, 2, 512>(nb, c0, st, pend);
+    else if constexpr (W <= 8) {
+      if (rows <= 1536) launch_panel<W, 3, 512>(nb, c0, st, pend);
+      else launch_panel<W, 4, 512>(nb, c0, st, pend);
+    }
   }
 }
 
 void launch_lu_panel(const NodeBatch& nb, int c0, int w, cudaStream_t st, const int* pend) {
   static const int none[4] = {0, 0, 0, 0};
   if (!pend) pend = none;
-  if (w == 16) launch_panel_w<16>(nb, c0, st, pend);
+  if (w == 32) launch_panel_w<32>(nb, c0, st, pend);
+  else if (w == 16) launch_panel_w<16>(nb, c0, st, pend);
   else launch_panel_w<8>(nb, c0, st, pend);
 }
 
