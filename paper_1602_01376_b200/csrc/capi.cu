@@ -43,6 +43,40 @@ constexpr double kCondWarn = 1e10;  // solver.py:51
 
 int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
+// Device memory for handles comes from the device's stream-ordered pool, which
+// keeps up to KS_POOL_GB (default 32) GB of freed memory: a handle created
+// after another one was destroyed (a new factorize call on the same shapes)
+// reuses its memory instead of going back to the driver. Frees keep the
+// device-wide synchronization cudaFree implies (buffers may still be in use on
+// any of the handle's streams).
+static cudaError_t pool_setup() {
+  static int done = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (done == dev) return cudaSuccess;
+  cudaMemPool_t pool;
+  if ((e = cudaDeviceGetDefaultMemPool(&pool, dev)) != cudaSuccess) return e;
+  const char* env = std::getenv("KS_POOL_GB");
+  uint64_t keep = (uint64_t)(env ? std::atof(env) : 32.0) << 30;
+  if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) return e;
+  done = dev;
+  return cudaSuccess;
+}
+
+static cudaError_t pool_alloc(void** p, size_t bytes) {
+  cudaError_t e = pool_setup();
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMallocAsync(p, bytes, 0)) != cudaSuccess) return e;
+  return cudaStreamSynchronize(0);  // usable from every stream once this returns
+}
+
+static void pool_free(void* p) {
+  cudaDeviceSynchronize();
+  cudaFreeAsync(p, 0);
+  cudaStreamSynchronize(0);
+}
+
 template <typename T>
 struct DBuf {
   T* p = nullptr;
@@ -50,7 +84,7 @@ struct DBuf {
   cudaError_t alloc(size_t count) {
     n = count;
     if (count == 0) return cudaSuccess;
-    return cudaMalloc(&p, count * sizeof(T));
+    return pool_alloc(reinterpret_cast<void**>(&p), count * sizeof(T));
   }
   cudaError_t upload(const std::vector<T>& v) {
     cudaError_t e = alloc(v.size());
@@ -58,7 +92,7 @@ struct DBuf {
     return cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) pool_free(p);
     p = nullptr;
     n = 0;
   }
