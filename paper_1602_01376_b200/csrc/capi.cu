@@ -127,6 +127,7 @@ struct ks_factor {
   DBuf<int> leaf_node, leaf_begin, leaf_size, leaf_info;
   DBuf<int> int_node, int_left, int_right, int_info, piv, moves, pm;
   DBuf<double> lu_scratch;
+  DBuf<unsigned> lu_sync;  // persistent-LU flags: 4 words per internal node + the watchdog word
   DBuf<double> dinv;  // condition estimator: diagonal-block inverses of every node's Z factors
   DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
   // solve scratch
@@ -254,7 +255,7 @@ struct ks_factor {
   void release_all() {
     coords.release(); xx.release(); rank_d.release(); skel_pos.release(); skel_off.release(); coeff_off.release();
     coeff.release(); leaf_node.release(); leaf_begin.release(); leaf_size.release(); leaf_info.release();
-    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release(); lu_scratch.release(); dinv.release();
+    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release(); lu_scratch.release(); lu_sync.release(); dinv.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
     norm1.release(); cond.release(); z.release(); c.release(); tin.release(); y.release();
     fb_aug.release(); fb_y.release(); fb_norm1.release(); fb_cond.release(); fb_piv.release(); fb_info.release();
@@ -628,6 +629,7 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     KS_CUDA(f->int_left.alloc(ileft.size()));
     KS_CUDA(f->int_right.alloc(iright.size()));
     KS_CUDA(f->int_info.alloc(std::max(f->n_int, 1)));
+    KS_CUDA(f->lu_sync.alloc((size_t)4 * f->n_int + 1));
     KS_CUDA(f->piv.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
     KS_CUDA(f->moves.alloc((size_t)std::max(f->n_int, 1) * (2 * 64 + 1)));
     KS_CUDA(f->pm.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
@@ -901,6 +903,7 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   if (int rc = mark(f->ev_phase[0])) return rc;
   KS_CUDA(cudaMemsetAsync(f->leaf_info.p, 0, sizeof(int) * nl, st));
   if (f->n_int) KS_CUDA(cudaMemsetAsync(f->int_info.p, 0, sizeof(int) * f->n_int, st));
+  if (f->lu_sync.p) KS_CUDA(cudaMemsetAsync(f->lu_sync.p + (int64_t)4 * f->n_int, 0, sizeof(unsigned), st));
   // ---- leaves: assemble [[K + lam I], [P]] and factor, leaves split into
   // independent groups on their own streams; on the first factorization each
   // group waits only for the uploads of its own P blocks
@@ -940,6 +943,14 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   return KS_OK;
 }
 
+// Levels with at most KS_SLAB_MAX (default 4) nodes run the persistent
+// per-node LU (lu_slab.cu); KS_SLAB_MAX=0 keeps the launch sequence everywhere.
+static bool use_slab(const ks_factor* f, const ks::NodeBatch& nb) {
+  const char* e = std::getenv("KS_SLAB_MAX");
+  const int mx = e ? std::atoi(e) : 4;
+  return nb.count <= mx && f->lu_sync.p && ks::slab_width(nb) > 0;
+}
+
 // One level's node work on L's stream for the node sub-batch nb (coupling,
 // augmented assembly, recursive LU, U12 / Schur, pivot composition, H out).
 static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool is_root_level) {
@@ -969,6 +980,20 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
     rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Pn + S, TP, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
                    OperandW{nb.Aug + (int64_t)TP * T + S, T, TT, nullptr}, -1.0, 0.0), false, true);
     if (rc) return rc;
+    if (use_slab(f, nb)) {
+      // narrow level: the whole LU, U12, Schur block and H in one cooperative launch
+      KS_CUDA(cudaMemsetAsync(nb.norm1, 0, sizeof(double) * cnt, st));
+      unsigned* sy = f->lu_sync.p + (int64_t)4 * nb.first;
+      KS_CUDA(cudaMemsetAsync(sy, 0, sizeof(unsigned) * 4 * cnt, st));
+      if (ks::launch_lu_slab(nb, f->hbuf.p, SS, !is_root_level, sy, f->lu_sync.p + (int64_t)4 * f->n_int, st))
+        return fail(KS_ERR_CUDA, "persistent LU launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      ++L.count[0];
+      if (int rc2 = L.check("lu_slab")) return rc2;
+      ks::launch_compose_perm(nb, st);
+      ++L.count[0];
+      KS_CUDA(cudaGetLastError());
+      return KS_OK;
+    }
     ks::launch_colnorm1(dt, nb, st);
     ++L.count[0];
     if (int rc2 = L.check("colnorm1")) return rc2;
@@ -1261,7 +1286,11 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
     KS_CUDA(cudaMemcpyAsync(f->int_info_h.data(), f->int_info.p, sizeof(int) * f->n_int, cudaMemcpyDeviceToHost, st));
     KS_CUDA(cudaMemcpyAsync(f->cond_h.data(), f->cond.p, sizeof(double) * f->n_int, cudaMemcpyDeviceToHost, st));
   }
+  unsigned watchdog = 0;
+  if (f->lu_sync.p)
+    KS_CUDA(cudaMemcpyAsync(&watchdog, f->lu_sync.p + (int64_t)4 * f->n_int, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
   KS_CUDA(cudaStreamSynchronize(st));
+  if (watchdog) return fail(KS_ERR_CUDA, "persistent LU: a node's slabs stopped making progress (watchdog)");
   if (f->profiling) {
     auto el = [](cudaEvent_t a, cudaEvent_t b) {
       float ms = 0.f;

@@ -17,6 +17,7 @@
 
 #include "gauss.cuh"
 #include "kernels.cuh"
+#include "lu_panel.cuh"
 #include "trsv.cuh"
 
 namespace ks {
@@ -620,23 +621,6 @@ __device__ long long* g_panel_clk = nullptr;
     if (clk && threadIdx.x == 0) clk[i] = clock64();                     \
   } while (0)
 
-struct __align__(16) PivKey {
-  unsigned hi, lo;
-  int pos, row;
-};
-
-// winner lane of a warp for (key hi, lo, logical position): max hi, then max
-// lo, then min position
-__device__ __forceinline__ int warp_winner(unsigned h, unsigned l, int p) {
-  const unsigned mh = __reduce_max_sync(0xffffffffu, h);
-  const unsigned m = __ballot_sync(0xffffffffu, h == mh);
-  if (__popc(m) == 1) return __ffs(m) - 1;
-  const unsigned ml = __reduce_max_sync(0xffffffffu, h == mh ? l : 0u);
-  const bool t = (h == mh && l == ml);
-  const unsigned mp = __reduce_min_sync(0xffffffffu, t ? (unsigned)p : 0x7fffffffu);
-  return __ffs(__ballot_sync(0xffffffffu, t && (unsigned)p == mp)) - 1;
-}
-
 template <int W, int RPT, int NT, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) k_lu_panel2(NodeBatch nb, int c0, int pr0, int pc0, int ph, int pcols) {
   pdl_wait();
@@ -659,10 +643,8 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel2(NodeBatch nb, int c0, in
   }
   const int rows = nb.t_pad - c0;
   extern __shared__ __align__(16) double fin[];  // rows x FS finished values
-  __shared__ __align__(16) double cand[2][NW][W];
-  __shared__ PivKey wk[2][NW];
+  __shared__ PanelShared<NW, W> ps;
   __shared__ double u11[W][W + 1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double a[RPT][W];
   int pos[RPT];
   bool done[RPT];
@@ -679,100 +661,31 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel2(NodeBatch nb, int c0, in
       a[i][2 * j + 1] = v.y;
     }
   }
-  int* info = nb.info + k;
-  int* piv = nb.piv + (int64_t)k * nb.t_pad + c0;
   PANEL_STAMP(1);
-#pragma unroll 1
-  for (int kb = 0; kb < W; kb += CB) {
-#pragma unroll
-    for (int c = 0; c < CB; ++c) {
-      const int kk = kb + c;
-      const int buf = c & 1;
-      // 1) this thread's best candidate row
-      unsigned bh = 0u, bl = 0u;
-      int bp = NONE, bi = -1;
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const double v = fabs(a[i][c]);
-        const unsigned h = (unsigned)__double2hiint(v) + 1u, l = (unsigned)__double2loint(v);
-        if (!done[i] && (h > bh || (h == bh && (l > bl || (l == bl && pos[i] < bp))))) {
-          bh = h; bl = l; bp = pos[i]; bi = i;
-        }
-      }
-      // 2) warp winner publishes its row and key
-      const int wl = warp_winner(bh, bl, bp);
-      if (lane == wl) {
-#pragma unroll
-        for (int i = 0; i < RPT; ++i)
-          if (i == bi) {
-#pragma unroll
-            for (int j = c; j < W; ++j) cand[buf][warp][j] = a[i][j];
-          }
-        PivKey q;
-        q.hi = bh; q.lo = bl; q.pos = bp; q.row = bi >= 0 ? (int)threadIdx.x + bi * NT : -1;
-        wk[buf][warp] = q;
-      }
-      __syncthreads();
-      // 3) CTA winner (every warp redundantly)
-      PivKey q;
-      if (lane < NW) q = wk[buf][lane];
-      else { q.hi = 0u; q.lo = 0u; q.pos = NONE; q.row = -1; }
-      const int ww = warp_winner(q.hi, q.lo, q.pos);
-      const int br = __shfl_sync(0xffffffffu, q.row, ww);
-      const int bpos = __shfl_sync(0xffffffffu, q.pos, ww);
-      const double pv = cand[buf][ww][c];
-      const bool singular = !(fabs(pv) > 0.0);
-      if (threadIdx.x == 0) {
-        if (singular && *info == 0) *info = c0 + kk + 1;  // linalg.py:205-206
-        piv[kk] = c0 + (singular ? kk : bpos);
-      }
-      // 4) logical swap kk <-> bpos, eliminate the other rows (linalg.py:209-212)
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const int r = threadIdx.x + i * NT;
-        const bool is_piv = !done[i] && (singular ? pos[i] == kk : r == br);
-        if (!singular && !done[i]) pos[i] = (r == br) ? kk : (pos[i] == kk ? bpos : pos[i]);
-        const bool keep = done[i] || is_piv;
-        done[i] = keep;
-        if (!keep && !singular) {
-          const double l = a[i][c] / pv;
-          a[i][c] = l;
-#pragma unroll
-          for (int j = c + 1; j < W; ++j) a[i][j] = fma(-l, cand[buf][ww][j], a[i][j]);
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int r = threadIdx.x + i * NT;
-      if (r < rows) {
-        double2* f2 = reinterpret_cast<double2*>(fin + r * FS + kb);
-#pragma unroll
-        for (int j = 0; j < CB / 2; ++j) f2[j] = make_double2(a[i][2 * j], a[i][2 * j + 1]);
-      }
-#pragma unroll
-      for (int j = 0; j < W; ++j) a[i][j] = (j + CB < W) ? a[i][j + CB] : 0.0;
-    }
-    PANEL_STAMP(2 + kb / CB);
-  }
+  panel_columns<W, RPT, NT, (W <= 16 ? W : 16)>(a, pos, done, ps, fin, FS, rows, nb.piv + (int64_t)k * nb.t_pad + c0,
+                                                c0, nb.info + k, c0);
   __syncthreads();
   PANEL_STAMP(20);
-  // panel rows back to their logical positions; the pivot rows (U) to u11
+  // panel rows back to their logical positions (coalesced: W/2 threads per
+  // row); the pivot rows (U) to u11
+  __shared__ int spos[RPT * NT];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     const int r = threadIdx.x + i * NT;
     if (r >= rows) continue;
-    double2* dst = reinterpret_cast<double2*>(A + (int64_t)(c0 + pos[i]) * T + c0);
-    const double2* f2 = reinterpret_cast<const double2*>(fin + r * FS);
-#pragma unroll
-    for (int j = 0; j < W / 2; ++j) dst[j] = f2[j];
+    spos[r] = pos[i];
     if (pos[i] < W) {
 #pragma unroll
       for (int j = 0; j < W; ++j) u11[pos[i]][j] = fin[r * FS + j];
     }
   }
-  // the augmented rows, eliminated against the panel's pivot rows
   __syncthreads();
+  for (int e = threadIdx.x; e < rows * (W / 2); e += NT) {
+    const int r = e / (W / 2), j2 = 2 * (e % (W / 2));
+    *reinterpret_cast<double2*>(A + (int64_t)(c0 + spos[r]) * T + c0 + j2) =
+        *reinterpret_cast<const double2*>(fin + r * FS + j2);
+  }
+  // the augmented rows, eliminated against the panel's pivot rows
   PANEL_STAMP(21);
   for (int r = threadIdx.x; r < T - nb.t_pad; r += NT) {
     double2* row = reinterpret_cast<double2*>(A + (int64_t)(nb.t_pad + r) * T + c0);
@@ -787,7 +700,7 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel2(NodeBatch nb, int c0, in
     }
 #pragma unroll
     for (int kk = 0; kk < W; ++kk) {
-      const double l = x[kk] / ut[kk * (W + 1) + kk];
+      const double l = x[kk] * ps.urcp[kk];
       x[kk] = l;
 #pragma unroll
       for (int j = kk + 1; j < W; ++j) x[j] = fma(-l, ut[kk * (W + 1) + j], x[j]);
@@ -1553,10 +1466,10 @@ extern "C" int ks_probe_panel(int T, int tp, int w, int count, int reps, double*
   cudaMalloc(&piv, (size_t)count * tp * 4); cudaMalloc(&info, count * 4);
   cudaMalloc(&moves, (size_t)count * 129 * 4); cudaMalloc(&pm, (size_t)count * tp * 4);
   cudaMalloc(&norm1, count * 8); cudaMalloc(&cond, count * 8);
-  cudaMalloc(&dclk, 32 * 8);
+  cudaMalloc(&dclk, 64 * 8);
   cudaMemcpy(A0, h.data(), nA * 8, cudaMemcpyHostToDevice);
   cudaMemset(info, 0, count * 4);
-  cudaMemset(dclk, 0, 32 * 8);
+  cudaMemset(dclk, 0, 64 * 8);
   NodeBatch nb{};
   nb.count = count; nb.first = 0; nb.s_pad = T - tp; nb.t_pad = tp; nb.T = T;
   nb.Aug = A; nb.piv = piv; nb.info = info; nb.moves = moves; nb.pm = pm; nb.scratch = scratch;
@@ -1582,7 +1495,7 @@ extern "C" int ks_probe_panel(int T, int tp, int w, int count, int reps, double*
   cudaError_t err = cudaDeviceSynchronize();
   std::sort(t.begin(), t.end());
   ms[0] = t[0]; ms[1] = t[t.size() / 2];
-  cudaMemcpy(clk, dclk, 25 * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(clk, dclk, 64 * 8, cudaMemcpyDeviceToHost);
   cudaFree(A); cudaFree(A0); cudaFree(scratch); cudaFree(piv); cudaFree(info); cudaFree(moves); cudaFree(pm);
   cudaFree(norm1); cudaFree(cond); cudaFree(dclk);
   cudaEventDestroy(e0); cudaEventDestroy(e1);

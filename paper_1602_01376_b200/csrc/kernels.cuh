@@ -72,6 +72,12 @@ int hager_launches(const NodeBatch& nb);
 void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st);
 void launch_compose_perm(const NodeBatch& nb, cudaStream_t st);
 void launch_lu_merge(const NodeBatch& nb, int c0, int h, int w, cudaStream_t st);
+// persistent per-node LU of a level (lu_slab.cu): slab width (0 = unsupported
+// shape) and the cooperative launch (0 ok). sync: 4 zeroed words per node;
+// err: the watchdog word. write_h: sym(H) -> H[node] (not at the root).
+int slab_width(const NodeBatch& nb);
+int launch_lu_slab(const NodeBatch& nb, double* H, int64_t h_stride, bool write_h, unsigned* sync, unsigned* err,
+                   cudaStream_t st);
 void launch_fb_assemble(const DevTree& t, const NodeBatch& fb, const int* begin, const int* size, const double* lam,
                         cudaStream_t st);
 void launch_fb_up(const NodeBatch& fb, const int* begin, const int* size, const double* B, int64_t ldb, double* Y,

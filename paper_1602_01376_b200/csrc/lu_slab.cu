@@ -1,0 +1,408 @@
+// Persistent per-node LU for the narrow (latency-bound) top levels of the tree.
+//
+// Reference: the internal-node step of factorize (solver.py:138-165): LU with
+// partial pivoting of Z (linalg.py:199-213), then H = P G Z^-1 P^T. The GPU
+// factors the augmented matrix [[Z, P^T], [-P G, 0]] (T x T, pivots among the
+// first t_pad rows); its trailing block is H. The recursive
+// launch sequence used for wide levels (capi.cu rlu: ~120 dependent launches
+// per level) is replaced here by ONE cooperative launch per level:
+//
+//   * each CTA owns a W-column slab of one node's matrix, resident in shared
+//     memory for the whole factorization (T x (W+1) doubles, <= 204 KB);
+//   * step j (columns [jW, jW+W)) is factored by the CTA owning slab j: the
+//     candidate rows in registers (lu_panel.cuh), the augmented rows after,
+//     then the slab's rows [jW, T) are published to HBM/L2 with a release flag;
+//   * every other CTA acquires the flag, applies the step's row interchanges to
+//     its slab (LAPACK convention: also to the finished L columns), and, for
+//     slabs right of the panel, U12 = L11^-1 A12 and the trailing update
+//     A22 -= L21 U12 on the fp64 tensor pipe (DMMA m8n8k4, L21 streamed from L2);
+//   * slab j+1 is updated by its owner right after step j, so the next panel
+//     starts while the other slabs are still updating (look-ahead of one step);
+//   * after the last step the slabs are written back in place (same layout as
+//     the launch sequence: L\U of Pi Z, U12 = L^-1 Pi P^T, L21aug, Schur block)
+//     and the H slabs write sym(H) for the parent (solver.py:163).
+// The 1-norm of Z for the condition estimate (linalg.py:176) is taken from the
+// slabs before the first step. Waits are bounded (a watchdog sets an error
+// word instead of hanging the GPU).
+#include <algorithm>
+#include <cstdlib>
+
+#include "kernels.cuh"
+#include "lu_panel.cuh"
+
+namespace ks {
+
+// KS_SLAB_TRACE=1: %globaltimer stamps of node 0 of the last traced launch,
+// [slab][step][phase] (phase 0 acquired / panel start, 1 moves done / columns
+// done, 2 U12 done / augmented rows done, 3 update done / published)
+__device__ long long* g_slab_ts = nullptr;
+constexpr int kTsSlabs = 128, kTsSteps = 64;
+
+namespace {
+
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// all threads of the CTA: wait until *p >= target (false: watchdog expired)
+__device__ bool cta_wait(const unsigned* p, unsigned target, unsigned* err, int* s_ok) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    if (ld_acquire(p) < target) {
+      const long long t0 = clock64();
+      while (ld_acquire(p) < target) {
+        if (clock64() - t0 > (1LL << 32)) {  // ~2 s: something is broken
+          atomicExch(err, 1u);
+          ok = 0;
+          break;
+        }
+      }
+    }
+    *s_ok = ok;
+  }
+  __syncthreads();
+  return *s_ok != 0;
+}
+
+// rows [c0, TP) of the slab permuted by the step's W row interchanges
+// (spiv[i] = pivot of column c0+i, relative to c0): each touched row is
+// followed through the swap sequence; all loads, one barrier, all stores.
+template <int W, int NT, int LD>
+__device__ __forceinline__ void slab_moves(double* Sl, int c0, const int* spiv, int* msrc, int* mdst) {
+  if (threadIdx.x < 2 * W) {
+    const int x = threadIdx.x < W ? (int)threadIdx.x : spiv[threadIdx.x - W];
+    int f = x;
+#pragma unroll 8
+    for (int i = 0; i < W; ++i) {
+      const int p = spiv[i];
+      f = (f == i) ? p : (f == p ? i : f);
+    }
+    msrc[threadIdx.x] = x;
+    mdst[threadIdx.x] = f;
+  }
+  __syncthreads();
+  constexpr int E = (2 * W * W + NT - 1) / NT;
+  double v[E];
+#pragma unroll
+  for (int u = 0; u < E; ++u) {
+    const int e = threadIdx.x + u * NT;
+    if (e < 2 * W * W) v[u] = Sl[(c0 + msrc[e / W]) * LD + e % W];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < E; ++u) {
+    const int e = threadIdx.x + u * NT;
+    if (e < 2 * W * W) {
+      const int m = e / W;
+      if (msrc[m] != mdst[m]) Sl[(c0 + mdst[m]) * LD + e % W] = v[u];
+    }
+  }
+  __syncthreads();
+}
+
+// Sl rows [r0, T) -= L21 (A rows [r0, T), columns [c0, c0+W), row-major ld T)
+// x U12 (Sl rows [c0, c0+W)): warp tiles of 16 rows x W columns on DMMA.
+template <int W, int NT, int LD>
+__device__ __forceinline__ void slab_update(double* Sl, const double* A, int64_t T, int c0, int r0, int rend) {
+  constexpr int KS = W / 4, NN = W / 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  double bf[KS][NN];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int n = 0; n < NN; ++n) bf[ks][n] = Sl[(c0 + ks * 4 + tq) * LD + n * 8 + gq];
+  const int ntiles = (rend - r0) / 16;
+  for (int t = warp; t < ntiles; t += NT / 32) {
+    const int r = r0 + t * 16;
+    double af[2][KS];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) af[m][ks] = -__ldcg(A + (int64_t)(r + m * 8 + gq) * T + c0 + ks * 4 + tq);
+    double acc[2][NN][2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < NN; ++n) {
+        acc[m][n][0] = Sl[(r + m * 8 + gq) * LD + n * 8 + 2 * tq];
+        acc[m][n][1] = Sl[(r + m * 8 + gq) * LD + n * 8 + 2 * tq + 1];
+      }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int n = 0; n < NN; ++n) dmma884(acc[m][n][0], acc[m][n][1], af[m][ks], bf[ks][n]);
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < NN; ++n) {
+        Sl[(r + m * 8 + gq) * LD + n * 8 + 2 * tq] = acc[m][n][0];
+        Sl[(r + m * 8 + gq) * LD + n * 8 + 2 * tq + 1] = acc[m][n][1];
+      }
+  }
+}
+
+}  // namespace
+
+template <int W, int RPT, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    k_lu_slab(NodeBatch nb, double* Hout, int64_t h_stride, int write_h, unsigned* sync, unsigned* err, int groups) {
+  constexpr int LD = W + 1;  // odd row stride: conflict-free row-per-thread access
+  constexpr int NW = NT / 32;
+  constexpr int CBX = (W <= 16) ? W : 16;
+  const int T = nb.T, TP = nb.t_pad, S = nb.s_pad;
+  const int G = T / W, nst = TP / W;
+  const int slab = blockIdx.x % G;
+  const int col0 = slab * W;
+  extern __shared__ __align__(16) double smem[];
+  double* Sl = smem;                   // T x LD: this CTA's slab
+  double* L11 = smem + (size_t)T * LD;  // W x LD: unit-lower diagonal block of the step
+  __shared__ PanelShared<NW, W> ps;
+  __shared__ int spiv[W], msrc[2 * W], mdst[2 * W];
+  __shared__ int s_ok;
+  long long* ts = g_slab_ts;
+  auto stamp = [&](int k, int j, int ph) {
+    if (ts && k == 0 && threadIdx.x == 0 && slab < kTsSlabs && j < kTsSteps) ts[(slab * kTsSteps + j) * 4 + ph] = gtime();
+  };
+  for (int k = blockIdx.x / G; k < nb.count; k += groups) {
+    double* A = nb.Aug + (int64_t)k * T * T;
+    unsigned* sy = sync + 4 * k;
+    int* pivk = nb.piv + (int64_t)k * TP;
+    __syncthreads();
+    for (int e = threadIdx.x; e < T * W; e += NT) {
+      const int r = e / W, c = e % W;
+      Sl[r * LD + c] = A[(int64_t)r * T + col0 + c];
+    }
+    __syncthreads();
+    if (slab < nst) {  // ||Z||_1 over this slab's columns (rows < t_pad)
+      constexpr int NG = NT / W;
+      double* red = &ps.cand[0][0][0];  // 2*NW*W >= NG*W doubles
+      const int c = threadIdx.x % W, g = threadIdx.x / W;
+      double s = 0.0;
+      for (int r = g; r < TP; r += NG) s += fabs(Sl[r * LD + c]);
+      red[g * W + c] = s;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        double t = 0.0;
+        if (threadIdx.x < W)
+          for (int gg = 0; gg < NG; ++gg) t += red[gg * W + threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+        if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(nb.norm1 + k), __double_as_longlong(t));
+      }
+      __syncthreads();  // the scratch is the panel's candidate buffer
+    }
+    for (int j = 0; j < nst; ++j) {
+      const int c0 = j * W;
+      if (slab == j) {
+        // ---- panel: candidate rows [c0, TP) in registers ----
+        const int rows = TP - c0;
+        __syncthreads();  // the previous step's update of this slab is complete
+        stamp(k, j, 0);
+        {
+          double a[RPT][W];
+          int pos[RPT];
+          bool done[RPT];
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            const int r = threadIdx.x + i * NT;
+            pos[i] = r;
+            done[i] = (r >= rows);
+#pragma unroll
+            for (int jj = 0; jj < W; ++jj) a[i][jj] = (r < rows) ? Sl[(c0 + r) * LD + jj] : 0.0;
+          }
+          panel_columns<W, RPT, NT, CBX>(a, pos, done, ps, Sl + (size_t)c0 * LD, LD, rows, pivk + c0, c0, nb.info + k,
+                                         c0);
+        }
+        __syncthreads();
+        stamp(k, j, 1);
+        if (threadIdx.x < W) spiv[threadIdx.x] = pivk[c0 + threadIdx.x] - c0;
+        __syncthreads();
+        slab_moves<W, NT, LD>(Sl, c0, spiv, msrc, mdst);
+        // augmented rows [TP, T): eliminated against the panel's U rows
+        for (int r = TP + threadIdx.x; r < T; r += NT) {
+          double x[W];
+#pragma unroll
+          for (int jj = 0; jj < W; ++jj) x[jj] = Sl[r * LD + jj];
+#pragma unroll
+          for (int kk = 0; kk < W; ++kk) {
+            const double l = x[kk] * ps.urcp[kk];
+            x[kk] = l;
+#pragma unroll
+            for (int jj = kk + 1; jj < W; ++jj) x[jj] = fma(-l, Sl[(c0 + kk) * LD + jj], x[jj]);
+          }
+#pragma unroll
+          for (int jj = 0; jj < W; ++jj) Sl[r * LD + jj] = x[jj];
+        }
+        __syncthreads();
+        stamp(k, j, 2);
+        // publish rows [c0, T) of the panel (current row order)
+        for (int e = threadIdx.x; e < (T - c0) * W; e += NT) {
+          const int r = c0 + e / W, c = e % W;
+          A[(int64_t)r * T + col0 + c] = Sl[r * LD + c];
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(sy, (unsigned)(j + 1));
+        stamp(k, j, 3);
+        continue;
+      }
+      // ---- any other slab: acquire step j ----
+      if (!cta_wait(sy, (unsigned)(j + 1), err, &s_ok)) return;
+      stamp(k, j, 0);
+      if (threadIdx.x < W) spiv[threadIdx.x] = __ldcg(pivk + c0 + threadIdx.x) - c0;
+      __syncthreads();
+      slab_moves<W, NT, LD>(Sl, c0, spiv, msrc, mdst);
+      stamp(k, j, 1);
+      if (slab < j) continue;  // finished L columns: the interchanges only
+      // U12 = L11^-1 A12 (one thread per column)
+      for (int e = threadIdx.x; e < W * W; e += NT) {
+        const int i = e / W, jj = e % W;
+        L11[i * LD + jj] = __ldcg(A + (int64_t)(c0 + i) * T + c0 + jj);
+      }
+      __syncthreads();
+      if (threadIdx.x < W) {
+        double x[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) x[i] = Sl[(c0 + i) * LD + threadIdx.x];
+#pragma unroll
+        for (int i = 1; i < W; ++i) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int q = 0; q + 3 < i; q += 4) {
+            s0 = fma(L11[i * LD + q], x[q], s0);
+            s1 = fma(L11[i * LD + q + 1], x[q + 1], s1);
+            s2 = fma(L11[i * LD + q + 2], x[q + 2], s2);
+            s3 = fma(L11[i * LD + q + 3], x[q + 3], s3);
+          }
+#pragma unroll
+          for (int q = i & ~3; q < i; ++q) s0 = fma(L11[i * LD + q], x[q], s0);
+          x[i] -= (s0 + s1) + (s2 + s3);
+        }
+#pragma unroll
+        for (int i = 0; i < W; ++i) Sl[(c0 + i) * LD + threadIdx.x] = x[i];
+      }
+      __syncthreads();
+      stamp(k, j, 2);
+      slab_update<W, NT, LD>(Sl, A, T, c0, c0 + W, T);
+      __syncthreads();
+      stamp(k, j, 3);
+    }
+    // ---- every CTA of the node is past the last step: write the slab back ----
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(sy + 1, 1u);
+    }
+    if (!cta_wait(sy + 1, (unsigned)G, err, &s_ok)) return;
+    for (int e = threadIdx.x; e < T * W; e += NT) {
+      const int r = e / W, c = e % W;
+      A[(int64_t)r * T + col0 + c] = Sl[r * LD + c];
+    }
+    if (write_h && slab >= nst) {  // H = sym(trailing block) -> Hout[node] (solver.py:163)
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(sy + 2, 1u);
+      if (!cta_wait(sy + 2, (unsigned)(G - nst), err, &s_ok)) return;
+      double* h = Hout + (int64_t)nb.node[k] * h_stride;
+      for (int e = threadIdx.x; e < S * W; e += NT) {
+        const int i = e / W, jj = e % W, j2 = col0 - TP + jj;
+        h[(int64_t)i * S + j2] = 0.5 * (Sl[(TP + i) * LD + jj] + __ldcg(A + (int64_t)(TP + j2) * T + TP + i));
+      }
+    }
+  }
+}
+
+namespace {
+
+template <int W, int RPT>
+int launch_slab_t(const NodeBatch& nb, double* H, int64_t hs, bool write_h, unsigned* sync, unsigned* err,
+                  cudaStream_t st) {
+  constexpr int NT = 512;
+  const size_t smem = (size_t)(nb.T + W) * (W + 1) * sizeof(double);
+  auto kern = k_lu_slab<W, RPT, NT>;
+  static size_t set = 0;
+  static int max_active = 0;
+  if (smem > set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+    set = smem;
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    max_active = per_sm * sms;
+  }
+  const int G = nb.T / W;
+  const int groups = std::min(nb.count, max_active / G);
+  if (groups < 1) return -1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(groups * G);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // slabs of a node wait on each other
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, nb, H, hs, write_h ? 1 : 0, sync, err, groups) == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace
+
+// W = 32 while a 32-column slab fits (T <= 800: configs 1-4), else 16 (T <= 1600).
+int slab_width(const NodeBatch& nb) {
+  if (nb.T % 32 == 0 && nb.t_pad <= 512 && (size_t)(nb.T + 32) * 33 * 8 <= 212 * 1024) return 32;
+  if (nb.T % 16 == 0 && nb.t_pad <= 1024 && (size_t)(nb.T + 16) * 17 * 8 <= 212 * 1024) return 16;
+  return 0;
+}
+
+static long long* slab_ts_buf() {
+  static long long* p = nullptr;
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("KS_SLAB_TRACE");
+    on = (e && e[0] == '1') ? 1 : 0;
+    if (on) {
+      cudaMalloc(&p, sizeof(long long) * kTsSlabs * kTsSteps * 4);
+      cudaMemset(p, 0, sizeof(long long) * kTsSlabs * kTsSteps * 4);
+      cudaMemcpyToSymbol(g_slab_ts, &p, sizeof(p));
+    }
+  }
+  return p;
+}
+
+int launch_lu_slab(const NodeBatch& nb, double* H, int64_t h_stride, bool write_h, unsigned* sync, unsigned* err,
+                   cudaStream_t st) {
+  slab_ts_buf();
+  const int w = slab_width(nb);
+  if (w == 32) return launch_slab_t<32, 1>(nb, H, h_stride, write_h, sync, err, st);
+  if (w == 16) return nb.t_pad <= 512 ? launch_slab_t<16, 1>(nb, H, h_stride, write_h, sync, err, st)
+                                      : launch_slab_t<16, 2>(nb, H, h_stride, write_h, sync, err, st);
+  return -1;
+}
+
+}  // namespace ks
+
+// Probe hook: copies the stamps of the last traced level (KS_SLAB_TRACE=1).
+extern "C" int ks_slab_trace(long long* out, int64_t cap) {
+  long long* p = ks::slab_ts_buf();
+  if (!p) return 0;
+  const int64_t n = std::min<int64_t>(cap, (int64_t)ks::kTsSlabs * ks::kTsSteps * 4);
+  cudaMemcpy(out, p, sizeof(long long) * n, cudaMemcpyDeviceToHost);
+  return (int)n;
+}

@@ -128,3 +128,28 @@ def test_leaf_lu_fallback_path(golden, case, monkeypatch):
     X_ref = O.solve_many_telescoping(O.factorize(O.Problem(g), float(g["lam"])), B)
     assert rel(ks.solve_many(hf, B), X_ref) <= 1e-10
     hf.close()
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg2s", "cfg3s", "cfg5s", "ragged"])
+@pytest.mark.parametrize("slab_max", ["0", "100000"])
+def test_persistent_lu_levels(golden, case, slab_max, monkeypatch):
+    """Every level through the launch sequence (KS_SLAB_MAX=0) or through the
+    persistent per-node LU (lu_slab.cu, KS_SLAB_MAX large): the same H,
+    solution and condition estimates as the reference."""
+    import paper_1602_01376_b200 as ks
+    g = golden(case)
+    monkeypatch.setenv("KS_SLAB_MAX", slab_max)
+    hf = ks.factorize(g, float(g["lam"]))
+    hf.refactorize(float(g["lam"]))  # second call replays the captured graph
+    monkeypatch.delenv("KS_SLAB_MAX")
+    u = ks.solve_many(hf, g["b"])
+    assert rel(u, g["u"]) <= TOL.get(case, 1e-10), rel(u, g["u"])
+    for i, v in enumerate(g["H_nodes"]):
+        H = g["H"][g["H_off"][i]:g["H_off"][i + 1]]
+        assert rel(hf.node_h(int(v)).ravel(), H) <= 1e-11, int(v)
+    zc = hf.diagnostics["z_cond"]
+    assert sorted(zc) == g["z_cond_nodes"].tolist()
+    if len(zc):
+        mine = np.array([zc[int(v)] for v in g["z_cond_nodes"]])
+        assert np.allclose(mine, g["z_cond"], rtol=1e-6)
+    hf.close()

@@ -5,10 +5,10 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 lib = C.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1602_01376_b200", "libinvaskit.so"))
 for T, tp, w, cnt in [(768, 512, 16, 1), (768, 512, 16, 16), (768, 512, 16, 256), (768, 512, 32, 1), (1536, 1024, 8, 1)]:
     ms = (C.c_double * 2)()
-    clk = (C.c_longlong * 25)()
+    clk = (C.c_longlong * 64)()
     rc = lib.ks_probe_panel(T, tp, w, cnt, 20, ms, clk)
     c = list(clk)
     base = c[0]
-    st = {i: c[i] - base for i in range(24) if c[i]}
+    st = {i: c[i] - base for i in list(range(24)) + list(range(26, 46)) if c[i]}
     print(f"T={T} tp={tp} w={w} count={cnt} rc={rc} min {ms[0]*1e3:.1f} us med {ms[1]*1e3:.1f} us moves={c[24]}")
     print("   stamps (cycles from start):", st)
