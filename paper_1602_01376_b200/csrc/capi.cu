@@ -152,6 +152,10 @@ struct ks_factor {
   int64_t n_factorizations = 0;
   DBuf<double> lam_dev;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // narrow levels' condition estimates: their own stream, so they do not queue
+  // behind the deferred wide-level batch on `side`
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   // uploads started by ks_create, consumed by the first factorization
   static constexpr int kLeafChunks = 4;
   cudaStream_t upl = nullptr;
@@ -647,6 +651,9 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     KS_CUDA(f->xx.alloc((size_t)p->n + f->m_pad));
     KS_CUDA(f->coeff.alloc((size_t)p->coeff_off[nn]));
     KS_CUDA(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
+    KS_CUDA(cudaStreamCreateWithFlags(&f->side2, cudaStreamNonBlocking));
+    KS_CUDA(cudaEventCreateWithFlags(&f->ev_fork2, cudaEventDisableTiming));
+    KS_CUDA(cudaEventCreateWithFlags(&f->ev_join2, cudaEventDisableTiming));
     KS_CUDA(cudaStreamCreateWithFlags(&f->cap, cudaStreamNonBlocking));
     for (auto& g : f->gst) KS_CUDA(cudaStreamCreateWithFlags(&g, cudaStreamNonBlocking));
     KS_CUDA(cudaEventCreateWithFlags(&f->gfork, cudaEventDisableTiming));
@@ -1045,6 +1052,12 @@ static int hager_ctas() {
   return e ? std::max(1, std::atoi(e)) : 96;
 }
 
+// KS_HAGER_SPLIT=0: narrow levels' estimates queue on `side` like the wide ones
+static bool hager_split() {
+  const char* e = std::getenv("KS_HAGER_SPLIT");
+  return !(e && e[0] == '0');
+}
+
 // Internal levels [lev0, lev1) of the plan (deepest first); wide levels split
 // into node groups on the group streams. Condition estimates run on the side
 // stream (they only feed diagnostics), joined at the end. The estimates of the
@@ -1057,6 +1070,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
     return KS_OK;
   };
   std::vector<int> deferred;  // levels whose estimate is not launched yet
+  bool used_side = false, used_side2 = false;
   auto flush = [&]() -> int {
     if (deferred.empty()) return KS_OK;
     if (trace_on()) {  // inline, so the trace times each estimate
@@ -1071,6 +1085,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
     }
     KS_CUDA(cudaEventRecord(f->ev_fork, st));
     KS_CUDA(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
+    used_side = true;
     for (int lv : deferred) {
       ks::launch_hager(dt, f->nodebatch(lv), f->dinv.p, hager_ctas(), f->side);
       L.count[0] += ks::hager_launches(f->nodebatch(lv));
@@ -1102,15 +1117,31 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
         KS_CUDA(cudaStreamWaitEvent(st, f->gjoin[g], 0));
       }
     }
-    // condition estimate off the critical path
-    deferred.push_back(lev);
-    if (!wide)
-      if (int rc = flush()) return rc;
+    // condition estimate off the critical path: a narrow level's right away
+    // on side2 (one CTA per node), a wide level's deferred (see above)
+    if (!wide && !trace_on() && hager_split()) {
+      KS_CUDA(cudaEventRecord(f->ev_fork2, st));
+      KS_CUDA(cudaStreamWaitEvent(f->side2, f->ev_fork2, 0));
+      used_side2 = true;
+      ks::launch_hager(dt, nb, f->dinv.p, nb.count, f->side2);
+      L.count[0] += ks::hager_launches(nb);
+      KS_CUDA(cudaGetLastError());
+    } else {
+      deferred.push_back(lev);
+      if (!wide)
+        if (int rc = flush()) return rc;
+    }
     if (int rc2 = mark(f->ev_level[lev])) return rc2;
   }
   if (int rc = flush()) return rc;
-  KS_CUDA(cudaEventRecord(f->ev_join, f->side));
-  KS_CUDA(cudaStreamWaitEvent(st, f->ev_join, 0));
+  if (used_side) {
+    KS_CUDA(cudaEventRecord(f->ev_join, f->side));
+    KS_CUDA(cudaStreamWaitEvent(st, f->ev_join, 0));
+  }
+  if (used_side2) {
+    KS_CUDA(cudaEventRecord(f->ev_join2, f->side2));
+    KS_CUDA(cudaStreamWaitEvent(st, f->ev_join2, 0));
+  }
   return KS_OK;
 }
 
@@ -2272,6 +2303,9 @@ void ks_destroy(ks_factor* f) {
   f->release_all();
   if (f->graph_exec) cudaGraphExecDestroy(f->graph_exec);
   if (f->side) cudaStreamDestroy(f->side);
+  if (f->side2) cudaStreamDestroy(f->side2);
+  if (f->ev_fork2) cudaEventDestroy(f->ev_fork2);
+  if (f->ev_join2) cudaEventDestroy(f->ev_join2);
   if (f->cap) cudaStreamDestroy(f->cap);
   for (auto g : f->gst)
     if (g) cudaStreamDestroy(g);

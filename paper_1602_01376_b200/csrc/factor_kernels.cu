@@ -1219,6 +1219,11 @@ static void launch_hager_own(const DevTree& t, const NodeBatch& nb, double* dinv
 int hager_launches(const NodeBatch& nb) { return nb.t_pad <= 1024 ? 2 : 1; }
 
 void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, int max_ctas, cudaStream_t st) {
+  const char* e = std::getenv("KS_HAGER_IMPL");
+  if (e && e[0] == 'b') {
+    launch_hager_blocked(t, nb, st);
+    return;
+  }
   if (nb.t_pad <= 512) launch_hager_own<8, 512>(t, nb, dinv, max_ctas, st);
   else if (nb.t_pad <= 1024) launch_hager_own<8, 1024>(t, nb, dinv, max_ctas, st);
   else launch_hager_blocked(t, nb, st);
