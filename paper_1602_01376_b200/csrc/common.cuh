@@ -39,6 +39,44 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// exp(x) for x <= 0 (the Gaussian kernel's argument, kernels.py:107-111) on
+// the FMA pipe only: x = k ln2 + r (Cody-Waite, k = rint(x log2 e) by the
+// 1.5*2^52 shift), exp(r) by its degree-13 Taylor polynomial (|r| <= ln2/2:
+// truncation < 5e-18 relative), times 2^k through the exponent bits (two steps
+// below 2^-1022, so subnormal results round once). Within ~1 ulp of exp().
+// Taylor coefficients 1/n!, n = 13..2, as constant-bank operands of the DFMAs
+static __constant__ double kExpTaylor[12] = {1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08,
+                                             2.755731922398589e-07,  2.7557319223985893e-06, 2.48015873015873e-05,
+                                             1.984126984126984e-04,  1.388888888888889e-03,  8.333333333333333e-03,
+                                             4.1666666666666664e-02, 1.6666666666666666e-01, 0.5};
+// cf: the Taylor coefficients held in registers by a caller that evaluates
+// many exponentials (no constant reloads per call)
+__device__ __forceinline__ double exp_neg(double x, const double (&cf)[12]) {
+  if (!(x > -745.2)) return x < 0.0 ? 0.0 : x;  // underflow (NaN passes through)
+  const double shift = 6755399441055744.0;
+  const double kd = fma(x, 1.4426950408889634, shift);
+  const double k = kd - shift;
+  const int ki = __double2loint(kd);
+  double r = fma(k, -6.93147180559945286227e-01, x);
+  r = fma(k, -2.31904681384629955842e-17, r);
+  double p = cf[0];
+#pragma unroll
+  for (int n = 1; n < 12; ++n) p = fma(p, r, cf[n]);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  if (ki >= -1022) return p * __hiloint2double((ki + 1023) << 20, 0);
+  return p * __hiloint2double((ki + 1623) << 20, 0) * 2.4099198651028841e-181;  // 2^(k+600) * 2^-600
+}
+__device__ __forceinline__ void exp_coeffs(double (&cf)[12]) {
+#pragma unroll
+  for (int n = 0; n < 12; ++n) cf[n] = kExpTaylor[n];
+}
+__device__ __forceinline__ double exp_neg(double x) {
+  double cf[12];
+  exp_coeffs(cf);
+  return exp_neg(x, cf);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -66,7 +66,7 @@ cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st) {
   GemmArgs t = g;
   t.tri = 1;
   // K = d is small and the exp epilogue dominates: small tiles, 2 stages, many warps per SM
-  return launch<64, 64, 2, 2, false, true, 2, 1>(t, st);
+  return launch<64, 64, 2, 4, false, true, 2, 1>(t, st);
 }
 
 cudaError_t gemm_update_trsm(const GemmArgs& g, cudaStream_t st) {

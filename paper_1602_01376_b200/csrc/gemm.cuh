@@ -263,6 +263,34 @@ __global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
     bsz = g.ge.size[b];
     bbeg = g.ge.begin[b];
   }
+  if constexpr (EPI == 1) {
+    // tiles strictly below the diagonal and inside the leaf (120 of the 136
+    // lower tiles of a full 1024-point leaf): no per-element cases
+    if (n0 + BN <= m0 && m0 + BM <= bsz) {
+      double cf[12];
+      exp_coeffs(cf);
+      double xc[Cfg::NT][2];
+#pragma unroll
+      for (int j = 0; j < Cfg::NT; ++j) {
+        xc[j][0] = g.ge.xx[bbeg + n0 + wn0 + j * 8 + 2 * tq];
+        xc[j][1] = g.ge.xx[bbeg + n0 + wn0 + j * 8 + 2 * tq + 1];
+      }
+#pragma unroll
+      for (int i = 0; i < Cfg::MT; ++i) {
+        const int r = m0 + wm0 + i * 8 + gq;
+        const double xr = g.ge.xx[bbeg + r];
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; ++j) {
+          const int c = n0 + wn0 + j * 8 + 2 * tq;
+          double2 v;
+          v.x = exp_neg(fmax(xr + xc[j][0] - 2.0 * acc[i][j][0], 0.0) * den, cf);
+          v.y = exp_neg(fmax(xr + xc[j][1] - 2.0 * acc[i][j][1], 0.0) * den, cf);
+          *reinterpret_cast<double2*>(C + (int64_t)r * g.C.ld + c) = v;
+        }
+      }
+      return;
+    }
+  }
 #pragma unroll
   for (int i = 0; i < Cfg::MT; ++i) {
     const int r = m0 + wm0 + i * 8 + gq;
@@ -285,7 +313,7 @@ __global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
           else if (r == cc) o[u] = 1.0 + lam;
           else {
             const double sq = fmax(xr + g.ge.xx[bbeg + cc] - 2.0 * acc[i][j][u], 0.0);
-            o[u] = exp(sq * den);
+            o[u] = exp_neg(sq * den);
           }
         }
         v.x = o[0];
