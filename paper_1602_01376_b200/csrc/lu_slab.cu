@@ -10,14 +10,17 @@
 //   * each CTA owns a W-column slab of one node's matrix, resident in shared
 //     memory for the whole factorization (T x (W+1) doubles, <= 204 KB);
 //   * step j (columns [jW, jW+W)) is factored by the CTA owning slab j: the
-//     candidate rows in registers (lu_panel.cuh), the augmented rows after,
-//     then the slab's rows [jW, T) are published to HBM/L2 with a release flag;
+//     candidate rows in registers (lu_panel.cuh), published (rows [jW, t_pad))
+//     with a release flag; then the augmented rows (never pivots) are
+//     eliminated and published behind a second flag, off the path from one
+//     panel to the next;
 //   * every other CTA acquires the flag, applies the step's row interchanges to
 //     its slab (LAPACK convention: also to the finished L columns), and, for
 //     slabs right of the panel, U12 = L11^-1 A12 and the trailing update
 //     A22 -= L21 U12 on the fp64 tensor pipe (DMMA m8n8k4, L21 streamed from L2);
-//   * slab j+1 is updated by its owner right after step j, so the next panel
-//     starts while the other slabs are still updating (look-ahead of one step);
+//   * slab j+1 updates its candidate rows right after step j and starts the
+//     next panel while the other slabs are still updating (look-ahead of one
+//     step); its augmented rows catch up after that panel;
 //   * after the last step the slabs are written back in place (same layout as
 //     the launch sequence: L\U of Pi Z, U12 = L^-1 Pi P^T, L21aug, Schur block)
 //     and the H slabs write sym(H) for the parent (solver.py:163).
@@ -233,7 +236,21 @@ __global__ void __launch_bounds__(NT, 1)
         if (threadIdx.x < W) spiv[threadIdx.x] = pivk[c0 + threadIdx.x] - c0;
         __syncthreads();
         slab_moves<W, NT, LD>(Sl, c0, spiv, msrc, mdst);
-        // augmented rows [TP, T): eliminated against the panel's U rows
+        // publish the candidate rows [c0, TP) first: the next panel needs only them
+        for (int e = threadIdx.x; e < (TP - c0) * W; e += NT) {
+          const int r = c0 + e / W, c = e % W;
+          A[(int64_t)r * T + col0 + c] = Sl[r * LD + c];
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(sy, (unsigned)(j + 1));
+        // augmented rows [TP, T): the previous step's update (deferred while this
+        // CTA was that step's look-ahead), then elimination against the U rows
+        if (j > 0) {
+          if (!cta_wait(sy + 3, (unsigned)j, err, &s_ok)) return;
+          slab_update<W, NT, LD>(Sl, A, T, c0 - W, TP, T);
+          __syncthreads();
+        }
         for (int r = TP + threadIdx.x; r < T; r += NT) {
           double x[W];
 #pragma unroll
@@ -250,14 +267,13 @@ __global__ void __launch_bounds__(NT, 1)
         }
         __syncthreads();
         stamp(k, j, 2);
-        // publish rows [c0, T) of the panel (current row order)
-        for (int e = threadIdx.x; e < (T - c0) * W; e += NT) {
-          const int r = c0 + e / W, c = e % W;
+        for (int e = threadIdx.x; e < (T - TP) * W; e += NT) {
+          const int r = TP + e / W, c = e % W;
           A[(int64_t)r * T + col0 + c] = Sl[r * LD + c];
         }
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) st_release(sy, (unsigned)(j + 1));
+        if (threadIdx.x == 0) st_release(sy + 3, (unsigned)(j + 1));
         stamp(k, j, 3);
         continue;
       }
@@ -298,7 +314,13 @@ __global__ void __launch_bounds__(NT, 1)
       }
       __syncthreads();
       stamp(k, j, 2);
-      slab_update<W, NT, LD>(Sl, A, T, c0, c0 + W, T);
+      slab_update<W, NT, LD>(Sl, A, T, c0, c0 + W, TP);  // candidate rows
+      // the augmented rows once the owner has published them; the look-ahead
+      // slab defers this until after its own panel
+      if (!(slab == j + 1 && slab < nst)) {
+        if (!cta_wait(sy + 3, (unsigned)(j + 1), err, &s_ok)) return;
+        slab_update<W, NT, LD>(Sl, A, T, c0, TP, T);
+      }
       __syncthreads();
       stamp(k, j, 3);
     }
