@@ -79,16 +79,16 @@ __device__ bool cta_wait(const unsigned* p, unsigned target, unsigned* err, int*
   return *s_ok != 0;
 }
 
-// rows [c0, TP) of the slab permuted by the step's W row interchanges
-// (spiv[i] = pivot of column c0+i, relative to c0): each touched row is
-// followed through the swap sequence; all loads, one barrier, all stores.
-template <int W, int NT, int LD>
+// rows [c0, TP) of the slab (all SW columns) permuted by the step's NP row
+// interchanges (spiv[i] = pivot of row c0+i, relative to c0): each touched row
+// is followed through the swap sequence; all loads, one barrier, all stores.
+template <int NP, int SW, int NT, int LD>
 __device__ __forceinline__ void slab_moves(double* Sl, int c0, const int* spiv, int* msrc, int* mdst) {
-  if (threadIdx.x < 2 * W) {
-    const int x = threadIdx.x < W ? (int)threadIdx.x : spiv[threadIdx.x - W];
+  if (threadIdx.x < 2 * NP) {
+    const int x = threadIdx.x < NP ? (int)threadIdx.x : spiv[threadIdx.x - NP];
     int f = x;
 #pragma unroll 8
-    for (int i = 0; i < W; ++i) {
+    for (int i = 0; i < NP; ++i) {
       const int p = spiv[i];
       f = (f == i) ? p : (f == p ? i : f);
     }
@@ -96,37 +96,40 @@ __device__ __forceinline__ void slab_moves(double* Sl, int c0, const int* spiv, 
     mdst[threadIdx.x] = f;
   }
   __syncthreads();
-  constexpr int E = (2 * W * W + NT - 1) / NT;
+  constexpr int NE = 2 * NP * SW;
+  constexpr int E = (NE + NT - 1) / NT;
   double v[E];
 #pragma unroll
   for (int u = 0; u < E; ++u) {
     const int e = threadIdx.x + u * NT;
-    if (e < 2 * W * W) v[u] = Sl[(c0 + msrc[e / W]) * LD + e % W];
+    if (e < NE) v[u] = Sl[(c0 + msrc[e / SW]) * LD + e % SW];
   }
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < E; ++u) {
     const int e = threadIdx.x + u * NT;
-    if (e < 2 * W * W) {
-      const int m = e / W;
-      if (msrc[m] != mdst[m]) Sl[(c0 + mdst[m]) * LD + e % W] = v[u];
+    if (e < NE) {
+      const int m = e / SW;
+      if (msrc[m] != mdst[m]) Sl[(c0 + mdst[m]) * LD + e % SW] = v[u];
     }
   }
   __syncthreads();
 }
 
-// Sl rows [r0, T) -= L21 (A rows [r0, T), columns [c0, c0+W), row-major ld T)
-// x U12 (Sl rows [c0, c0+W)): warp tiles of 16 rows x W columns on DMMA.
-template <int W, int NT, int LD>
-__device__ __forceinline__ void slab_update(double* Sl, const double* A, int64_t T, int c0, int r0, int rend) {
-  constexpr int KS = W / 4, NN = W / 8;
+// Sl[r][cc + n] -= sum_k A[r][ac + k] * Sl[ur + k][cc + n] for rows [r0, rend),
+// k < KW, n < NC: warp tiles of 16 rows x NC columns on DMMA. A is the slab
+// itself (ASM: shared memory, ld LD) or a published panel (global, ld lda).
+template <int KW, int NC, int NT, int LD, bool ASM>
+__device__ __forceinline__ void tile_update(double* Sl, int cc, const double* A, int64_t lda, int ac, int ur, int r0,
+                                            int rend) {
+  constexpr int KS = KW / 4, NN = NC / 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
   double bf[KS][NN];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-    for (int n = 0; n < NN; ++n) bf[ks][n] = Sl[(c0 + ks * 4 + tq) * LD + n * 8 + gq];
+    for (int n = 0; n < NN; ++n) bf[ks][n] = Sl[(ur + ks * 4 + tq) * LD + cc + n * 8 + gq];
   const int ntiles = (rend - r0) / 16;
   for (int t = warp; t < ntiles; t += NT / 32) {
     const int r = r0 + t * 16;
@@ -134,14 +137,17 @@ __device__ __forceinline__ void slab_update(double* Sl, const double* A, int64_t
 #pragma unroll
     for (int m = 0; m < 2; ++m)
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) af[m][ks] = -__ldcg(A + (int64_t)(r + m * 8 + gq) * T + c0 + ks * 4 + tq);
+      for (int ks = 0; ks < KS; ++ks) {
+        const int row = r + m * 8 + gq, col = ac + ks * 4 + tq;
+        af[m][ks] = ASM ? -Sl[row * LD + col] : -__ldcg(A + (int64_t)row * lda + col);
+      }
     double acc[2][NN][2];
 #pragma unroll
     for (int m = 0; m < 2; ++m)
 #pragma unroll
       for (int n = 0; n < NN; ++n) {
-        acc[m][n][0] = Sl[(r + m * 8 + gq) * LD + n * 8 + 2 * tq];
-        acc[m][n][1] = Sl[(r + m * 8 + gq) * LD + n * 8 + 2 * tq + 1];
+        acc[m][n][0] = Sl[(r + m * 8 + gq) * LD + cc + n * 8 + 2 * tq];
+        acc[m][n][1] = Sl[(r + m * 8 + gq) * LD + cc + n * 8 + 2 * tq + 1];
       }
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
@@ -153,29 +159,61 @@ __device__ __forceinline__ void slab_update(double* Sl, const double* A, int64_t
     for (int m = 0; m < 2; ++m)
 #pragma unroll
       for (int n = 0; n < NN; ++n) {
-        Sl[(r + m * 8 + gq) * LD + n * 8 + 2 * tq] = acc[m][n][0];
-        Sl[(r + m * 8 + gq) * LD + n * 8 + 2 * tq + 1] = acc[m][n][1];
+        Sl[(r + m * 8 + gq) * LD + cc + n * 8 + 2 * tq] = acc[m][n][0];
+        Sl[(r + m * 8 + gq) * LD + cc + n * 8 + 2 * tq + 1] = acc[m][n][1];
       }
+  }
+}
+
+// Sl rows [c0, c0+KW), columns [cc, cc+NC) := L^-1 (...), L unit lower KW x KW
+// at Lm (ld LLD, shared memory): one thread per column.
+template <int KW, int NC, int LD, int LLD>
+__device__ __forceinline__ void tile_trsm(double* Sl, int c0, int cc, const double* Lm) {
+  if (threadIdx.x < NC) {
+    double x[KW];
+#pragma unroll
+    for (int i = 0; i < KW; ++i) x[i] = Sl[(c0 + i) * LD + cc + threadIdx.x];
+#pragma unroll
+    for (int i = 1; i < KW; ++i) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int q = 0; q + 3 < i; q += 4) {
+        s0 = fma(Lm[i * LLD + q], x[q], s0);
+        s1 = fma(Lm[i * LLD + q + 1], x[q + 1], s1);
+        s2 = fma(Lm[i * LLD + q + 2], x[q + 2], s2);
+        s3 = fma(Lm[i * LLD + q + 3], x[q + 3], s3);
+      }
+#pragma unroll
+      for (int q = i & ~3; q < i; ++q) s0 = fma(Lm[i * LLD + q], x[q], s0);
+      x[i] -= (s0 + s1) + (s2 + s3);
+    }
+#pragma unroll
+    for (int i = 0; i < KW; ++i) Sl[(c0 + i) * LD + cc + threadIdx.x] = x[i];
   }
 }
 
 }  // namespace
 
-template <int W, int RPT, int NT>
+// SW: slab width (columns per CTA); PW: panel width (columns per step, SW/PW
+// steps per slab: the second panel of a slab is updated by its own CTA from
+// shared memory right after the first); RPT: candidate rows per thread.
+template <int SW, int PW, int RPT, int NT>
 __global__ void __launch_bounds__(NT, 1)
     k_lu_slab(NodeBatch nb, double* Hout, int64_t h_stride, int write_h, unsigned* sync, unsigned* err, int groups) {
-  constexpr int LD = W + 1;  // odd row stride: conflict-free row-per-thread access
+  constexpr int LD = SW + 1;  // odd row stride: conflict-free row-per-thread access
   constexpr int NW = NT / 32;
-  constexpr int CBX = (W <= 16) ? W : 16;
+  constexpr int HV = SW / PW;  // steps per slab
+  static_assert(HV == 1 || HV == 2, "slab = 1 or 2 panels");
   const int T = nb.T, TP = nb.t_pad, S = nb.s_pad;
-  const int G = T / W, nst = TP / W;
+  const int G = T / SW, nzs = TP / SW, nst = TP / PW;
   const int slab = blockIdx.x % G;
-  const int col0 = slab * W;
+  const int col0 = slab * SW;
   extern __shared__ __align__(16) double smem[];
-  double* Sl = smem;                   // T x LD: this CTA's slab
-  double* L11 = smem + (size_t)T * LD;  // W x LD: unit-lower diagonal block of the step
-  __shared__ PanelShared<NW, W> ps;
-  __shared__ int spiv[W], msrc[2 * W], mdst[2 * W];
+  double* Sl = smem;                    // T x LD: this CTA's slab
+  double* L11 = smem + (size_t)T * LD;  // PW x (PW+1): unit-lower diagonal block of the step
+  __shared__ PanelShared<NW, PW> ps;
+  __shared__ double urcp[SW];  // the pivots' reciprocals of this slab's panels
+  __shared__ int spiv[PW], msrc[2 * PW], mdst[2 * PW];
   __shared__ int s_ok;
   long long* ts = g_slab_ts;
   auto stamp = [&](int k, int j, int ph) {
@@ -186,144 +224,158 @@ __global__ void __launch_bounds__(NT, 1)
     unsigned* sy = sync + 4 * k;
     int* pivk = nb.piv + (int64_t)k * TP;
     __syncthreads();
-    for (int e = threadIdx.x; e < T * W; e += NT) {
-      const int r = e / W, c = e % W;
+    for (int e = threadIdx.x; e < T * SW; e += NT) {
+      const int r = e / SW, c = e % SW;
       Sl[r * LD + c] = A[(int64_t)r * T + col0 + c];
     }
     __syncthreads();
-    if (slab < nst) {  // ||Z||_1 over this slab's columns (rows < t_pad)
-      constexpr int NG = NT / W;
-      double* red = &ps.cand[0][0][0];  // 2*NW*W >= NG*W doubles
-      const int c = threadIdx.x % W, g = threadIdx.x / W;
-      double s = 0.0;
-      for (int r = g; r < TP; r += NG) s += fabs(Sl[r * LD + c]);
-      red[g * W + c] = s;
+    if (slab < nzs) {  // ||Z||_1 over this slab's columns (rows < t_pad), linalg.py:176
+      constexpr int NG = NT / SW;
+      double* red = &ps.cand[0][0][0];  // 2*NW*PW >= NG*SW doubles
+      static_assert(2 * NW * PW >= NG * SW, "scratch");
+      const int c = threadIdx.x % SW, g = threadIdx.x / SW;
+      double sacc = 0.0;
+      for (int r = g; r < TP; r += NG) sacc += fabs(Sl[r * LD + c]);
+      red[g * SW + c] = sacc;
       __syncthreads();
       if (threadIdx.x < 32) {
         double t = 0.0;
-        if (threadIdx.x < W)
-          for (int gg = 0; gg < NG; ++gg) t += red[gg * W + threadIdx.x];
+        if (threadIdx.x < SW)
+          for (int gg = 0; gg < NG; ++gg) t += red[gg * SW + threadIdx.x];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
         if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(nb.norm1 + k), __double_as_longlong(t));
       }
       __syncthreads();  // the scratch is the panel's candidate buffer
     }
+    // Augmented rows lag behind: aug_done = steps whose update has been applied
+    // to this slab's augmented rows (the columns right of that step's panel).
+    // They never pivot and no panel needs them, so they are caught up off the
+    // panel-to-panel path (before this slab's own eliminations and at the end).
+    int aug_done = 0;
+    auto aug_catch_up = [&](int upto) -> bool {
+      for (int t = aug_done; t < upto; ++t) {
+        const int ow = t / HV, ct = t * PW;
+        if (ow < slab) {
+          if (!cta_wait(sy + 3, (unsigned)(t + 1), err, &s_ok)) return false;
+          tile_update<PW, SW, NT, LD, false>(Sl, 0, A, T, ct, ct, TP, T);
+        } else if (ow == slab && (t % HV) + 1 < HV) {  // own left panel -> the right half
+          if constexpr (HV > 1) {
+            __syncthreads();
+            tile_update<PW, SW - PW, NT, LD, true>(Sl, PW, nullptr, 0, 0, ct, TP, T);
+          }
+        }
+      }
+      aug_done = max(aug_done, upto);
+      __syncthreads();
+      return true;
+    };
     for (int j = 0; j < nst; ++j) {
-      const int c0 = j * W;
-      if (slab == j) {
-        // ---- panel: candidate rows [c0, TP) in registers ----
-        const int rows = TP - c0;
-        __syncthreads();  // the previous step's update of this slab is complete
-        stamp(k, j, 0);
-        {
-          double a[RPT][W];
-          int pos[RPT];
-          bool done[RPT];
-#pragma unroll
-          for (int i = 0; i < RPT; ++i) {
-            const int r = threadIdx.x + i * NT;
-            pos[i] = r;
-            done[i] = (r >= rows);
-#pragma unroll
-            for (int jj = 0; jj < W; ++jj) a[i][jj] = (r < rows) ? Sl[(c0 + r) * LD + jj] : 0.0;
+      const int c0 = j * PW;
+      const int owner = j / HV;
+      if (slab == owner) {
+        // ---- this slab's HV panels: candidate rows first, published step by step ----
+        for (int hh = 0; hh < HV; ++hh) {
+          const int jj = j + hh, cj = jj * PW, pc = hh * PW;
+          __syncthreads();  // the previous step's update of this slab is complete
+          if (hh > 0) {
+            // own previous panel (columns [0, PW)): U12 and the candidate rows of
+            // this half, from shared memory
+            tile_trsm<PW, PW, LD, LD>(Sl, cj - PW, PW, Sl + (size_t)(cj - PW) * LD);
+            __syncthreads();
+            tile_update<PW, PW, NT, LD, true>(Sl, PW, nullptr, 0, 0, cj - PW, cj, TP);
+            __syncthreads();
           }
-          panel_columns<W, RPT, NT, CBX>(a, pos, done, ps, Sl + (size_t)c0 * LD, LD, rows, pivk + c0, c0, nb.info + k,
-                                         c0);
-        }
-        __syncthreads();
-        stamp(k, j, 1);
-        if (threadIdx.x < W) spiv[threadIdx.x] = pivk[c0 + threadIdx.x] - c0;
-        __syncthreads();
-        slab_moves<W, NT, LD>(Sl, c0, spiv, msrc, mdst);
-        // publish the candidate rows [c0, TP) first: the next panel needs only them
-        for (int e = threadIdx.x; e < (TP - c0) * W; e += NT) {
-          const int r = c0 + e / W, c = e % W;
-          A[(int64_t)r * T + col0 + c] = Sl[r * LD + c];
-        }
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) st_release(sy, (unsigned)(j + 1));
-        // augmented rows [TP, T): the previous step's update (deferred while this
-        // CTA was that step's look-ahead), then elimination against the U rows
-        if (j > 0) {
-          if (!cta_wait(sy + 3, (unsigned)j, err, &s_ok)) return;
-          slab_update<W, NT, LD>(Sl, A, T, c0 - W, TP, T);
+          stamp(k, jj, 0);
+          const int rows = TP - cj;
+          {
+            double a[RPT][PW];
+            int pos[RPT];
+            bool done[RPT];
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+              const int r = threadIdx.x + i * NT;
+              pos[i] = r;
+              done[i] = (r >= rows);
+#pragma unroll
+              for (int q = 0; q < PW; ++q) a[i][q] = (r < rows) ? Sl[(cj + r) * LD + pc + q] : 0.0;
+            }
+            panel_columns<PW, RPT, NT, (PW <= 16 ? PW : 16)>(a, pos, done, ps, Sl + (size_t)cj * LD + pc, LD, rows,
+                                                             pivk + cj, cj, nb.info + k, cj);
+          }
           __syncthreads();
-        }
-        for (int r = TP + threadIdx.x; r < T; r += NT) {
-          double x[W];
-#pragma unroll
-          for (int jj = 0; jj < W; ++jj) x[jj] = Sl[r * LD + jj];
-#pragma unroll
-          for (int kk = 0; kk < W; ++kk) {
-            const double l = x[kk] * ps.urcp[kk];
-            x[kk] = l;
-#pragma unroll
-            for (int jj = kk + 1; jj < W; ++jj) x[jj] = fma(-l, Sl[(c0 + kk) * LD + jj], x[jj]);
+          stamp(k, jj, 1);
+          if (threadIdx.x < PW) {
+            spiv[threadIdx.x] = pivk[cj + threadIdx.x] - cj;
+            urcp[pc + threadIdx.x] = ps.urcp[threadIdx.x];
           }
+          __syncthreads();
+          slab_moves<PW, SW, NT, LD>(Sl, cj, spiv, msrc, mdst);
+          for (int e = threadIdx.x; e < (TP - cj) * PW; e += NT) {
+            const int r = cj + e / PW, c = e % PW;
+            A[(int64_t)r * T + col0 + pc + c] = Sl[r * LD + pc + c];
+          }
+          __threadfence();
+          __syncthreads();
+          if (threadIdx.x == 0) st_release(sy, (unsigned)(jj + 1));
+          stamp(k, jj, 2);
+        }
+        // ---- then their augmented rows ----
+        for (int hh = 0; hh < HV; ++hh) {
+          const int jj = j + hh, cj = jj * PW, pc = hh * PW;
+          if (!aug_catch_up(jj)) return;
+          for (int r = TP + threadIdx.x; r < T; r += NT) {
+            double x[PW];
 #pragma unroll
-          for (int jj = 0; jj < W; ++jj) Sl[r * LD + jj] = x[jj];
+            for (int q = 0; q < PW; ++q) x[q] = Sl[r * LD + pc + q];
+#pragma unroll
+            for (int kk = 0; kk < PW; ++kk) {
+              const double l = x[kk] * urcp[pc + kk];
+              x[kk] = l;
+#pragma unroll
+              for (int q = kk + 1; q < PW; ++q) x[q] = fma(-l, Sl[(cj + kk) * LD + pc + q], x[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < PW; ++q) Sl[r * LD + pc + q] = x[q];
+          }
+          __syncthreads();
+          for (int e = threadIdx.x; e < (T - TP) * PW; e += NT) {
+            const int r = TP + e / PW, c = e % PW;
+            A[(int64_t)r * T + col0 + pc + c] = Sl[r * LD + pc + c];
+          }
+          __threadfence();
+          __syncthreads();
+          if (threadIdx.x == 0) st_release(sy + 3, (unsigned)(jj + 1));
+          stamp(k, jj, 3);
         }
-        __syncthreads();
-        stamp(k, j, 2);
-        for (int e = threadIdx.x; e < (T - TP) * W; e += NT) {
-          const int r = TP + e / W, c = e % W;
-          A[(int64_t)r * T + col0 + c] = Sl[r * LD + c];
-        }
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) st_release(sy + 3, (unsigned)(j + 1));
-        stamp(k, j, 3);
+        j += HV - 1;
         continue;
       }
       // ---- any other slab: acquire step j ----
       if (!cta_wait(sy, (unsigned)(j + 1), err, &s_ok)) return;
       stamp(k, j, 0);
-      if (threadIdx.x < W) spiv[threadIdx.x] = __ldcg(pivk + c0 + threadIdx.x) - c0;
+      if (threadIdx.x < PW) spiv[threadIdx.x] = __ldcg(pivk + c0 + threadIdx.x) - c0;
       __syncthreads();
-      slab_moves<W, NT, LD>(Sl, c0, spiv, msrc, mdst);
+      slab_moves<PW, SW, NT, LD>(Sl, c0, spiv, msrc, mdst);
       stamp(k, j, 1);
-      if (slab < j) continue;  // finished L columns: the interchanges only
-      // U12 = L11^-1 A12 (one thread per column)
-      for (int e = threadIdx.x; e < W * W; e += NT) {
-        const int i = e / W, jj = e % W;
-        L11[i * LD + jj] = __ldcg(A + (int64_t)(c0 + i) * T + c0 + jj);
+      if (slab < owner) continue;  // finished L columns: the interchanges only
+      for (int e = threadIdx.x; e < PW * PW; e += NT) {
+        const int i = e / PW, q = e % PW;
+        L11[i * (PW + 1) + q] = __ldcg(A + (int64_t)(c0 + i) * T + c0 + q);
       }
       __syncthreads();
-      if (threadIdx.x < W) {
-        double x[W];
-#pragma unroll
-        for (int i = 0; i < W; ++i) x[i] = Sl[(c0 + i) * LD + threadIdx.x];
-#pragma unroll
-        for (int i = 1; i < W; ++i) {
-          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-          for (int q = 0; q + 3 < i; q += 4) {
-            s0 = fma(L11[i * LD + q], x[q], s0);
-            s1 = fma(L11[i * LD + q + 1], x[q + 1], s1);
-            s2 = fma(L11[i * LD + q + 2], x[q + 2], s2);
-            s3 = fma(L11[i * LD + q + 3], x[q + 3], s3);
-          }
-#pragma unroll
-          for (int q = i & ~3; q < i; ++q) s0 = fma(L11[i * LD + q], x[q], s0);
-          x[i] -= (s0 + s1) + (s2 + s3);
-        }
-#pragma unroll
-        for (int i = 0; i < W; ++i) Sl[(c0 + i) * LD + threadIdx.x] = x[i];
-      }
+      tile_trsm<PW, SW, LD, PW + 1>(Sl, c0, 0, L11);
       __syncthreads();
       stamp(k, j, 2);
-      slab_update<W, NT, LD>(Sl, A, T, c0, c0 + W, TP);  // candidate rows
-      // the augmented rows once the owner has published them; the look-ahead
-      // slab defers this until after its own panel
-      if (!(slab == j + 1 && slab < nst)) {
-        if (!cta_wait(sy + 3, (unsigned)(j + 1), err, &s_ok)) return;
-        slab_update<W, NT, LD>(Sl, A, T, c0, TP, T);
-      }
+      tile_update<PW, SW, NT, LD, false>(Sl, 0, A, T, c0, c0, c0 + PW, TP);  // candidate rows
+      // augmented rows one step behind, except on the slab that owns the next
+      // panel (it catches up after its panels)
+      const bool lookahead = (j + 1 < nst) && ((j + 1) / HV == slab);
+      if (!lookahead && !aug_catch_up(j)) return;
       __syncthreads();
       stamp(k, j, 3);
     }
+    if (!aug_catch_up(nst)) return;
     // ---- every CTA of the node is past the last step: write the slab back ----
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -331,19 +383,19 @@ __global__ void __launch_bounds__(NT, 1)
       atomicAdd(sy + 1, 1u);
     }
     if (!cta_wait(sy + 1, (unsigned)G, err, &s_ok)) return;
-    for (int e = threadIdx.x; e < T * W; e += NT) {
-      const int r = e / W, c = e % W;
+    for (int e = threadIdx.x; e < T * SW; e += NT) {
+      const int r = e / SW, c = e % SW;
       A[(int64_t)r * T + col0 + c] = Sl[r * LD + c];
     }
-    if (write_h && slab >= nst) {  // H = sym(trailing block) -> Hout[node] (solver.py:163)
+    if (write_h && slab >= nzs) {  // H = sym(trailing block) -> Hout[node] (solver.py:163)
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) atomicAdd(sy + 2, 1u);
-      if (!cta_wait(sy + 2, (unsigned)(G - nst), err, &s_ok)) return;
-      double* h = Hout + (int64_t)nb.node[k] * h_stride;
-      for (int e = threadIdx.x; e < S * W; e += NT) {
-        const int i = e / W, jj = e % W, j2 = col0 - TP + jj;
-        h[(int64_t)i * S + j2] = 0.5 * (Sl[(TP + i) * LD + jj] + __ldcg(A + (int64_t)(TP + j2) * T + TP + i));
+      if (!cta_wait(sy + 2, (unsigned)(G - nzs), err, &s_ok)) return;
+      double* hh = Hout + (int64_t)nb.node[k] * h_stride;
+      for (int e = threadIdx.x; e < S * SW; e += NT) {
+        const int i = e / SW, jj = e % SW, j2 = col0 - TP + jj;
+        hh[(int64_t)i * S + j2] = 0.5 * (Sl[(TP + i) * LD + jj] + __ldcg(A + (int64_t)(TP + j2) * T + TP + i));
       }
     }
   }
@@ -351,12 +403,12 @@ __global__ void __launch_bounds__(NT, 1)
 
 namespace {
 
-template <int W, int RPT>
+template <int SW, int PW, int RPT>
 int launch_slab_t(const NodeBatch& nb, double* H, int64_t hs, bool write_h, unsigned* sync, unsigned* err,
                   cudaStream_t st) {
   constexpr int NT = 512;
-  const size_t smem = (size_t)(nb.T + W) * (W + 1) * sizeof(double);
-  auto kern = k_lu_slab<W, RPT, NT>;
+  const size_t smem = ((size_t)nb.T * (SW + 1) + (size_t)PW * (PW + 1)) * sizeof(double);
+  auto kern = k_lu_slab<SW, PW, RPT, NT>;
   static size_t set = 0;
   static int max_active = 0;
   if (smem > set) {
@@ -368,7 +420,7 @@ int launch_slab_t(const NodeBatch& nb, double* H, int64_t hs, bool write_h, unsi
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
     max_active = per_sm * sms;
   }
-  const int G = nb.T / W;
+  const int G = nb.T / SW;
   const int groups = std::min(nb.count, max_active / G);
   if (groups < 1) return -1;
   cudaLaunchConfig_t cfg = {};
@@ -388,6 +440,9 @@ int launch_slab_t(const NodeBatch& nb, double* H, int64_t hs, bool write_h, unsi
 
 // W = 32 while a 32-column slab fits (T <= 800: configs 1-4), else 16 (T <= 1600).
 int slab_width(const NodeBatch& nb) {
+  const char* e = std::getenv("KS_SLAB_W");  // 16: force 16-column slabs where they fit
+  if (e && std::atoi(e) == 16 && nb.T % 16 == 0 && nb.t_pad <= 1024 && (size_t)(nb.T + 16) * 17 * 8 <= 212 * 1024)
+    return 16;
   if (nb.T % 32 == 0 && nb.t_pad <= 512 && (size_t)(nb.T + 32) * 33 * 8 <= 212 * 1024) return 32;
   if (nb.T % 16 == 0 && nb.t_pad <= 1024 && (size_t)(nb.T + 16) * 17 * 8 <= 212 * 1024) return 16;
   return 0;
@@ -412,9 +467,12 @@ int launch_lu_slab(const NodeBatch& nb, double* H, int64_t h_stride, bool write_
                    cudaStream_t st) {
   slab_ts_buf();
   const int w = slab_width(nb);
-  if (w == 32) return launch_slab_t<32, 1>(nb, H, h_stride, write_h, sync, err, st);
-  if (w == 16) return nb.t_pad <= 512 ? launch_slab_t<16, 1>(nb, H, h_stride, write_h, sync, err, st)
-                                      : launch_slab_t<16, 2>(nb, H, h_stride, write_h, sync, err, st);
+  const char* e = std::getenv("KS_SLAB_PW");  // 32: one 32-column panel per slab step
+  const bool pw32 = e && std::atoi(e) == 32;
+  if (w == 32) return pw32 ? launch_slab_t<32, 32, 1>(nb, H, h_stride, write_h, sync, err, st)
+                           : launch_slab_t<32, 16, 1>(nb, H, h_stride, write_h, sync, err, st);
+  if (w == 16) return nb.t_pad <= 512 ? launch_slab_t<16, 16, 1>(nb, H, h_stride, write_h, sync, err, st)
+                                      : launch_slab_t<16, 16, 2>(nb, H, h_stride, write_h, sync, err, st);
   return -1;
 }
 

@@ -25,11 +25,13 @@ T = 3 * 256 if cfg.name == "cfg3" else None
 G = int(np.sum(~np.isnan(a[:, 0, 0])))
 nst = int(np.sum(~np.isnan(a[np.arange(64) % 128, np.arange(64), 0]))) if False else None
 print("slabs with stamps:", G)
+hv = 1 if os.environ.get("KS_SLAB_PW") == "32" or os.environ.get("KS_SLAB_W") == "16" else 2
 for j in range(64):
-    own = a[j, j] if j < 128 else None
-    if own is None or np.isnan(own[0]):
+    o = j // hv
+    own = a[o, j]
+    if np.isnan(own[0]):
         break
-    la = a[j + 1, j] if j + 1 < 128 else np.full(4, np.nan)
+    la = a[o + 1, j]
     last_upd = np.nanmax(a[:, j, 3])
     print(f"step {j:2d} owner: start {own[0]:8.1f} cols {own[1]-own[0]:6.1f} aug {own[2]-own[1]:6.1f} pub {own[3]-own[2]:6.1f} | "
           f"lookahead: acq +{la[0]-own[3]:5.1f} moves {la[1]-la[0]:5.1f} u12 {la[2]-la[1]:5.1f} upd {la[3]-la[2]:6.1f} | last update done {last_upd - own[3]:6.1f}")
