@@ -662,8 +662,12 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel2(NodeBatch nb, int c0, in
     }
   }
   PANEL_STAMP(1);
-  panel_columns<W, RPT, NT, (W <= 16 ? W : 16)>(a, pos, done, ps, fin, FS, rows, nb.piv + (int64_t)k * nb.t_pad + c0,
-                                                c0, nb.info + k, c0);
+  {
+    const int nact = panel_warps(rows, NT);
+    if ((int)(threadIdx.x >> 5) < nact)
+      panel_columns<W, RPT, NT, (W <= 16 ? W : 16)>(a, pos, done, ps, fin, FS, rows, nb.piv + (int64_t)k * nb.t_pad + c0,
+                                                  c0, nb.info + k, c0, nact);
+  }
   __syncthreads();
   PANEL_STAMP(20);
   // panel rows back to their logical positions (coalesced: W/2 threads per

@@ -52,10 +52,15 @@ __device__ __forceinline__ int warp_winner3(unsigned h, unsigned l, int p) {
 // of physical row r go to fbase[r * fstride + kb + j] (shared memory).
 // piv[kk] = piv_base + logical pivot position; *info = info_base + kk + 1 at
 // the first zero pivot column (SingularMatrixError, linalg.py:205-206).
+// Only the first nact warps (those holding candidate rows) take part; they
+// synchronize on named barrier 1. The caller skips the call on the others and
+// synchronizes the whole CTA afterwards.
+__device__ __forceinline__ int panel_warps(int rows, int nt) { return (min(rows, nt) + 31) / 32; }
+
 template <int W, int RPT, int NT, int CB = 4>
 __device__ __forceinline__ void panel_columns(double (&a)[RPT][W], int (&pos)[RPT], bool (&done)[RPT],
                                               PanelShared<NT / 32, W>& ps, double* fbase, int fstride, int rows,
-                                              int* piv, int piv_base, int* info, int info_base) {
+                                              int* piv, int piv_base, int* info, int info_base, int nact) {
   constexpr int NW = NT / 32;
   constexpr int NONE = 0x7fffffff;
   static_assert(NW <= 32 && W % CB == 0 && W <= 32, "panel shape");
@@ -94,12 +99,12 @@ __device__ __forceinline__ void panel_columns(double (&a)[RPT][W], int (&pos)[RP
         q.hi = bh; q.lo = bl; q.pos = bp; q.pad = 0; q.rcp = rc; q.pad2 = 0.0;
         ps.rec[buf][warp] = q;
       }
-      __syncthreads();
+      asm volatile("bar.sync 1, %0;" ::"r"(nact * 32) : "memory");
       // 3) the CTA's winner (every warp redundantly)
       unsigned qh = 0u, ql = 0u;
       int qp = NONE;
       double qr = 0.0;
-      if (lane < NW) {
+      if (lane < nact) {
         const PivRec& q = ps.rec[buf][lane];
         qh = q.hi; ql = q.lo; qp = q.pos; qr = q.rcp;
       }

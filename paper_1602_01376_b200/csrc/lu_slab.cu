@@ -300,8 +300,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
               for (int q = 0; q < PW; ++q) a[i][q] = (r < rows) ? Sl[(cj + r) * LD + pc + q] : 0.0;
             }
-            panel_columns<PW, RPT, NT, (PW <= 16 ? PW : 16)>(a, pos, done, ps, Sl + (size_t)cj * LD + pc, LD, rows,
-                                                             pivk + cj, cj, nb.info + k, cj);
+            const int nact = panel_warps(rows, NT);
+            if ((int)(threadIdx.x >> 5) < nact)
+              panel_columns<PW, RPT, NT, (PW <= 16 ? PW : 16)>(a, pos, done, ps, Sl + (size_t)cj * LD + pc, LD, rows,
+                                                               pivk + cj, cj, nb.info + k, cj, nact);
           }
           __syncthreads();
           stamp(k, jj, 1);

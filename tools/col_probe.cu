@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(NT, 1) k_real(const double* in, double* out, l
     done[0] = false;
     __syncthreads();
     long long t0 = clock64();
-    panel_columns<W, 1, NT, CB>(a, pos, done, ps, fin, W + 2, NT, piv, 0, info, 0);
+    panel_columns<W, 1, NT, CB>(a, pos, done, ps, fin, W + 2, NT, piv, 0, info, 0, NT / 32);
     __syncthreads();
     tot += clock64() - t0;
   }
