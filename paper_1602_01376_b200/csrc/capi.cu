@@ -969,7 +969,7 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
   cudaStream_t st = L.st;
     ks::launch_coupling(dt, nb, st);
     ks::launch_aug_init(dt, nb, st);
-    L.count[0] += 2;
+    L.count[0] += 3;
     int rc = L.check("coupling/aug_init");
     if (rc) return rc;
     // Z12 = B H_r, Z21 = B^T H_l   (W G, solver.py:142-148, zero blocks skipped)

@@ -299,54 +299,66 @@ void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
 // Padded candidate index i' maps to the reference's cand index
 // (cand = [skel_l; skel_r], compress.py:213): i' < s_pad -> i' (if < s_l),
 // i' >= s_pad -> s_l + (i' - s_pad) (if < s_r).
-__global__ void k_aug_init(DevTree t, NodeBatch nb) {
+__device__ __forceinline__ int cand_index(int i, int S, int sl, int sr) {
+  return (i < S) ? (i < sl ? i : -1) : (i - S < sr ? sl + (i - S) : -1);
+}
+
+// one CTA per row: rows [0, TP) the identity diagonal blocks of Z, rows
+// [TP, T) the zero bottom-right block, then the S rows of the padded P copy
+__global__ void __launch_bounds__(256) k_aug_init(DevTree t, NodeBatch nb) {
   pdl_wait();
-  const int k = blockIdx.y;
-  const int v = nb.node[k], l = nb.left[k], r = nb.right[k];
-  const int sl = t.rank[l], sr = t.rank[r], sv = t.rank[v];
+  const int k = blockIdx.y, row = blockIdx.x;
   const int S = nb.s_pad, TP = nb.t_pad, T = nb.T;
-  const double* P = t.coeff + t.coeff_off[v];
-  const int cand = sl + sr;
   double* A = nb.Aug + (int64_t)k * T * T;
-  double* Pn = nb.Pn + (int64_t)k * S * TP;
-  // (a) identity blocks of Z: rows/cols in the same half
-  const int64_t n_id = 2LL * S * S;
-  // (b) P^T block: TP x S at (0, TP);  (c) zero block S x S at (TP, TP);  (d) Pn: S x TP
-  const int64_t n_pt = (int64_t)TP * S, n_z = (int64_t)S * S, n_pn = (int64_t)S * TP;
-  const int64_t total = n_id + n_pt + n_z + n_pn;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    if (e < n_id) {
-      const int half = (int)(e / ((int64_t)S * S));
-      const int64_t f = e % ((int64_t)S * S);
-      const int i = (int)(f / S), j = (int)(f % S);
-      A[(int64_t)(half * S + i) * T + half * S + j] = (i == j) ? 1.0 : 0.0;
-      continue;
-    }
-    int64_t f = e - n_id;
-    if (f < n_pt) {
-      const int i = (int)(f / S), j = (int)(f % S);  // P^T[i][j] = P[j][i']
-      const int ci = (i < S) ? (i < sl ? i : -1) : (i - S < sr ? sl + (i - S) : -1);
-      A[(int64_t)i * T + TP + j] = (ci >= 0 && j < sv) ? P[(int64_t)j * cand + ci] : 0.0;
-      continue;
-    }
-    f -= n_pt;
-    if (f < n_z) {
-      const int i = (int)(f / S), j = (int)(f % S);
-      A[(int64_t)(TP + i) * T + TP + j] = 0.0;
-      continue;
-    }
-    f -= n_z;
-    {
-      const int j = (int)(f / TP), i = (int)(f % TP);
-      const int ci = (i < S) ? (i < sl ? i : -1) : (i - S < sr ? sl + (i - S) : -1);
-      Pn[f] = (ci >= 0 && j < sv) ? P[(int64_t)j * cand + ci] : 0.0;
-    }
+  if (row < TP) {  // (a) identity block of Z: row i, columns of its half
+    const int half = row / S, i = row - half * S;
+    double* out = A + (int64_t)row * T + half * S;
+    for (int j = threadIdx.x; j < S; j += 256) out[j] = (i == j) ? 1.0 : 0.0;
+    return;
+  }
+  if (row < T) {  // (c) zero block S x S at (TP, TP)
+    double* out = A + (int64_t)row * T + TP;
+    for (int j = threadIdx.x; j < S; j += 256) out[j] = 0.0;
+    return;
+  }
+  // (d) Pn row j: P[j][cand(i)] for the padded candidate index i
+  const int j = row - T;
+  const int v = nb.node[k], sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]], sv = t.rank[v];
+  const double* P = t.coeff + t.coeff_off[v] + (int64_t)j * (sl + sr);
+  double* out = nb.Pn + (int64_t)k * S * TP + (int64_t)j * TP;
+  for (int i = threadIdx.x; i < TP; i += 256) {
+    const int ci = cand_index(i, S, sl, sr);
+    out[i] = (ci >= 0 && j < sv) ? P[ci] : 0.0;
   }
 }
 
+// (b) the P^T block (TP x S at (0, TP)) through 32 x 32 shared-memory tiles:
+// reads along P's rows, writes along Aug's rows
+__global__ void __launch_bounds__(256) k_aug_pt(DevTree t, NodeBatch nb) {
+  pdl_wait();
+  __shared__ double tile[32][33];
+  const int k = blockIdx.z;
+  const int S = nb.s_pad, TP = nb.t_pad, T = nb.T;
+  const int v = nb.node[k], sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]], sv = t.rank[v];
+  const double* P = t.coeff + t.coeff_off[v];
+  const int cand = sl + sr;
+  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  {
+    const int ci = cand_index(i0 + tx, S, sl, sr);
+    for (int jj = ty; jj < 32; jj += 8) {
+      const int j = j0 + jj;
+      tile[jj][tx] = (ci >= 0 && j < sv) ? P[(int64_t)j * cand + ci] : 0.0;
+    }
+  }
+  __syncthreads();
+  double* A = nb.Aug + (int64_t)k * T * T;
+  for (int ii = ty; ii < 32; ii += 8) A[(int64_t)(i0 + ii) * T + TP + j0 + tx] = tile[tx][ii];
+}
+
 void launch_aug_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
-  dim3 g(128, nb.count);
-  launch_pdl(k_aug_init, g, dim3(256), 0, st, t, nb);
+  launch_pdl(k_aug_init, dim3(nb.T + nb.s_pad, nb.count), dim3(256), 0, st, t, nb);
+  launch_pdl(k_aug_pt, dim3(nb.s_pad / 32, nb.t_pad / 32, nb.count), dim3(256), 0, st, t, nb);
 }
 
 // 1-norm of Z (max column abs sum, linalg.py:176), before the LU overwrites it.
@@ -1290,56 +1302,58 @@ void launch_fb_assemble(const DevTree& t, const NodeBatch& fb, const int* begin,
 
 // Composed row interchanges of each node's LU: (Pi v)[i] = v[pm[i]], from the
 // LAPACK-style swap sequence (linalg.py:250-253). One warp per node.
-__global__ void __launch_bounds__(256) k_compose_perm(NodeBatch nb) {
+__global__ void __launch_bounds__(1024) k_compose_perm(NodeBatch nb) {
   pdl_wait();
   const int k = blockIdx.x;
   const int TP = nb.t_pad;
   const int* piv = nb.piv + (int64_t)k * TP;
   int* pm = nb.pm + (int64_t)k * TP;
-  extern __shared__ int ps[];
+  extern __shared__ __align__(16) int ps[];
   for (int i = threadIdx.x; i < TP; i += blockDim.x) ps[i] = piv[i];
   __syncthreads();
-  // every thread follows its rows through the swap sequence: the row that
-  // starts at r ends at f(r), so pm[f(r)] = r (same result as swapping pm)
-  constexpr int U = 8;
-  for (int base = 0; base < TP; base += U * blockDim.x) {
-    int f[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) f[u] = base + threadIdx.x + u * blockDim.x;
-    for (int i = 0; i < TP; ++i) {
-      const int p = ps[i];
-#pragma unroll
-      for (int u = 0; u < U; ++u) f[u] = (f[u] == i) ? p : (f[u] == p ? i : f[u]);
+  // every thread follows one row through the swap sequence: the row that
+  // starts at r ends at f(r), so pm[f(r)] = r (same result as swapping pm);
+  // t_pad is a multiple of 64, the swaps are read four at a time
+  for (int r = threadIdx.x; r < TP; r += blockDim.x) {
+    int f = r;
+    const int4* p4 = reinterpret_cast<const int4*>(ps);
+    for (int i = 0; i < TP / 4; ++i) {
+      const int4 q = p4[i];
+      const int i0 = 4 * i;
+      f = (f == i0) ? q.x : (f == q.x ? i0 : f);
+      f = (f == i0 + 1) ? q.y : (f == q.y ? i0 + 1 : f);
+      f = (f == i0 + 2) ? q.z : (f == q.z ? i0 + 2 : f);
+      f = (f == i0 + 3) ? q.w : (f == q.w ? i0 + 3 : f);
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int r = base + threadIdx.x + u * blockDim.x;
-      if (r < TP) pm[f[u]] = r;
-    }
+    pm[f] = r;
   }
 }
 
 void launch_compose_perm(const NodeBatch& nb, cudaStream_t st) {
-  launch_pdl(k_compose_perm, dim3(nb.count), dim3(256), sizeof(int) * nb.t_pad, st, nb);
+  launch_pdl(k_compose_perm, dim3(nb.count), dim3(std::min(1024, nb.t_pad)), sizeof(int) * nb.t_pad, st, nb);
 }
 
-// H = sym(trailing block) -> Hbuf[node] (solver.py:163).
-__global__ void k_extract_h(NodeBatch nb, double* H, int64_t stride) {
+// H = sym(trailing block) -> Hbuf[node] (solver.py:163): 32 x 32 tiles, the
+// transposed tile through shared memory so both reads run along rows.
+__global__ void __launch_bounds__(256) k_extract_h(NodeBatch nb, double* H, int64_t stride) {
   pdl_wait();
-  const int k = blockIdx.y;
+  __shared__ double tt[32][33];
+  const int k = blockIdx.z;
   const int S = nb.s_pad, T = nb.T, TP = nb.t_pad;
   const double* A = nb.Aug + (int64_t)k * T * T + (int64_t)TP * T + TP;
   double* h = H + (int64_t)nb.node[k] * stride;
-  const int64_t total = (int64_t)S * S;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / S), j = (int)(e % S);
-    h[e] = 0.5 * (A[(int64_t)i * T + j] + A[(int64_t)j * T + i]);
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) tt[r][tx] = A[(int64_t)(j0 + r) * T + i0 + tx];  // A[j][i]
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int i = i0 + r, j = j0 + tx;
+    h[(int64_t)i * S + j] = 0.5 * (A[(int64_t)i * T + j] + tt[tx][r]);
   }
 }
 
 void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st) {
-  dim3 g(32, nb.count);
-  launch_pdl(k_extract_h, g, dim3(256), 0, st, nb, H, h_stride);
+  launch_pdl(k_extract_h, dim3(nb.s_pad / 32, nb.s_pad / 32, nb.count), dim3(256), 0, st, nb, H, h_stride);
 }
 
 }  // namespace ks

@@ -10,4 +10,7 @@ ncu --set full --import-source on --clock-control none --profile-from-start off 
   -o gpurun_out/ncu_top_gemm python tools/profile_step.py --what factor > gpurun_out/ncu_top.log 2>&1
 ncu --set full --import-source on --clock-control none --profile-from-start off \
   -k regex:k_leaf_bwd --launch-count 1 -o gpurun_out/ncu_leafbwd python tools/profile_step.py --what solve > gpurun_out/ncu_bwd.log 2>&1
+ncu --set full --import-source on --clock-control none --profile-from-start off \
+  -k regex:k_lu_slab --launch-skip 2 --launch-count 1 -o gpurun_out/ncu_slab python tools/profile_step.py --what factor > gpurun_out/ncu_slab.log 2>&1
+python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 ls -la gpurun_out
