@@ -115,6 +115,10 @@ struct ks_factor {
   int64_t shard_root = 0;
   int shard_level = 0;
   int n_local_levels = 0;
+  // subtree pipelining: the deepest npipe levels split into kLeafChunks
+  // subtrees, each factored on its own stream right after its own leaves
+  // (children of a subtree's nodes lie in the same subtree one level down)
+  int npipe = 0;
   int64_t loc_begin = 0, loc_end = 0;   // tree-order rows owned by the shard
   std::vector<int64_t> peers;           // nodes at the shard level (all shards' roots)
   bool local_factored = false;
@@ -141,7 +145,7 @@ struct ks_factor {
   cudaStream_t side = nullptr, cap = nullptr;
   // independent node groups run on their own streams so latency-bound kernels
   // (POTRF, LU panels, TRSM) of one group overlap the GEMMs of another
-  static constexpr int kGroups = 2;
+  static constexpr int kGroups = 4;  // stream slots; KS_GROUPS picks how many are used (default 4)
   cudaStream_t gst[kGroups] = {};
   cudaEvent_t gfork = nullptr, gjoin[kGroups] = {};
   cudaEvent_t ev_phase[5] = {};
@@ -159,7 +163,7 @@ struct ks_factor {
   // uploads started by ks_create, consumed by the first factorization
   static constexpr int kLeafChunks = 4;
   cudaStream_t upl = nullptr;
-  cudaEvent_t ev_up_coords = nullptr, ev_up_all = nullptr, ev_up_leaf[kLeafChunks] = {};
+  cudaEvent_t ev_up_coords = nullptr, ev_up_all = nullptr, ev_up_leaf[kLeafChunks] = {}, ev_up_sub[kLeafChunks] = {};
   std::vector<cudaEvent_t> ev_up_level;
   bool upload_pending = false;
   // diagnostics
@@ -568,6 +572,26 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     for (int v : lv) f->int_nodes.push_back(v);
   }
   f->n_int = (int)f->int_nodes.size();
+  {  // subtree pipelining plan
+    const int G = ks_factor::kLeafChunks;
+    const size_t nlv = f->leaf_nodes.size();
+    std::vector<int> grp(nn, -1);
+    if (nlv % G == 0 && nlv >= (size_t)G)
+      for (size_t li = 0; li < nlv; ++li) grp[f->leaf_nodes[li]] = (int)(li / (nlv / G));
+    for (int lev = 0; lev < f->n_local_levels && nlv % G == 0; ++lev) {
+      const auto& lv = f->levels[lev];
+      const int c = (int)lv.size();
+      if (c % G || c / G < 16) break;
+      bool ok = true;
+      for (int i = 0; i < c; ++i) {
+        const int g = i / (c / G), v = lv[i];
+        if (grp[f->left[v]] != g || grp[f->right[v]] != g) ok = false;
+      }
+      if (!ok) break;
+      for (int i = 0; i < c; ++i) grp[lv[i]] = i / (c / G);
+      f->npipe = lev + 1;
+    }
+  }
   f->m_pad = (int)roundup(m_max, 64);
   f->s_pad = (int)roundup(s_max, 64);
   f->t_pad = 2 * f->s_pad;
@@ -676,6 +700,7 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_up_coords, cudaEventDisableTiming));
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_up_all, cudaEventDisableTiming));
     for (auto& e : f->ev_up_leaf) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : f->ev_up_sub) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     f->ev_up_level.resize(f->levels.size());
     for (auto& e : f->ev_up_level) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     cudaStream_t u = f->upl;
@@ -733,10 +758,20 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
         if (int rc = add(f->leaf_nodes[li])) return rc;
       if (int rc = flush()) return rc;
       KS_CUDA(cudaEventRecord(f->ev_up_leaf[c], u));
+      // with subtree pipelining: then this subtree's nodes of the pipelined levels
+      for (int lev = 0; lev < f->npipe; ++lev) {
+        const auto& lv = f->levels[lev];
+        const size_t c0 = lv.size() * c / ks_factor::kLeafChunks, c1 = lv.size() * (c + 1) / ks_factor::kLeafChunks;
+        for (size_t i = c0; i < c1; ++i)
+          if (int rc = add(lv[i])) return rc;
+      }
+      if (int rc = flush()) return rc;
+      KS_CUDA(cudaEventRecord(f->ev_up_sub[c], u));
     }
     for (size_t lev = 0; lev < f->levels.size(); ++lev) {
       for (int v : f->levels[lev])
-        if (int rc = add(v)) return rc;
+        if (!sent[v])
+          if (int rc = add(v)) return rc;
       if (int rc = flush()) return rc;
       KS_CUDA(cudaEventRecord(f->ev_up_level[lev], u));
     }
@@ -885,14 +920,24 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
   return KS_OK;
 }
 
-static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1);
+static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1, int deferred_before = 0);
+static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool is_root_level);
+static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt, int T, int S, int TP);
+// subtree pipelining (ks_factor::npipe) in this factorization: the default 4
+// node groups, not under the per-level profiler or the tracer (their level
+// boundaries would blur); KS_PIPE=0 disables it
+static bool pipelined(const ks_factor* f, int G) {
+  const char* e = std::getenv("KS_PIPE");
+  if (e && e[0] == '0') return false;
+  return f->npipe > 0 && G == ks_factor::kLeafChunks && !f->profiling && !trace_on();
+}
 
 // node groups per phase (KS_GROUPS, default 2; tracing forces 1 so per-launch
 // events stay on one stream)
 static int n_groups() {
   if (trace_on()) return 1;
   const char* e = std::getenv("KS_GROUPS");
-  const int g = e ? std::atoi(e) : ks_factor::kGroups;
+  const int g = e ? std::atoi(e) : 4;
   return std::max(1, std::min(g, ks_factor::kGroups));
 }
 
@@ -916,9 +961,11 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   // group waits only for the uploads of its own P blocks
   if (f->upload_pending) KS_CUDA(cudaStreamWaitEvent(st, f->ev_up_coords, 0));
   if (int rc = L.check("start")) return rc;
+  bool pipe = false;
   if (int rc = mark(f->ev_phase[1])) return rc;
   {
     const int G = (nl >= 2 * 64) ? n_groups() : 1;
+    pipe = pipelined(f, G);
     if (G > 1) {
       KS_CUDA(cudaEventRecord(f->gfork, st));
       for (int g = 0; g < G; ++g) KS_CUDA(cudaStreamWaitEvent(f->gst[g], f->gfork, 0));
@@ -934,6 +981,16 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
       Launcher Lg{f, gs, &f->launches[0]};
       if (int rc = enqueue_leaf_assemble(f, Lg, l0, l1)) return rc;
       if (int rc = enqueue_leaf_chol(f, Lg, l0, l1)) return rc;
+      if (pipe) {  // this subtree's nodes of the deepest npipe levels, on the same stream
+        if (f->upload_pending) KS_CUDA(cudaStreamWaitEvent(gs, f->ev_up_sub[g], 0));
+        for (int lev = 0; lev < f->npipe; ++lev) {
+          f->cur_tag = lev;
+          const ks::NodeBatch nb = f->nodebatch(lev);
+          const int c = nb.count / G;
+          if (int rc = enqueue_level_body(f, Lg, sub_batch(nb, g * c, c, f->T, f->s_pad, f->t_pad), false)) return rc;
+        }
+        f->cur_tag = -1;
+      }
     }
     if (G > 1)
       for (int g = 0; g < G; ++g) {
@@ -944,8 +1001,9 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   KS_CUDA(cudaGetLastError());
   if (int rc = mark(f->ev_phase[2])) return rc;
   if (int rc = mark(f->ev_phase[3])) return rc;
-  // ---- the shard's internal levels, deepest first ----
-  if (int rc = enqueue_levels(f, st, L, 0, f->n_local_levels)) return rc;
+  // ---- the shard's internal levels, deepest first (the pipelined ones are
+  // done; their condition estimates are still to be launched) ----
+  if (int rc = enqueue_levels(f, st, L, pipe ? f->npipe : 0, f->n_local_levels, pipe ? f->npipe : 0)) return rc;
   if (int rc = mark(f->ev_phase[4])) return rc;
   return KS_OK;
 }
@@ -1063,13 +1121,14 @@ static bool hager_split() {
 // stream (they only feed diagnostics), joined at the end. The estimates of the
 // wide (HBM-heavy) levels wait for the first narrow level, whose latency-bound
 // launches leave most SMs idle, instead of competing with the next wide level.
-static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1) {
+static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1, int deferred_before) {
   const ks::DevTree dt = f->devtree();
   auto mark = [&](cudaEvent_t e) -> int {
     if (f->profiling) KS_CUDA(cudaEventRecord(e, st));
     return KS_OK;
   };
   std::vector<int> deferred;  // levels whose estimate is not launched yet
+  for (int lv = 0; lv < deferred_before; ++lv) deferred.push_back(lv);
   bool used_side = false, used_side2 = false;
   auto flush = [&]() -> int {
     if (deferred.empty()) return KS_OK;
@@ -2323,6 +2382,8 @@ void ks_destroy(ks_factor* f) {
   if (f->ev_up_coords) cudaEventDestroy(f->ev_up_coords);
   if (f->ev_up_all) cudaEventDestroy(f->ev_up_all);
   for (auto e : f->ev_up_leaf)
+    if (e) cudaEventDestroy(e);
+  for (auto e : f->ev_up_sub)
     if (e) cudaEventDestroy(e);
   for (auto e : f->ev_up_level)
     if (e) cudaEventDestroy(e);
