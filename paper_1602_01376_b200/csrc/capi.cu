@@ -145,7 +145,7 @@ struct ks_factor {
   cudaStream_t side = nullptr, cap = nullptr;
   // independent node groups run on their own streams so latency-bound kernels
   // (POTRF, LU panels, TRSM) of one group overlap the GEMMs of another
-  static constexpr int kGroups = 4;  // stream slots; KS_GROUPS picks how many are used (default 4)
+  static constexpr int kGroups = 8;  // stream slots; KS_GROUPS picks how many are used (default 8)
   cudaStream_t gst[kGroups] = {};
   cudaEvent_t gfork = nullptr, gjoin[kGroups] = {};
   cudaEvent_t ev_phase[5] = {};
@@ -161,7 +161,7 @@ struct ks_factor {
   cudaStream_t side2 = nullptr;
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   // uploads started by ks_create, consumed by the first factorization
-  static constexpr int kLeafChunks = 4;
+  static constexpr int kLeafChunks = 8;
   cudaStream_t upl = nullptr;
   cudaEvent_t ev_up_coords = nullptr, ev_up_all = nullptr, ev_up_leaf[kLeafChunks] = {}, ev_up_sub[kLeafChunks] = {};
   std::vector<cudaEvent_t> ev_up_level;
@@ -822,7 +822,9 @@ int ks_create_shard(const ks_problem* p, int device, int64_t shard_root, ks_fact
 // inverse), then H = L21 L21^T (solver.py:123-135).
 // Leaves [l0, l1): K(X_leaf, X_leaf) + lam I (lower triangle) and the P rows of
 // the trapezoid [[A], [P]].
-static int enqueue_leaf_assemble(ks_factor* f, Launcher& L, int l0, int l1) {
+// wait_p: on the first factorization, the upload milestone of these leaves' P
+// blocks (the Gaussian blocks need only the points, so they start before it)
+static int enqueue_leaf_assemble(ks_factor* f, Launcher& L, int l0, int l1, cudaEvent_t wait_p = nullptr) {
   if (l1 <= l0) return KS_OK;
   const ks::DevTree dt = f->devtree();
   const ks::LeafBatch all = f->leafbatch();
@@ -841,8 +843,10 @@ static int enqueue_leaf_assemble(ks_factor* f, Launcher& L, int l0, int l1) {
     ++L.count[0];
     cudaError_t e = ks::gemm_gauss(g, L.st);
     if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf gauss gemm: %s", cudaGetErrorString(e));
+    if (wait_p) KS_CUDA(cudaStreamWaitEvent(L.st, wait_p, 0));
     ks::launch_leaf_copy_p(dt, lb, L.st);
   } else {
+    if (wait_p) KS_CUDA(cudaStreamWaitEvent(L.st, wait_p, 0));
     ks::launch_leaf_assemble(dt, lb, f->lam_dev.p, L.st);
   }
   L.count[0] += 1;
@@ -937,7 +941,7 @@ static bool pipelined(const ks_factor* f, int G) {
 static int n_groups() {
   if (trace_on()) return 1;
   const char* e = std::getenv("KS_GROUPS");
-  const int g = e ? std::atoi(e) : 4;
+  const int g = e ? std::atoi(e) : 8;
   return std::max(1, std::min(g, ks_factor::kGroups));
 }
 
@@ -973,13 +977,14 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
     for (int g = 0; g < G; ++g) {
       const int l0 = (int)((int64_t)nl * g / G), l1 = (int)((int64_t)nl * (g + 1) / G);
       cudaStream_t gs = (G > 1) ? f->gst[g] : st;
+      cudaEvent_t wait_p = nullptr;
       if (f->upload_pending && l1 > l0) {
         int c = 0;  // the upload chunk holding this group's last leaf
         while ((int64_t)nl * (c + 1) / ks_factor::kLeafChunks <= l1 - 1) ++c;
-        KS_CUDA(cudaStreamWaitEvent(gs, f->ev_up_leaf[c], 0));
+        wait_p = f->ev_up_leaf[c];
       }
       Launcher Lg{f, gs, &f->launches[0]};
-      if (int rc = enqueue_leaf_assemble(f, Lg, l0, l1)) return rc;
+      if (int rc = enqueue_leaf_assemble(f, Lg, l0, l1, wait_p)) return rc;
       if (int rc = enqueue_leaf_chol(f, Lg, l0, l1)) return rc;
       if (pipe) {  // this subtree's nodes of the deepest npipe levels, on the same stream
         if (f->upload_pending) KS_CUDA(cudaStreamWaitEvent(gs, f->ev_up_sub[g], 0));
