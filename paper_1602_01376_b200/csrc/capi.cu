@@ -1115,6 +1115,13 @@ static int hager_ctas() {
   return e ? std::max(1, std::atoi(e)) : 96;
 }
 
+// KS_HAGER_FLUSH=n: launch the deferred wide-level estimates at the first
+// level with <= n nodes (default 0: the first narrow level)
+static int hager_flush_nodes() {
+  const char* e = std::getenv("KS_HAGER_FLUSH");
+  return e ? std::atoi(e) : 0;
+}
+
 // KS_HAGER_SPLIT=0: narrow levels' estimates queue on `side` like the wide ones
 static bool hager_split() {
   const char* e = std::getenv("KS_HAGER_SPLIT");
@@ -1164,7 +1171,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
     const ks::NodeBatch nb = f->nodebatch((int)lev);
     const bool is_root_level = (f->levels[lev][0] == 0);
     const bool wide = nb.count >= 64;
-    if (!wide)
+    if (!wide || nb.count <= hager_flush_nodes())
       if (int rc = flush()) return rc;
     const int G = wide ? n_groups() : 1;
     if (G == 1) {
