@@ -133,6 +133,7 @@ struct ks_factor {
   DBuf<double> lu_scratch;
   DBuf<unsigned> lu_sync;  // persistent-LU flags: 4 words per internal node + the watchdog word
   DBuf<double> dinv;  // condition estimator: diagonal-block inverses of every node's Z factors
+  DBuf<double> lut;   // condition estimator: column-major copies of every node's Z factors (t_pad <= 512)
   DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
   // solve scratch
   DBuf<double> z, c, tin, y, wtmp, bdev, xdev;
@@ -263,7 +264,7 @@ struct ks_factor {
   void release_all() {
     coords.release(); xx.release(); rank_d.release(); skel_pos.release(); skel_off.release(); coeff_off.release();
     coeff.release(); leaf_node.release(); leaf_begin.release(); leaf_size.release(); leaf_info.release();
-    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release(); lu_scratch.release(); lu_sync.release(); dinv.release();
+    int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release(); pm.release(); lu_scratch.release(); lu_sync.release(); dinv.release(); lut.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
     norm1.release(); cond.release(); z.release(); c.release(); tin.release(); y.release();
     fb_aug.release(); fb_y.release(); fb_norm1.release(); fb_cond.release(); fb_piv.release(); fb_info.release();
@@ -663,6 +664,7 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     KS_CUDA(f->pm.alloc((size_t)std::max(f->n_int, 1) * f->t_pad + 1));
     KS_CUDA(f->lu_scratch.alloc((size_t)std::max(f->n_int, 1) * 32 * 64));
     KS_CUDA(f->dinv.alloc((size_t)std::max(f->n_int, 1) * 2 * f->t_pad * 16));
+    if (f->t_pad <= 512) KS_CUDA(f->lut.alloc((size_t)std::max(f->n_int, 1) * f->t_pad * f->t_pad));
     KS_CUDA(f->leafA.alloc(nl * (size_t)f->R * f->m_pad));
     KS_CUDA(f->inv.alloc(nl * (size_t)f->m_pad * 64));
     KS_CUDA(f->hbuf.alloc((size_t)nn * f->s_pad * f->s_pad + 1));
@@ -1147,7 +1149,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
     if (trace_on()) {  // inline, so the trace times each estimate
       for (int lv : deferred) {
         f->cur_tag = lv;
-        ks::launch_hager(dt, f->nodebatch(lv), f->dinv.p, 1 << 30, st);
+        ks::launch_hager(dt, f->nodebatch(lv), f->dinv.p, f->lut.p, 1 << 30, st);
         L.count[0] += ks::hager_launches(f->nodebatch(lv));
         if (int rc = L.check("hager")) return rc;
       }
@@ -1158,7 +1160,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
     KS_CUDA(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
     used_side = true;
     for (int lv : deferred) {
-      ks::launch_hager(dt, f->nodebatch(lv), f->dinv.p, hager_ctas(), f->side);
+      ks::launch_hager(dt, f->nodebatch(lv), f->dinv.p, f->lut.p, hager_ctas(), f->side);
       L.count[0] += ks::hager_launches(f->nodebatch(lv));
     }
     deferred.clear();
@@ -1194,7 +1196,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
       KS_CUDA(cudaEventRecord(f->ev_fork2, st));
       KS_CUDA(cudaStreamWaitEvent(f->side2, f->ev_fork2, 0));
       used_side2 = true;
-      ks::launch_hager(dt, nb, f->dinv.p, nb.count, f->side2);
+      ks::launch_hager(dt, nb, f->dinv.p, f->lut.p, nb.count, f->side2);
       L.count[0] += ks::hager_launches(nb);
       KS_CUDA(cudaGetLastError());
     } else {

@@ -1053,11 +1053,15 @@ __global__ void __launch_bounds__(256) k_diag_inv(NodeBatch nb, double* dinv) {
 // v (thread i's entry) <- M^-1 v for M = L (unit lower), U, U^T or L^T of the
 // packed factors in A (rows of length lda); di: the matching diagonal-block
 // inverses in shared memory; xs: a shared broadcast buffer (n entries).
-template <int SB, int NT, int MODE>
+// COLMAJ: A is the column-major copy of the factors (At[j][i] = A[i][j]), so
+// the non-transposed solves read it down columns like the transposed ones
+// (coalesced across the threads that own consecutive entries)
+template <int SB, int NT, int MODE, bool COLMAJ = false>
 __device__ __forceinline__ double own_solve(const double* __restrict__ A, int64_t lda, int n, const double* di, double v,
                             double* xs) {
   constexpr bool ASC = (MODE == SOLVE_L || MODE == SOLVE_UT);
   constexpr bool TRANS = (MODE == SOLVE_UT || MODE == SOLVE_LT);
+  constexpr bool COLACC = TRANS || COLMAJ;
   const int i = threadIdx.x, lane = i & 31;
   const bool own = i < n;
   const int nblk = n / SB;
@@ -1065,7 +1069,7 @@ __device__ __forceinline__ double own_solve(const double* __restrict__ A, int64_
   auto load = [&](int b, double (&c)[SB]) {
     const int r0 = b * SB;
     const bool need = own && (ASC ? i >= r0 + SB : i < r0);  // solved after block b
-    if (TRANS) {
+    if (COLACC) {
       const double* p = A + (int64_t)r0 * lda + (own ? i : 0);
 #pragma unroll
       for (int j = 0; j < SB; ++j, p += lda) c[j] = need ? __ldg(p) : 0.0;
@@ -1156,8 +1160,8 @@ __device__ __forceinline__ void nt_argmax(double& bv, int& bi, double* red, int*
     if (red[w] > bv || (red[w] == bv && redi[w] < bi)) { bv = red[w]; bi = redi[w]; }
 }
 
-template <int SB, int NT>
-__global__ void __launch_bounds__(NT, 1) k_hager_own(DevTree t, NodeBatch nb, const double* dinv) {
+template <int SB, int NT, bool COLMAJ>
+__global__ void __launch_bounds__(NT, 1) k_hager_own(DevTree t, NodeBatch nb, const double* dinv, const double* lut) {
   extern __shared__ __align__(16) double hs[];
   // persistent over nodes: the grid may be smaller than the batch so that the
   // estimate leaves SMs free for the factorization it overlaps
@@ -1195,8 +1199,14 @@ __global__ void __launch_bounds__(NT, 1) k_hager_own(DevTree t, NodeBatch nb, co
     if (own) xs[i] = x;
     __syncthreads();
     double y = own ? xs[pm[i]] : 0.0;
-    y = own_solve<SB, NT, SOLVE_L>(A, T, TP, dL, y, xs);
-    y = own_solve<SB, NT, SOLVE_U>(A, T, TP, dU, y, xs);
+    if constexpr (COLMAJ) {
+      const double* At = lut + (int64_t)(nb.first + k) * TP * TP;
+      y = own_solve<SB, NT, SOLVE_L, true>(At, TP, TP, dL, y, xs);
+      y = own_solve<SB, NT, SOLVE_U, true>(At, TP, TP, dU, y, xs);
+    } else {
+      y = own_solve<SB, NT, SOLVE_L>(A, T, TP, dL, y, xs);
+      y = own_solve<SB, NT, SOLVE_U>(A, T, TP, dU, y, xs);
+    }
     est = nt_sum<NT>(real ? fabs(y) : 0.0, red);
     // z = Z^-T sign(y)   (solve_transposed: U^T, unit L^T, undo swaps)
     double w = real ? (y >= 0.0 ? 1.0 : -1.0) : 0.0;
@@ -1219,29 +1229,49 @@ __global__ void __launch_bounds__(NT, 1) k_hager_own(DevTree t, NodeBatch nb, co
   }
 }
 
-template <int SB, int NT>
-static void launch_hager_own(const DevTree& t, const NodeBatch& nb, double* dinv, int max_ctas, cudaStream_t st) {
+// column-major copy of each node's Z factors (L\U, t_pad x t_pad) for the
+// estimator's non-transposed solves: lut[first + k] = Z_k^T
+__global__ void __launch_bounds__(256) k_lu_transpose(NodeBatch nb, double* lut) {
+  __shared__ double tt[32][33];
+  const int k = blockIdx.z, TP = nb.t_pad, T = nb.T;
+  const double* A = nb.Aug + (int64_t)k * T * T;
+  double* At = lut + (int64_t)(nb.first + k) * TP * TP;
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) tt[r][tx] = A[(int64_t)(i0 + r) * T + j0 + tx];
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) At[(int64_t)(j0 + r) * TP + i0 + tx] = tt[tx][r];
+}
+
+template <int SB, int NT, bool COLMAJ>
+static void launch_hager_own(const DevTree& t, const NodeBatch& nb, double* dinv, double* lut, int max_ctas,
+                             cudaStream_t st) {
   dim3 g(nb.count, 2);
   k_diag_inv<SB><<<g, 256, 0, st>>>(nb, dinv);
+  if (COLMAJ) k_lu_transpose<<<dim3(nb.t_pad / 32, nb.t_pad / 32, nb.count), 256, 0, st>>>(nb, lut);
   const size_t smem = sizeof(double) * (2 * (size_t)nb.t_pad * SB + nb.t_pad + 2 * NT / 32) + sizeof(int) * nb.t_pad;
   static size_t set = 0;
   if (smem > set) {
-    cudaFuncSetAttribute(k_hager_own<SB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_hager_own<SB, NT, COLMAJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set = smem;
   }
-  k_hager_own<SB, NT><<<std::min(nb.count, max_ctas), NT, smem, st>>>(t, nb, dinv);
+  k_hager_own<SB, NT, COLMAJ><<<std::min(nb.count, max_ctas), NT, smem, st>>>(t, nb, dinv, lut);
 }
 
-int hager_launches(const NodeBatch& nb) { return nb.t_pad <= 1024 ? 2 : 1; }
+int hager_launches(const NodeBatch& nb) { return (nb.t_pad <= 512 && nb.count < 64) ? 3 : (nb.t_pad <= 1024 ? 2 : 1); }
 
-void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, int max_ctas, cudaStream_t st) {
+void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, double* lut, int max_ctas, cudaStream_t st) {
   const char* e = std::getenv("KS_HAGER_IMPL");
   if (e && e[0] == 'b') {
     launch_hager_blocked(t, nb, st);
     return;
   }
-  if (nb.t_pad <= 512) launch_hager_own<8, 512>(t, nb, dinv, max_ctas, st);
-  else if (nb.t_pad <= 1024) launch_hager_own<8, 1024>(t, nb, dinv, max_ctas, st);
+  if (nb.t_pad <= 512) {
+    // the column-major copy pays for itself where the factors are still in L2
+    // (narrow levels); for wide levels the extra HBM pass costs more than it saves
+    if (lut && nb.count < 64) launch_hager_own<8, 512, true>(t, nb, dinv, lut, max_ctas, st);
+    else launch_hager_own<8, 512, false>(t, nb, dinv, lut, max_ctas, st);
+  } else if (nb.t_pad <= 1024) launch_hager_own<8, 1024, false>(t, nb, dinv, nullptr, max_ctas, st);
   else launch_hager_blocked(t, nb, st);
 }
 

@@ -67,7 +67,9 @@ void launch_lu_swap(const NodeBatch& nb, int c0, int w, cudaStream_t st);
 void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncols, cudaStream_t st);
 // dinv: scratch for the diagonal-block inverses, 2 x t_pad x 16 doubles per internal node
 // max_ctas bounds the estimator's grid (it loops over the batch's nodes)
-void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, int max_ctas, cudaStream_t st);
+// lut (may be null): t_pad x t_pad per internal node, the column-major copy of
+// Z's factors the estimator's non-transposed solves read (t_pad <= 512)
+void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, double* lut, int max_ctas, cudaStream_t st);
 int hager_launches(const NodeBatch& nb);
 void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st);
 void launch_compose_perm(const NodeBatch& nb, cudaStream_t st);
