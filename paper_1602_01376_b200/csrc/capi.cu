@@ -367,32 +367,43 @@ bool fused_merge_off() {
 }
 
 // Recursive LU of columns [c0, c0+w) over rows [c0, T), pivots among rows < t_pad.
-int rlu(Launcher& L, const ks::NodeBatch& nb, int c0, int w, int pw, int* pend) {
+// ext > 0: the ext columns right after [c0, c0+w) (the P^T block, on the right
+// spine of the recursion) take part in every merge as part of the right block,
+// so U12 = L^-1 Pi P^T and the Schur block H come out of the merges' TRSMs and
+// GEMMs instead of a separate TRSM chain and Schur GEMM after the LU.
+int rlu(Launcher& L, const ks::NodeBatch& nb, int c0, int w, int pw, int* pend, int ext = 0) {
+  const int64_t TT = (int64_t)nb.T * nb.T;
   if (w <= pw) {
     ks::launch_lu_panel(nb, c0, w, L.st, pend);  // panel LU + its row interchanges everywhere else
     pend[2] = 0;                                   // the pending U12 block (if any) is in place now
     *L.count += 1;
-    return L.check("lu_panel");
+    if (int rc = L.check("lu_panel")) return rc;
+    if (ext <= 0) return KS_OK;
+    int rc = trsm_ul(L, nb, c0, w, c0 + w, ext);
+    if (rc) return rc;
+    Operand A{nb.Aug + (int64_t)(c0 + w) * nb.T + c0, nb.T, TT, nullptr};
+    Operand B{nb.Aug + (int64_t)c0 * nb.T + c0 + w, nb.T, TT, nullptr};
+    OperandW C{nb.Aug + (int64_t)(c0 + w) * nb.T + c0 + w, nb.T, TT, nullptr};
+    return L.gemm(mk(nb.T - c0 - w, ext, w, nb.count, A, B, C, -1.0, 1.0), false, false, "rlu_gemm");
   }
   const int h = (int)roundup(w / 2, pw);
   int rc = rlu(L, nb, c0, h, pw, pend);
   if (rc) return rc;
-  if ((h == 16 || h == 32) && w - h <= 64 && !fused_merge_off() && nb.scratch) {
+  if ((h == 16 || h == 32) && w - h <= 64 && ext == 0 && !fused_merge_off() && nb.scratch) {
     ks::launch_lu_merge(nb, c0, h, w, L.st);  // TRSM + trailing GEMM in one launch
     ++*L.count;
     if ((rc = L.check("lu_merge"))) return rc;
     pend[0] = c0; pend[1] = c0 + h; pend[2] = h; pend[3] = w - h;  // U12 -> next panel kernel
     return rlu(L, nb, c0 + h, w - h, pw, pend);
   }
-  rc = trsm_ul(L, nb, c0, h, c0 + h, w - h);
+  rc = trsm_ul(L, nb, c0, h, c0 + h, w - h + ext);
   if (rc) return rc;
-  const int64_t TT = (int64_t)nb.T * nb.T;
   Operand A{nb.Aug + (int64_t)(c0 + h) * nb.T + c0, nb.T, TT, nullptr};
   Operand B{nb.Aug + (int64_t)c0 * nb.T + c0 + h, nb.T, TT, nullptr};
   OperandW C{nb.Aug + (int64_t)(c0 + h) * nb.T + c0 + h, nb.T, TT, nullptr};
-  rc = L.gemm(mk(nb.T - c0 - h, w - h, h, nb.count, A, B, C, -1.0, 1.0), false, false, "rlu_gemm");
+  rc = L.gemm(mk(nb.T - c0 - h, w - h + ext, h, nb.count, A, B, C, -1.0, 1.0), false, false, "rlu_gemm");
   if (rc) return rc;
-  return rlu(L, nb, c0 + h, w - h, pw, pend);
+  return rlu(L, nb, c0 + h, w - h, pw, pend, ext);
 }
 
 struct PhaseTimer {
@@ -1023,6 +1034,13 @@ static bool use_slab(const ks_factor* f, const ks::NodeBatch& nb) {
   return nb.count <= mx && f->lu_sync.p && ks::slab_width(nb) > 0;
 }
 
+// batches of at most KS_SPINE_MAX (default 16) nodes carry the P^T columns
+// through the recursive LU (rlu ext)
+static int spine_max() {
+  const char* e = std::getenv("KS_SPINE_MAX");
+  return e ? std::atoi(e) : 16;
+}
+
 // One level's node work on L's stream for the node sub-batch nb (coupling,
 // augmented assembly, recursive LU, U12 / Schur, pivot composition, H out).
 static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool is_root_level) {
@@ -1071,15 +1089,21 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
     if (int rc2 = L.check("colnorm1")) return rc2;
     // LU of the Z columns with pivots restricted to Z's rows
     int pend[4] = {0, 0, 0, 0};
-    rc = rlu(L, nb, 0, TP, f->pw, pend);
+    // ... with the P^T columns on the right spine of the recursion: U12 =
+    // L^-1 Pi P^T and the Schur complement H = P G Z^-1 P^T come out of it
+    // (small batches: fewer dependent launches; large batches keep the separate
+    // U12 TRSM and Schur GEMM, which run at a higher tensor-pipe rate)
+    const bool spine = nb.count <= spine_max();
+    rc = rlu(L, nb, 0, TP, f->pw, pend, spine ? S : 0);
     if (rc) return rc;
-    // U12 = L^-1 Pi P^T and the Schur complement H = P G Z^-1 P^T
-    rc = trsm_ul(L, nb, 0, TP, TP, S);
-    if (rc) return rc;
-    rc = L.gemm(mk(S, S, TP, cnt, Operand{nb.Aug + (int64_t)TP * T, T, TT, nullptr},
-                   Operand{nb.Aug + TP, T, TT, nullptr}, OperandW{nb.Aug + (int64_t)TP * T + TP, T, TT, nullptr},
-                   -1.0, 1.0), false, false);
-    if (rc) return rc;
+    if (!spine) {
+      rc = trsm_ul(L, nb, 0, TP, TP, S);
+      if (rc) return rc;
+      rc = L.gemm(mk(S, S, TP, cnt, Operand{nb.Aug + (int64_t)TP * T, T, TT, nullptr},
+                     Operand{nb.Aug + TP, T, TT, nullptr}, OperandW{nb.Aug + (int64_t)TP * T + TP, T, TT, nullptr},
+                     -1.0, 1.0), false, false);
+      if (rc) return rc;
+    }
     ks::launch_compose_perm(nb, st);
     ++L.count[0];
     if (!is_root_level) {
@@ -1285,16 +1309,9 @@ static int factor_fallback_leaves(ks_factor* f, cudaStream_t st) {
   KS_CUDA(cudaMemsetAsync(f->fb_info.p, 0, sizeof(int) * nf, st));
   ks::launch_fb_assemble(f->devtree(), fb, f->fb_begin.p, f->fb_size.p, f->lam_dev.p, st);
   int pend[4] = {0, 0, 0, 0};
-  int rc = rlu(L, fb, 0, M, T <= 1024 ? 16 : 8, pend);
+  int rc = rlu(L, fb, 0, M, T <= 1024 ? 16 : 8, pend, S);  // the -P^T columns on the spine: H comes out of it
   if (rc) return rc;
-  if (S > 0) {
-    if ((rc = trsm_ul(L, fb, 0, M, M, S))) return rc;
-    const int64_t TT = (int64_t)T * T;
-    rc = L.gemm(mk(S, S, M, nf, Operand{fb.Aug + (int64_t)M * T, T, TT, nullptr}, Operand{fb.Aug + M, T, TT, nullptr},
-                   OperandW{fb.Aug + (int64_t)M * T + M, T, TT, nullptr}, -1.0, 1.0), false, false);
-    if (rc) return rc;
-    ks::launch_extract_h(fb, f->hbuf.p, (int64_t)f->s_pad * f->s_pad, st);
-  }
+  if (S > 0) ks::launch_extract_h(fb, f->hbuf.p, (int64_t)f->s_pad * f->s_pad, st);
   ks::launch_compose_perm(fb, st);
   KS_CUDA(cudaGetLastError());
   std::vector<int> info(nf, 0);
