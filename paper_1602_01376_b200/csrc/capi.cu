@@ -894,9 +894,15 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
       Operand A{leafA + (int64_t)j0 * M, M, AS, nullptr};
       Operand B{leafA + (int64_t)j0 * M, M, AS, nullptr};
       OperandW C{leafA + (int64_t)j0 * M + j0, M, AS, nullptr};
-      int rc = L.gemm(mk(fused ? 64 : R - j0, 64, j0, nl, A, B, C, -1.0, 1.0), false, true,
-                      fused ? "leaf_update_diag" : "leaf_update");
-      if (rc) return rc;
+      if (fused) {
+        ++L.count[0];
+        cudaError_t e = ks::gemm_small_tile(mk(64, 64, j0, nl, A, B, C, -1.0, 1.0), st);
+        if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf diagonal update: %s", cudaGetErrorString(e));
+        if (int rc = L.check("leaf_update_diag")) return rc;
+      } else {
+        int rc = L.gemm(mk(R - j0, 64, j0, nl, A, B, C, -1.0, 1.0), false, true, "leaf_update");
+        if (rc) return rc;
+      }
     }
     ks::launch_potrf64(lb, j0, inv, info, st);
     ++L.count[0];

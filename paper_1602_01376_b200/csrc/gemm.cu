@@ -69,6 +69,15 @@ cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st) {
   return launch<64, 64, 2, 4, false, true, 2, 1>(t, st);
 }
 
+cudaError_t gemm_small_tile(const GemmArgs& g, cudaStream_t st) {
+  // one 64 x 64 output per batch entry with a long K (leaf diagonal-block
+  // updates): 8 warps per tile so one tile keeps the tensor pipe busier
+  if (g.M != 64 || g.N != 64 || (g.K & 1) || g.K <= 0 || ((g.A.ld | g.B.ld | g.C.ld) & 1)) return gemm(g, false, true, st);
+  const char* e = std::getenv("KS_DIAG_TILE");
+  if (e && e[0] == '0') return gemm(g, false, true, st);
+  return launch<64, 64, 2, 4, false, true, 4>(g, st);
+}
+
 cudaError_t gemm_update_trsm(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.batch <= 0) return cudaSuccess;
   if (g.N != 64 || (g.K & 1) || g.K <= 0 || ((g.A.ld | g.B.ld | g.C.ld | g.E.ld) & 1)) return cudaErrorInvalidValue;

@@ -338,6 +338,8 @@ cudaError_t gemm(const GemmArgs& g, bool ta, bool tb, cudaStream_t st);
 // Leaf Gaussian blocks through the Gram GEMM with the EPI == 1 epilogue
 // (lower-triangular tiles only).
 cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st);
+// 64 x 64 outputs with long K (op(B) = B^T), 8 warps per tile.
+cudaError_t gemm_small_tile(const GemmArgs& g, cudaStream_t st);
 // Panel update with the panel TRSM folded in (EPI == 2): N must be 64, op(B) = B^T.
 cudaError_t gemm_update_trsm(const GemmArgs& g, cudaStream_t st);
 // Gaussian cross-kernel row sums (EPI == 3), op(B) = B^T: partial sums per
