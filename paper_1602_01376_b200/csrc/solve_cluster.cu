@@ -20,6 +20,22 @@ namespace ks {
 
 constexpr int CN = 8;  // CTAs per cluster (portable cluster size)
 
+// The node's factor rows this pass reads, pulled into L2 at the start of the
+// kernel (rows [r0, r1), columns [0, ncols) of the row-major matrix): the
+// triangular solve below walks them block by block and would otherwise wait on
+// an HBM round trip per block step. One prefetch per 128-byte line, spread over
+// the cluster's threads.
+// DESC: last rows first (the backward solve starts at the bottom).
+__device__ __forceinline__ void l2_prefetch_rows(const double* A, int64_t lda, int r0, int r1, int ncols, int rank,
+                                                 bool desc = false) {
+  const int lines = (ncols + 15) / 16;
+  const int total = (r1 - r0) * lines;
+  for (int e = rank * STHREADS + threadIdx.x; e < total; e += CN * STHREADS) {
+    const int r = desc ? r1 - 1 - e / lines : r0 + e / lines, c = (e % lines) * 16;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(A + (int64_t)r * lda + c));
+  }
+}
+
 // Cluster-blocked triangular solve in place on every CTA's copy of x (n x QC):
 // UPPER selects U (backward, non-unit) vs unit L (forward).
 template <int QC, bool UPPER>
@@ -84,12 +100,15 @@ __device__ void cluster_trsv(cg::cluster_group& cl, const double* __restrict__ A
         for (int r = 0; r < CN; ++r) sum += part[(r * SB + lane) * QC + q];
         v[q] = x[(r0 + lane) * QC + q] - sum;
       }
+      // 1 / pivot for this lane's row, started before the substitution chain
+      // (a multiply in the chain instead of a division)
+      const double rd = UPPER ? 1.0 / D[lane][lane] : 1.0;
 #pragma unroll 4
       for (int s2 = 0; s2 < SB; ++s2) {
         const int c = UPPER ? SB - 1 - s2 : s2;
         if (UPPER && lane == c) {
 #pragma unroll
-          for (int q = 0; q < QC; ++q) v[q] /= D[c][c];
+          for (int q = 0; q < QC; ++q) v[q] *= rd;
         }
         const double dl = D[lane][c];
         const bool upd = UPPER ? (lane < c) : (lane > c);
@@ -151,6 +170,8 @@ __global__ void __cluster_dims__(CN, 1, 1) __launch_bounds__(STHREADS)
   double* red = part + CN * SB * QC;  // SWARPS x 32 x QC
   __shared__ double D[SB][SB + 1];
   const int v = nb.node[k], l = nb.left[k], r = nb.right[k];
+  // L (rows < TP, columns < TP) and L21aug (rows >= TP): columns [0, TP) of every row
+  l2_prefetch_rows(nb.Aug + (int64_t)k * T * T, T, 0, T, TP, rank);
   const double* cl_ = sb.c + (int64_t)l * S * sb.q;
   const double* cr_ = sb.c + (int64_t)r * S * sb.q;
   for (int e = threadIdx.x; e < S * QC; e += STHREADS) {
@@ -207,6 +228,8 @@ __global__ void __cluster_dims__(CN, 1, 1) __launch_bounds__(STHREADS)
   double* part = tv + S * QC;    // CN x SB x QC
   __shared__ double D[SB][SB + 1];
   const int v = nb.node[k], l = nb.left[k], r = nb.right[k];
+  // U and U12aug: the first TP rows, all T columns
+  l2_prefetch_rows(nb.Aug + (int64_t)k * T * T, T, 0, TP, T, rank, true);
   const double* yg = sb.y + (int64_t)(nb.first + k) * TP * sb.q;
   for (int e = threadIdx.x; e < TP * QC; e += STHREADS) u[e] = yg[(e / QC) * sb.q + q0 + e % QC];
   if (!root) {

@@ -107,12 +107,13 @@ __device__ void cta_trsv_rows(const double* __restrict__ A, int64_t lda, int n, 
       double v[QC];
 #pragma unroll
       for (int q = 0; q < QC; ++q) v[q] = x[(r0 + lane) * QC + q];
+      const double rd = UNIT ? 1.0 : 1.0 / D[lane][lane];  // (multiply in the chain)
 #pragma unroll 4
       for (int s2 = 0; s2 < SB; ++s2) {
         const int c = UPPER ? SB - 1 - s2 : s2;
         if (!UNIT && lane == c) {
 #pragma unroll
-          for (int q = 0; q < QC; ++q) v[q] /= D[c][c];
+          for (int q = 0; q < QC; ++q) v[q] *= rd;
         }
         const double dl = D[lane][c];
         const bool upd = UPPER ? (lane < c) : (lane > c);
@@ -246,12 +247,13 @@ __device__ void cta_trsv_trans(const double* __restrict__ A, int64_t lda, int n,
         for (int w = 0; w < SWARPS; ++w) sum += red[(w * 32 + lane) * QC + q];
         v[q] = x[(r0 + lane) * QC + q] - sum;
       }
+      const double rd = UNIT ? 1.0 : 1.0 / D[lane][lane];  // (multiply in the chain)
 #pragma unroll 4
       for (int s2 = 0; s2 < SB; ++s2) {
         const int c = FORWARD ? s2 : SB - 1 - s2;
         if (!UNIT && lane == c) {
 #pragma unroll
-          for (int q = 0; q < QC; ++q) v[q] /= D[c][c];
+          for (int q = 0; q < QC; ++q) v[q] *= rd;
         }
         const double dl = D[c][lane];  // (A^T)[lane][c] = A[c][lane]
         const bool upd = FORWARD ? (lane > c) : (lane < c);
