@@ -155,12 +155,26 @@ __global__ void __launch_bounds__(256, 6) k_potrf64(LeafBatch lb, int j0, double
   //   a[i][j] -= a[i][k] a[j][k] / p_k  (k < j <= i),  p_k = a[k][k] at step k;
   // afterwards L[k][k] = sqrt(p_k), L[i][k] = a[i][k] / sqrt(p_k)
   // (_cholesky, linalg.py:185-196; a non-positive p_k is NotSPDError, :190-192)
+  // 1/p_k leaves the chain: the next pivot p_{k+1} = a[k+1][k+1] - a[k+1][k]^2/p_k
+  // is formed (by the thread that also writes it) and inverted at the start of
+  // step k, while the other threads update; rpiv[k] holds 1/p_k
+  __shared__ double rpiv[64];
+  if (threadIdx.x == 0) {
+    double p0 = a[0][0];
+    if (!(p0 > 0.0) || !isfinite(p0)) p0 = 1.0;  // recorded below; keep the block finite
+    rpiv[0] = 1.0 / p0;
+  }
+  __syncthreads();
   for (int k = 0; k < 63; ++k) {
-    double p = a[k][k];
-    if (!(p > 0.0) || !isfinite(p)) p = 1.0;  // recorded below; keep the block finite
-    const double rp = 1.0 / p;
-    // 16 x 16 thread grid over the trailing lower triangle, no index division
+    const double rp = rpiv[k];
     const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
+    if (threadIdx.x == 0) {  // the same arithmetic as the (k+1, k+1) update below
+      const double l1 = a[k + 1][k] * rp;
+      double pn = fma(-l1, a[k + 1][k], a[k + 1][k + 1]);
+      if (!(pn > 0.0) || !isfinite(pn)) pn = 1.0;
+      rpiv[k + 1] = 1.0 / pn;
+    }
+    // 16 x 16 thread grid over the trailing lower triangle, no index division
     for (int i = k + 1 + ti; i < 64; i += 16) {
       const double li = a[i][k] * rp;
       for (int j = k + 1 + tj; j <= i; j += 16) a[i][j] = fma(-li, a[j][k], a[i][j]);
@@ -188,8 +202,10 @@ __global__ void __launch_bounds__(256, 6) k_potrf64(LeafBatch lb, int j0, double
   __syncthreads();
   // X = L^-1 right-looking: rows below k lose L[i][k] X[k] / L[k][k], then row
   // k is scaled; one barrier per step. x[i][j] (i > j) lives at a[j][i].
+  if (threadIdx.x < 64) rpiv[threadIdx.x] = 1.0 / a[threadIdx.x][threadIdx.x];  // 1 / L[k][k], all at once
+  __syncthreads();
   for (int k = 0; k < 64; ++k) {
-    const double rk = 1.0 / a[k][k];
+    const double rk = rpiv[k];
     const int cols = k + 1;
     const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
     for (int i = k + 1 + ti; i < 64; i += 16) {
