@@ -16,9 +16,12 @@ template <int W, bool UPPER, bool UNIT>
 __global__ void __launch_bounds__(128) k_trsm_rhs(const double* A, int64_t lda, int64_t sa, double* B, int64_t ldb,
                                                  int64_t sb, int ncols) {
   __shared__ double L[W][W + 1];
+  __shared__ double rdiag[W];  // 1 / diagonal, formed once (a multiply in the chain)
   const int b = blockIdx.y;
   const double* T = A + (int64_t)b * sa;
   for (int e = threadIdx.x; e < W * W; e += blockDim.x) L[e / W][e % W] = T[(int64_t)(e / W) * lda + e % W];
+  if (!UNIT)
+    for (int i = threadIdx.x; i < W; i += blockDim.x) rdiag[i] = 1.0 / T[(int64_t)i * lda + i];
   __syncthreads();
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= ncols) return;
@@ -53,7 +56,7 @@ __global__ void __launch_bounds__(128) k_trsm_rhs(const double* A, int64_t lda, 
         if (j > i) s0 = fma(L[i][j], x[j], s0);
     }
     double v = x[i] - ((s0 + s1) + (s2 + s3));
-    if (!UNIT) v /= L[i][i];
+    if (!UNIT) v *= rdiag[i];
     x[i] = v;
   }
 #pragma unroll
