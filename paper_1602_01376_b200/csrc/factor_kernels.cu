@@ -1142,6 +1142,83 @@ __device__ __forceinline__ double own_solve(const double* __restrict__ A, int64_
   return v;
 }
 
+// The non-transposed solves (L, U) with the coefficient loads coalesced: each
+// thread needs the 8 coefficients of its own row, but one row per lane makes
+// every load instruction touch 32 cache lines (the L1 tag lookups, not the
+// bytes, bound the step). Here the CTA loads the block's row segments 4 lanes
+// per row (8 lines per instruction), one step ahead, and stages them through
+// shared memory (cb: 2 x NT x 10 doubles); the step's barrier publishes them.
+template <int NT, int MODE>
+__device__ __forceinline__ double own_solve_rows(const double* __restrict__ A, int64_t lda, int n, const double* di,
+                                                 double v, double* xs, double* cb) {
+  constexpr int SB = 8, CS = 10;  // 8 coefficients per row, padded row stride (16 B aligned, conflict-free)
+  constexpr bool ASC = (MODE == SOLVE_L);
+  static_assert(MODE == SOLVE_L || MODE == SOLVE_U, "non-transposed solves only");
+  const int i = threadIdx.x, lane = i & 31;
+  const bool own = i < n;
+  const int nblk = n / SB;
+  double2 ld[4];
+  auto issue = [&](int b) {
+    const int r0 = b * SB;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = threadIdx.x + u * NT, row = c >> 2, part = c & 3;
+      const bool need = row < n && (ASC ? row >= r0 + SB : row < r0);
+      ld[u] = need ? ldg2(A + (int64_t)row * lda + r0 + 2 * part) : make_double2(0.0, 0.0);
+    }
+  };
+  auto stage = [&](int st) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = threadIdx.x + u * NT, row = c >> 2, part = c & 3;
+      if (row < NT) *reinterpret_cast<double2*>(cb + ((int64_t)st * NT + row) * CS + 2 * part) = ld[u];
+    }
+  };
+  __syncthreads();  // xs and cb may still be read by the caller's previous phase
+  issue(ASC ? 0 : nblk - 1);
+  stage(0);
+#pragma unroll 1
+  for (int step = 0; step < nblk; ++step) {
+    const int b = ASC ? step : nblk - 1 - step;
+    if (step + 1 < nblk) issue(ASC ? b + 1 : b - 1);
+    const int r0 = b * SB;
+    if ((i >> 5) == (r0 >> 5)) {  // the warp holding block b: x_b = D_b^-1 v_b
+      const int base = r0 & 31, s2 = lane - base;
+      const bool inb = own && s2 >= 0 && s2 < SB;
+      const double* d = di + (int64_t)b * SB * SB;
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+      for (int t2 = 0; t2 < SB; t2 += 2) {
+        const double v0 = __shfl_sync(0xffffffffu, v, base + t2);
+        const double v1 = __shfl_sync(0xffffffffu, v, base + t2 + 1);
+        if (inb) {
+          acc0 = fma(d[s2 * SB + t2], v0, acc0);
+          acc1 = fma(d[s2 * SB + t2 + 1], v1, acc1);
+        }
+      }
+      if (inb) {
+        v = acc0 + acc1;
+        xs[i] = v;
+      }
+    }
+    __syncthreads();
+    const bool after = own && (ASC ? i >= r0 + SB : i < r0);
+    if (after) {
+      const double* c = cb + ((int64_t)(step & 1) * NT + i) * CS;
+      double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < SB; j += 2) {
+        const double2 cc = *reinterpret_cast<const double2*>(c + j);
+        q0 = fma(cc.x, xs[r0 + j], q0);
+        q1 = fma(cc.y, xs[r0 + j + 1], q1);
+      }
+      v -= q0 + q1;
+    }
+    if (step + 1 < nblk) stage((step + 1) & 1);
+  }
+  return v;
+}
+
 template <int NT>
 __device__ __forceinline__ double nt_sum(double v, double* red) {
   constexpr int NWp = NT / 32;
@@ -1219,6 +1296,10 @@ __global__ void __launch_bounds__(NT, 1) k_hager_own(DevTree t, NodeBatch nb, co
       const double* At = lut + (int64_t)(nb.first + k) * TP * TP;
       y = own_solve<SB, NT, SOLVE_L, true>(At, TP, TP, dL, y, xs);
       y = own_solve<SB, NT, SOLVE_U, true>(At, TP, TP, dU, y, xs);
+    } else if constexpr (SB == 8 && NT == 512) {
+      double* cb = reinterpret_cast<double*>(pm + TP);  // 2 x NT x 10 staged coefficients
+      y = own_solve_rows<NT, SOLVE_L>(A, T, TP, dL, y, xs, cb);
+      y = own_solve_rows<NT, SOLVE_U>(A, T, TP, dU, y, xs, cb);
     } else {
       y = own_solve<SB, NT, SOLVE_L>(A, T, TP, dL, y, xs);
       y = own_solve<SB, NT, SOLVE_U>(A, T, TP, dU, y, xs);
@@ -1265,7 +1346,8 @@ static void launch_hager_own(const DevTree& t, const NodeBatch& nb, double* dinv
   dim3 g(nb.count, 2);
   k_diag_inv<SB><<<g, 256, 0, st>>>(nb, dinv);
   if (COLMAJ) k_lu_transpose<<<dim3(nb.t_pad / 32, nb.t_pad / 32, nb.count), 256, 0, st>>>(nb, lut);
-  const size_t smem = sizeof(double) * (2 * (size_t)nb.t_pad * SB + nb.t_pad + 2 * NT / 32) + sizeof(int) * nb.t_pad;
+  size_t smem = sizeof(double) * (2 * (size_t)nb.t_pad * SB + nb.t_pad + 2 * NT / 32) + sizeof(int) * nb.t_pad;
+  if (!COLMAJ && SB == 8 && NT == 512) smem = (smem + 15) / 16 * 16 + sizeof(double) * 2 * NT * 10;
   static size_t set = 0;
   if (smem > set) {
     cudaFuncSetAttribute(k_hager_own<SB, NT, COLMAJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
