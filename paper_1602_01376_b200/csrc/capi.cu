@@ -374,7 +374,10 @@ bool fused_merge_off() {
 int rlu(Launcher& L, const ks::NodeBatch& nb, int c0, int w, int pw, int* pend, int ext = 0) {
   const int64_t TT = (int64_t)nb.T * nb.T;
   if (w <= pw) {
-    ks::launch_lu_panel(nb, c0, w, L.st, pend);  // panel LU + its row interchanges everywhere else
+    if (w == 32 && pend[2] == 0 && ks::lu_panel32_ok(nb))
+      ks::launch_lu_panel32(nb, c0, L.st);  // two 16-column halves and their merge in one launch
+    else
+      ks::launch_lu_panel(nb, c0, w, L.st, pend);  // panel LU + its row interchanges everywhere else
     pend[2] = 0;                                   // the pending U12 block (if any) is in place now
     *L.count += 1;
     if (int rc = L.check("lu_panel")) return rc;
@@ -609,13 +612,18 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
   f->t_pad = 2 * f->s_pad;
   f->T = 3 * f->s_pad;
   f->R = f->m_pad + f->s_pad;
-  // LU panel width: the panel's Z rows live in registers (16 columns up to 1024
-  // rows, 8 beyond). KS_PANEL_W=32 selects 32-column panels where t_pad <= 512
-  // (measured no faster at config 3: 75.7 vs 75.5 ms); 8 forces narrow panels.
+  // LU panel width of the launch sequence: register panels of 16 columns (up to
+  // 1024 candidate rows, 8 beyond). KS_PANEL_W=32 selects 32-column panels where
+  // they fit in shared memory: two 16-column halves and their merge in one
+  // launch (k_lu_panel32) -- measured slower at config 3 (69.6 vs 69.1 ms: the
+  // merge then runs on one SM per node instead of a grid); 8 forces narrow panels.
   f->pw = (f->T <= 1024) ? 16 : 8;
   if (const char* e = std::getenv("KS_PANEL_W")) {
     const int w = std::atoi(e);
-    if (w == 32 && f->t_pad <= 512) f->pw = 32;
+    ks::NodeBatch probe{};
+    probe.t_pad = f->t_pad;
+    probe.T = f->T;
+    if (w == 32 && ks::lu_panel32_ok(probe)) f->pw = 32;
     else if (w == 8) f->pw = 8;
   }
   if (f->T > 2048) { delete f; return fail(KS_ERR_UNSUPPORTED, "skeleton rank %lld too large (max 682)", (long long)s_max); }

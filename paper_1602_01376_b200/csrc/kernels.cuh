@@ -78,6 +78,9 @@ void launch_lu_merge(const NodeBatch& nb, int c0, int h, int w, cudaStream_t st)
 // shape) and the cooperative launch (0 ok). sync: 4 zeroed words per node;
 // err: the watchdog word. write_h: sym(H) -> H[node] (not at the root).
 int slab_width(const NodeBatch& nb);
+// 32-column panel as two 16-column halves in shared memory (lu_slab.cu)
+bool lu_panel32_ok(const NodeBatch& nb);
+void launch_lu_panel32(const NodeBatch& nb, int c0, cudaStream_t st);
 int launch_lu_slab(const NodeBatch& nb, double* H, int64_t h_stride, bool write_h, unsigned* sync, unsigned* err,
                    cudaStream_t st);
 void launch_fb_assemble(const DevTree& t, const NodeBatch& fb, const int* begin, const int* size, const double* lam,

@@ -403,6 +403,149 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// 32-column LU panel of the launch sequence (wide levels), factored as two
+// 16-column halves in shared memory by one CTA per node: the second half is
+// updated from the first (TRSM + DMMA tile update) inside the kernel, which
+// replaces two panel launches, a 16-wide TRSM launch and a 16-wide GEMM launch
+// of the recursion (capi.cu rlu) per 32 columns. Same pivot rule and output
+// layout as two k_lu_panel2 launches with their merge; the row interchanges
+// are applied to every column outside the panel.
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_lu_panel32(NodeBatch nb, int c0) {
+  constexpr int PW = 16, SW = 32, LD = SW + 1, NW = NT / 32;
+  pdl_wait();
+  const int k = blockIdx.x;
+  const int T = nb.T, TP = nb.t_pad;
+  const int nr = T - c0;          // panel rows [c0, T), relative index
+  const int nz = TP - c0;         // candidate rows [0, nz)
+  double* A = nb.Aug + (int64_t)k * T * T;
+  int* pivk = nb.piv + (int64_t)k * TP;
+  extern __shared__ __align__(16) double smem[];
+  double* Sl = smem;  // nr x LD
+  __shared__ PanelShared<NW, PW> ps;
+  __shared__ double urcp[SW];
+  __shared__ int spiv[SW], msrc[2 * SW], mdst[2 * SW];
+  for (int e = threadIdx.x; e < nr * SW; e += NT) {
+    const int r = e / SW, c = e % SW;
+    Sl[r * LD + c] = A[(int64_t)(c0 + r) * T + c0 + c];
+  }
+  __syncthreads();
+  for (int hh = 0; hh < 2; ++hh) {
+    const int cj = hh * PW;  // relative first row/column of this half
+    if (hh > 0) {
+      tile_trsm<PW, PW, LD, LD>(Sl, 0, PW, Sl);
+      __syncthreads();
+      tile_update<PW, PW, NT, LD, true>(Sl, PW, nullptr, 0, 0, 0, PW, nz);
+      __syncthreads();
+    }
+    const int rows = nz - cj;
+    {
+      double a[1][PW];
+      int pos[1];
+      bool done[1];
+      const int r = threadIdx.x;
+      pos[0] = r;
+      done[0] = (r >= rows);
+#pragma unroll
+      for (int q = 0; q < PW; ++q) a[0][q] = (r < rows) ? Sl[(cj + r) * LD + cj + q] : 0.0;
+      const int nact = panel_warps(rows, NT);
+      if ((int)(threadIdx.x >> 5) < nact)
+        panel_columns<PW, 1, NT, PW>(a, pos, done, ps, Sl + (size_t)cj * LD + cj, LD, rows, pivk + c0 + cj, c0 + cj,
+                                     nb.info + k, c0 + cj, nact);
+    }
+    __syncthreads();
+    if (threadIdx.x < PW) {
+      spiv[threadIdx.x] = pivk[c0 + cj + threadIdx.x] - (c0 + cj);
+      urcp[cj + threadIdx.x] = ps.urcp[threadIdx.x];
+    }
+    __syncthreads();
+    slab_moves<PW, SW, NT, LD>(Sl, cj, spiv, msrc, mdst);
+  }
+  // augmented rows: first half, its update of the second half, second half
+  for (int hh = 0; hh < 2; ++hh) {
+    const int cj = hh * PW;
+    if (hh > 0) {
+      tile_update<PW, PW, NT, LD, true>(Sl, PW, nullptr, 0, 0, 0, nz, nr);
+      __syncthreads();
+    }
+    for (int r = nz + threadIdx.x; r < nr; r += NT) {
+      double x[PW];
+#pragma unroll
+      for (int q = 0; q < PW; ++q) x[q] = Sl[r * LD + cj + q];
+#pragma unroll
+      for (int kk = 0; kk < PW; ++kk) {
+        const double l = x[kk] * urcp[cj + kk];
+        x[kk] = l;
+#pragma unroll
+        for (int q = kk + 1; q < PW; ++q) x[q] = fma(-l, Sl[(cj + kk) * LD + cj + q], x[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < PW; ++q) Sl[r * LD + cj + q] = x[q];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < nr * SW; e += NT) {
+    const int r = e / SW, c = e % SW;
+    A[(int64_t)(c0 + r) * T + c0 + c] = Sl[r * LD + c];
+  }
+  // the 32 interchanges for every column outside the panel (rows [c0, TP)):
+  // touched rows followed through the swap sequence, all loads, then stores
+  if (threadIdx.x < SW) spiv[threadIdx.x] = pivk[c0 + threadIdx.x] - c0;
+  __syncthreads();
+  if (threadIdx.x < 2 * SW) {
+    const int x = threadIdx.x < SW ? (int)threadIdx.x : spiv[threadIdx.x - SW];
+    int f = x;
+    for (int i = 0; i < SW; ++i) {
+      const int p = spiv[i];
+      f = (f == i) ? p : (f == p ? i : f);
+    }
+    msrc[threadIdx.x] = (f != x) ? x : -1;
+    mdst[threadIdx.x] = f;
+  }
+  __syncthreads();
+  const int npair = (T - SW) / 2;
+  constexpr int PER = 12;
+  for (int e0 = 0; e0 < 2 * SW * npair; e0 += PER * NT) {
+    double2 v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = e0 + u * NT + threadIdx.x;
+      if (e < 2 * SW * npair) {
+        const int m = e / npair, x2 = 2 * (e % npair);
+        const int col = x2 < c0 ? x2 : x2 + SW;
+        if (msrc[m] >= 0) v[u] = *reinterpret_cast<const double2*>(A + (int64_t)(c0 + msrc[m]) * T + col);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = e0 + u * NT + threadIdx.x;
+      if (e < 2 * SW * npair) {
+        const int m = e / npair, x2 = 2 * (e % npair);
+        const int col = x2 < c0 ? x2 : x2 + SW;
+        if (msrc[m] >= 0) *reinterpret_cast<double2*>(A + (int64_t)(c0 + mdst[m]) * T + col) = v[u];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+bool lu_panel32_ok(const NodeBatch& nb) {
+  return nb.t_pad <= 512 && nb.T % 32 == 0 && (size_t)nb.T * 33 * 8 <= 200 * 1024;
+}
+
+void launch_lu_panel32(const NodeBatch& nb, int c0, cudaStream_t st) {
+  const size_t smem = (size_t)(nb.T - c0) * 33 * sizeof(double);
+  static size_t set = 0;
+  if (smem > set) {
+    cudaFuncSetAttribute(k_lu_panel32<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    set = 200 * 1024;
+  }
+  launch_pdl(k_lu_panel32<512>, dim3(nb.count), dim3(512), smem, st, nb, c0);
+}
+
 namespace {
 
 template <int SW, int PW, int RPT>
