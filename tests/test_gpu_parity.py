@@ -153,3 +153,22 @@ def test_persistent_lu_levels(golden, case, slab_max, monkeypatch):
         mine = np.array([zc[int(v)] for v in g["z_cond_nodes"]])
         assert np.allclose(mine, g["z_cond"], rtol=1e-6)
     hf.close()
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg3s", "ragged"])
+def test_panel32_launch_sequence(golden, case, monkeypatch):
+    """The opt-in 32-column LU panel (two 16-column halves in one launch,
+    KS_PANEL_W=32) on every level of the launch sequence (KS_SLAB_MAX=0)."""
+    import paper_1602_01376_b200 as ks
+    g = golden(case)
+    monkeypatch.setenv("KS_PANEL_W", "32")
+    monkeypatch.setenv("KS_SLAB_MAX", "0")
+    hf = ks.factorize(g, float(g["lam"]))
+    monkeypatch.delenv("KS_PANEL_W")
+    monkeypatch.delenv("KS_SLAB_MAX")
+    u = ks.solve_many(hf, g["b"])
+    assert rel(u, g["u"]) <= TOL.get(case, 1e-10), rel(u, g["u"])
+    for i, v in enumerate(g["H_nodes"]):
+        H = g["H"][g["H_off"][i]:g["H_off"][i + 1]]
+        assert rel(hf.node_h(int(v)).ravel(), H) <= 1e-11, int(v)
+    hf.close()
