@@ -717,10 +717,19 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel2(NodeBatch nb, int c0, in
     *reinterpret_cast<double2*>(A + (int64_t)(c0 + spos[r]) * T + c0 + j2) =
         *reinterpret_cast<const double2*>(fin + r * FS + j2);
   }
-  // the augmented rows, eliminated against the panel's pivot rows
+  // the augmented rows, eliminated against the panel's pivot rows; loaded and
+  // stored W/2 lanes per row (coalesced) through the finished-value buffer
+  __syncthreads();  // fin is free once the panel rows are written back
   PANEL_STAMP(21);
-  for (int r = threadIdx.x; r < T - nb.t_pad; r += NT) {
-    double2* row = reinterpret_cast<double2*>(A + (int64_t)(nb.t_pad + r) * T + c0);
+  const int naug = T - nb.t_pad;
+  for (int e = threadIdx.x; e < naug * (W / 2); e += NT) {
+    const int r = e / (W / 2), j2 = 2 * (e % (W / 2));
+    *reinterpret_cast<double2*>(fin + r * FS + j2) =
+        *reinterpret_cast<const double2*>(A + (int64_t)(nb.t_pad + r) * T + c0 + j2);
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < naug; r += NT) {
+    double2* row = reinterpret_cast<double2*>(fin + r * FS);
     const double* ut = &u11[0][0];
     asm volatile("" : "+l"(ut));
     double x[W];
@@ -739,6 +748,12 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel2(NodeBatch nb, int c0, in
     }
 #pragma unroll
     for (int j = 0; j < W / 2; ++j) row[j] = make_double2(x[2 * j], x[2 * j + 1]);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < naug * (W / 2); e += NT) {
+    const int r = e / (W / 2), j2 = 2 * (e % (W / 2));
+    *reinterpret_cast<double2*>(A + (int64_t)(nb.t_pad + r) * T + c0 + j2) =
+        *reinterpret_cast<const double2*>(fin + r * FS + j2);
   }
   // the same row interchanges for every column outside the panel
   __shared__ int msrc[RPT * NT < 2 * W ? RPT * NT : 2 * W], mdst[RPT * NT < 2 * W ? RPT * NT : 2 * W];
@@ -797,7 +812,7 @@ static bool panel_v1() {
 template <int W, int RPT, int NT, int MINB = 1>
 static void launch_panel(const NodeBatch& nb, int c0, cudaStream_t st, const int* pend) {
   if (!panel_v1()) {
-    const size_t smem = (size_t)(nb.t_pad - c0) * (W + 2) * sizeof(double);
+    const size_t smem = (size_t)std::max(nb.t_pad - c0, nb.T - nb.t_pad) * (W + 2) * sizeof(double);
     static size_t set2 = 0;
     if (smem > set2) {
       cudaFuncSetAttribute(k_lu_panel2<W, RPT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
