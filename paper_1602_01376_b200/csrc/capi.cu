@@ -9,6 +9,7 @@
 #include <ctime>
 #include <string>
 #include <type_traits>
+#include <atomic>
 #include <thread>
 #include <vector>
 
@@ -629,21 +630,43 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
   if (f->T > 2048) { delete f; return fail(KS_ERR_UNSUPPORTED, "skeleton rank %lld too large (max 682)", (long long)s_max); }
 
   const double t_plan = host_ms();
-  // the permutation first: the device gather of the points trusts it
-  std::vector<int64_t> pos(p->n, -1);
-  for (int64_t i = 0; i < p->n; ++i) {
-    const int64_t id = p->perm[i];
-    if (id < 0 || id >= p->n || pos[id] >= 0) return bad("perm is not a permutation");
-    pos[id] = i;
-  }
+  // the permutation first: the device gather of the points trusts it. Host
+  // worker threads (the inverse is N random writes): pass 1 range-checks and
+  // inverts, pass 2 confirms pos[perm[i]] == i (any duplicate fails it).
+  auto parallel_for = [](int64_t n, auto&& body) {
+    const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(16, n / (1 << 16)));
+    std::vector<std::thread> th;
+    for (int t = 1; t < nth; ++t) th.emplace_back([&, t]() { body(n * t / nth, n * (t + 1) / nth); });
+    body(0, n / nth);
+    for (auto& x : th) x.join();
+  };
+  std::vector<int64_t> pos(p->n);
+  std::atomic<int> perm_bad{0};
+  parallel_for(p->n, [&](int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) {
+      const int64_t id = p->perm[i];
+      if (id < 0 || id >= p->n) { perm_bad = 1; return; }
+      pos[id] = i;
+    }
+  });
+  if (!perm_bad)
+    parallel_for(p->n, [&](int64_t a, int64_t b) {
+      for (int64_t i = a; i < b; ++i)
+        if (pos[p->perm[i]] != i) { perm_bad = 1; return; }
+    });
+  if (perm_bad) return bad("perm is not a permutation");
   const size_t nl = f->leaf_nodes.size();
   const int64_t nsk = p->skel_off[nn];
   std::vector<int> sp((size_t)nsk);
-  for (int64_t i = 0; i < nsk; ++i) {
-    const int64_t id = p->skel[i];
-    if (id < 0 || id >= p->n) return bad("skeleton id out of range");
-    sp[i] = (int)pos[id];
-  }
+  std::atomic<int> skel_bad{0};
+  parallel_for(nsk, [&](int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) {
+      const int64_t id = p->skel[i];
+      if (id < 0 || id >= p->n) { skel_bad = 1; return; }
+      sp[i] = (int)pos[id];
+    }
+  });
+  if (skel_bad) return bad("skeleton id out of range");
   std::vector<int64_t> so(p->skel_off, p->skel_off + nn + 1), co(p->coeff_off, p->coeff_off + nn + 1);
   std::vector<int> rk(nn);
   for (int64_t v = 0; v < nn; ++v) rk[v] = (int)f->rank[v];
@@ -809,7 +832,7 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
   // ---- host checks while the copies run: point coordinates on worker threads
   {
     const int64_t total = p->n * p->d;
-    const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(8, total / (1 << 20)));
+    const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(16, total / (1 << 20)));
     std::vector<char> ok(nth, 1);
     std::vector<std::thread> th;
     for (int t = 0; t < nth; ++t)
