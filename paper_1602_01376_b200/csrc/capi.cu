@@ -483,6 +483,13 @@ static bool host_timing() {
   return v == 1;
 }
 
+// subtree pipelining covers the deepest levels with at least KS_PIPE_MIN
+// (default 16) nodes per subtree
+static int pipe_min_nodes() {
+  const char* e = std::getenv("KS_PIPE_MIN");
+  return e ? std::max(1, std::atoi(e)) : 16;
+}
+
 static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor** out) {
   const double t_start = host_ms();
   if (!p || !out) return fail(KS_ERR_INVALID, "null argument");
@@ -597,7 +604,7 @@ static int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_f
     for (int lev = 0; lev < f->n_local_levels && nlv % G == 0; ++lev) {
       const auto& lv = f->levels[lev];
       const int c = (int)lv.size();
-      if (c % G || c / G < 16) break;
+      if (c % G || c / G < pipe_min_nodes()) break;
       bool ok = true;
       for (int i = 0; i < c; ++i) {
         const int g = i / (c / G), v = lv[i];
