@@ -410,237 +410,15 @@ void launch_colnorm1(const DevTree&, const NodeBatch& nb, cudaStream_t st) {
 
 // --------------------------------------------------------------------------
 // LU with partial pivoting restricted to rows < t_pad (linalg.py:199-213 on
-// the Z block; the -PG rows are eliminated but never chosen as pivots).
-// Base panel: W columns [c0, c0+W), rows [c0, T), held in registers (each of
-// the NT threads owns up to RPT physical rows). Rows are never moved inside
-// the panel: each thread tracks its rows' LOGICAL positions (the
-// row-interchange sequence of the reference, swaps[k] = p). Columns go in
-// unrolled blocks of CB; after a block its finished values go to shared
-// memory and the register window shifts left by CB (compact code: the i-cache
-// is what limits a fully unrolled panel). One barrier per column.
-// Pivot search: |v| >= 0 compares like its bit pattern, so a warp maximum is
-// three redux ops (hi word, lo word, then the smallest logical position among
-// the maxima: np.argmax's first-occurrence rule), within and across warps.
-// --------------------------------------------------------------------------
-__device__ __forceinline__ void warp_argmax(double v, int p, unsigned& mh, unsigned& ml, int& mp, bool& top) {
-  const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
-  mh = __reduce_max_sync(0xffffffffu, hi);
-  ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-  top = (hi == mh && lo == ml);
-  mp = (int)__reduce_min_sync(0xffffffffu, top ? (unsigned)p : 0x7fffffffu);
-}
-
-template <int W, int RPT, int NT, int MINB = 1>
-__global__ void __launch_bounds__(NT, MINB) k_lu_panel(NodeBatch nb, int c0, int pr0, int pc0, int ph, int pcols) {
-  pdl_wait();
-  constexpr int NW = NT / 32;
-  constexpr int NONE = 0x7fffffff;
-  constexpr int CB = 4;       // columns per unrolled block
-  constexpr int FS = W + 2;   // finished-value row stride (16 B aligned, conflict-free 16 B stores)
-  static_assert(NW <= 32 && W % CB == 0, "panel shape");
-  const int k = blockIdx.x;
-  const int T = nb.T;
-  double* A = nb.Aug + (int64_t)k * T * T;
-  if (ph > 0) {  // U12 of the preceding fused merge (k_lu_merge), disjoint from this panel
-    const double* sc = nb.scratch + (int64_t)k * 32 * 64;
-    for (int e = threadIdx.x; e < ph * pcols; e += NT) {
-      const int i = e / pcols, j = e % pcols;
-      A[(int64_t)(pr0 + i) * T + pc0 + j] = sc[i * 64 + j];
-    }
-  }
-  // the register panel holds Z's rows [c0, t_pad) only (every one a pivot
-  // candidate); the augmented rows [t_pad, T) are never pivots and are reduced
-  // afterwards with the same operations (phase 2)
-  const int rows = nb.t_pad - c0;
-  const int plim = rows;
-  extern __shared__ __align__(16) double fin[];  // rows x FS finished values
-  __shared__ __align__(16) double cand[2][NW][W];  // per-warp candidate pivot rows, by column parity
-  __shared__ double wv[2][NW];
-  __shared__ int wp[2][NW], wr[2][NW];
-  __shared__ double u11[W][W + 1];  // effective pivot rows (U of the panel), for phase 2
-  __shared__ double urcp[W];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double a[RPT][W];
-  int pos[RPT];
-  bool done[RPT];
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int r = threadIdx.x + i * NT;
-    pos[i] = r;
-    done[i] = (r >= rows);
-    const double2* src = reinterpret_cast<const double2*>(A + (int64_t)(c0 + (r < rows ? r : 0)) * T + c0);
-#pragma unroll
-    for (int j = 0; j < W / 2; ++j) {
-      const double2 v = (r < rows) ? src[j] : make_double2(0.0, 0.0);
-      a[i][2 * j] = v.x;
-      a[i][2 * j + 1] = v.y;
-    }
-  }
-  int* info = nb.info + k;
-  int* piv = nb.piv + (int64_t)k * nb.t_pad + c0;
-#pragma unroll 1
-  for (int kb = 0; kb < W; kb += CB) {
-#pragma unroll
-    for (int c = 0; c < CB; ++c) {
-      const int kk = kb + c;  // panel column; c is its slot in the register window
-      const int buf = c & 1;
-      // 1) this thread's best eligible row (none: value 0, position NONE)
-      double bv = 0.0;
-      int bp = NONE, bi = -1;
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const int r = threadIdx.x + i * NT;
-        const double v = fabs(a[i][c]);
-        if (r < plim && !done[i] && (v > bv || (v == bv && pos[i] < bp))) { bv = v; bp = pos[i]; bi = i; }
-      }
-      unsigned mh, ml;
-      int mp;
-      bool top;
-      warp_argmax(bv, bp, mh, ml, mp, top);
-      if (top && bp == mp && bi >= 0) {  // the warp's winning lane publishes its row
-#pragma unroll
-        for (int i = 0; i < RPT; ++i)
-          if (i == bi) {
-#pragma unroll
-            for (int j = c; j < W; ++j) cand[buf][warp][j] = a[i][j];
-            wr[buf][warp] = threadIdx.x + i * NT;
-          }
-      }
-      if (lane == 0) { wv[buf][warp] = __hiloint2double((int)mh, (int)ml); wp[buf][warp] = mp; }
-      __syncthreads();
-      // 2) across warps, lane-parallel
-      {
-        const double v = lane < NW ? wv[buf][lane] : 0.0;
-        const int p = lane < NW ? wp[buf][lane] : NONE;
-        warp_argmax(v, p, mh, ml, mp, top);
-        bv = __hiloint2double((int)mh, (int)ml);
-        bp = mp;
-      }
-      const bool singular = !(bv > 0.0);
-      const int ww = singular ? 0 : __ffs(__ballot_sync(0xffffffffu, lane < NW && wp[buf][lane < NW ? lane : 0] == bp &&
-                                                                   wv[buf][lane < NW ? lane : 0] == bv)) - 1;
-      const int br = singular ? -1 : wr[buf][ww];
-      if (threadIdx.x == 0) {
-        if (singular && *info == 0) *info = c0 + kk + 1;  // linalg.py:205-206
-        piv[kk] = c0 + (singular ? kk : bp);
-      }
-      const double rcp = 1.0 / (singular ? 1.0 : cand[buf][ww][c]);
-      // 3) logical swap kk <-> bp, eliminate every other remaining row (linalg.py:209-212)
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const int r = threadIdx.x + i * NT;
-        const bool is_piv = !done[i] && (singular ? pos[i] == kk : r == br);
-        if (!singular && !done[i]) pos[i] = (r == br) ? kk : (pos[i] == kk ? bp : pos[i]);
-        const bool keep = done[i] || is_piv;  // U rows: values from column kk on are final
-        done[i] = keep;
-        const double l = keep ? 0.0 : a[i][c] * rcp;
-        if (!keep) a[i][c] = l;
-#pragma unroll
-        for (int j = c + 1; j < W; ++j) a[i][j] = fma(-l, singular ? 0.0 : cand[buf][ww][j], a[i][j]);
-      }
-    }
-    // block finished: flush its CB columns, shift the window
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int r = threadIdx.x + i * NT;
-      if (r < rows) {
-        double2* f2 = reinterpret_cast<double2*>(fin + r * FS + kb);
-#pragma unroll
-        for (int j = 0; j < CB / 2; ++j) f2[j] = make_double2(a[i][2 * j], a[i][2 * j + 1]);
-      }
-#pragma unroll
-      for (int j = 0; j < W; ++j) a[i][j] = (j + CB < W) ? a[i][j + CB] : 0.0;
-    }
-  }
-  __syncthreads();
-  // panel rows back to their logical positions
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int r = threadIdx.x + i * NT;
-    if (r >= rows) continue;
-    double2* dst = reinterpret_cast<double2*>(A + (int64_t)(c0 + pos[i]) * T + c0);
-    const double2* f2 = reinterpret_cast<const double2*>(fin + r * FS);
-#pragma unroll
-    for (int j = 0; j < W / 2; ++j) dst[j] = f2[j];
-    if (pos[i] < W) {  // a pivot row: U of the panel, for phase 2
-#pragma unroll
-      for (int j = 0; j < W; ++j) u11[pos[i]][j] = fin[r * FS + j];
-      urcp[pos[i]] = 1.0 / fin[r * FS + pos[i]];  // the loop's reciprocal of this pivot
-    }
-  }
-  // phase 2: the augmented rows, eliminated against the panel's pivot rows
-  // exactly as the register loop would have (same multiply and FMA order; a
-  // zero pivot column is a SingularMatrixError either way)
-  __syncthreads();
-  for (int r = threadIdx.x; r < T - nb.t_pad; r += NT) {
-    double2* row = reinterpret_cast<double2*>(A + (int64_t)(nb.t_pad + r) * T + c0);
-    // read the pivot rows through an opaque pointer: hoisting all W*W of them
-    // out of this loop would not fit in registers
-    const double* ut = &u11[0][0];
-    asm volatile("" : "+l"(ut));
-    double x[W];
-#pragma unroll
-    for (int j = 0; j < W / 2; ++j) {
-      const double2 v = row[j];
-      x[2 * j] = v.x;
-      x[2 * j + 1] = v.y;
-    }
-#pragma unroll
-    for (int kk = 0; kk < W; ++kk) {
-      const double l = x[kk] * urcp[kk];
-      x[kk] = l;
-#pragma unroll
-      for (int j = kk + 1; j < W; ++j) x[j] = fma(-l, ut[kk * (W + 1) + j], x[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < W / 2; ++j) row[j] = make_double2(x[2 * j], x[2 * j + 1]);
-  }
-  // the same row interchanges for every column outside the panel: at most 2W
-  // rows moved; the list goes through shared memory, all loads before stores
-  __shared__ int msrc[2 * W], mdst[2 * W];
-  __shared__ int nmove;
-  if (threadIdx.x == 0) nmove = 0;
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int r = threadIdx.x + i * NT;
-    if (r < rows && pos[i] != r) {
-      const int slot = atomicAdd(&nmove, 1);
-      msrc[slot] = (c0 + r) * T;
-      mdst[slot] = (c0 + pos[i]) * T;
-    }
-  }
-  __syncthreads();
-  const int nm = nmove;
-  // staged through the (now free) finished-value buffer, PC columns at a time
-  constexpr int PC = 256;
-  for (int cb = 0; cb < T - W; cb += PC) {
-    const int ncol = min(PC, T - W - cb);
-    for (int e = threadIdx.x; e < nm * PC; e += NT) {
-      const int m = e / PC, col = cb + e % PC;
-      if (col < cb + ncol) fin[e] = A[msrc[m] + (col < c0 ? col : col + W)];
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < nm * PC; e += NT) {
-      const int m = e / PC, col = cb + e % PC;
-      if (col < cb + ncol) A[mdst[m] + (col < c0 ? col : col + W)] = fin[e];
-    }
-    __syncthreads();
-  }
-}
-
-// --------------------------------------------------------------------------
-// Panel v2: the same elimination (same pivot rule, same logical-position
-// bookkeeping) with a shorter per-column critical path, which is what bounds
-// the top levels (one CTA per node, 16-32 dependent columns per launch):
-//  * pivot search on a 32-bit key (hi word of |v| + 1; 0 = not a candidate):
-//    one redux + one ballot decide the warp / CTA winner unless two keys tie
-//    on the hi word (then the low word and the logical position decide, as in
-//    np.argmax: first occurrence);
-//  * the winner's key, position and row travel in one 16-byte record;
-//  * l = a / pivot (a division, as linalg.py:210 divides the column);
-//  * the row interchanges outside the panel are staged in registers: all
-//    loads of a column chunk, one barrier, all stores.
+// the Z block; the -PG rows are eliminated but never chosen as pivots): one
+// W-column panel per launch and node (k_lu_panel2). The candidate rows live in
+// registers and never move inside the panel; each thread tracks its rows'
+// LOGICAL positions (the reference's swap sequence, swaps[k] = p). The column
+// loop is lu_panel.cuh (shared with the persistent LU of lu_slab.cu); then the
+// rows go back to their logical positions (coalesced), the augmented rows are
+// eliminated against the panel's U rows (coalesced through shared memory), and
+// the panel's row interchanges are applied to every column outside it (all
+// loads of a column chunk, one barrier, all stores).
 // --------------------------------------------------------------------------
 // probe hook (ks_probe_panel): clock64 stamps of CTA 0 at phase boundaries
 __device__ long long* g_panel_clk = nullptr;
@@ -800,35 +578,15 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel2(NodeBatch nb, int c0, in
   if (clk && threadIdx.x == 0) clk[24] = nm;
 }
 
-static bool panel_v1() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("KS_PANEL_V1");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 template <int W, int RPT, int NT, int MINB = 1>
 static void launch_panel(const NodeBatch& nb, int c0, cudaStream_t st, const int* pend) {
-  if (!panel_v1()) {
-    const size_t smem = (size_t)std::max(nb.t_pad - c0, nb.T - nb.t_pad) * (W + 2) * sizeof(double);
-    static size_t set2 = 0;
-    if (smem > set2) {
-      cudaFuncSetAttribute(k_lu_panel2<W, RPT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      set2 = smem;
-    }
-    launch_pdl(k_lu_panel2<W, RPT, NT, MINB>, dim3(nb.count), dim3(NT), smem, st, nb, c0, pend[0], pend[1], pend[2],
-               pend[3]);
-    return;
-  }
-  const size_t smem = (size_t)std::max((nb.t_pad - c0) * (W + 2), 2 * W * 256) * sizeof(double);
+  const size_t smem = (size_t)std::max(nb.t_pad - c0, nb.T - nb.t_pad) * (W + 2) * sizeof(double);
   static size_t set = 0;
   if (smem > set) {
-    cudaFuncSetAttribute(k_lu_panel<W, RPT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_lu_panel2<W, RPT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set = smem;
   }
-  launch_pdl(k_lu_panel<W, RPT, NT, MINB>, dim3(nb.count), dim3(NT), smem, st, nb, c0, pend[0], pend[1], pend[2],
+  launch_pdl(k_lu_panel2<W, RPT, NT, MINB>, dim3(nb.count), dim3(NT), smem, st, nb, c0, pend[0], pend[1], pend[2],
              pend[3]);
 }
 
@@ -856,32 +614,6 @@ void launch_lu_panel(const NodeBatch& nb, int c0, int w, cudaStream_t st, const 
   if (w == 32) launch_panel_w<32>(nb, c0, st, pend);
   else if (w == 16) launch_panel_w<16>(nb, c0, st, pend);
   else launch_panel_w<8>(nb, c0, st, pend);
-}
-
-// Apply the panel's row interchanges (swaps[c0..c0+w)) to every column outside
-// the panel (LAPACK getrf convention: L keeps later swaps; linalg.py:209). The
-// panel kernel lists the (at most 2w) rows its swaps moved; every column applies
-// that permutation with all loads issued before any store.
-__global__ void k_lu_swap(NodeBatch nb, int c0, int w) {
-  const int k = blockIdx.y;
-  const int T = nb.T;
-  const int* mv = nb.moves + (int64_t)k * (2 * 64 + 1);
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= T || (col >= c0 && col < c0 + w)) return;
-  double* A = nb.Aug + (int64_t)k * T * T + col;
-  const int n = mv[0];
-  double v[64];
-#pragma unroll
-  for (int i = 0; i < 64; ++i)
-    if (i < n) v[i] = A[(int64_t)mv[1 + 2 * i] * T];
-#pragma unroll
-  for (int i = 0; i < 64; ++i)
-    if (i < n) A[(int64_t)mv[2 + 2 * i] * T] = v[i];
-}
-
-void launch_lu_swap(const NodeBatch& nb, int c0, int w, cudaStream_t st) {
-  dim3 g((nb.T + 127) / 128, nb.count);
-  k_lu_swap<<<g, 128, 0, st>>>(nb, c0, w);
 }
 
 // B := L^-1 B for the unit-lower W x W block at (r0, r0), B = rows r0..r0+W,

@@ -63,7 +63,6 @@ void launch_aug_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
 void launch_colnorm1(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
 // pend (may be null): {row0, col0, rows, cols} of a U12 block waiting in nb.scratch
 void launch_lu_panel(const NodeBatch& nb, int c0, int w, cudaStream_t st, const int* pend = nullptr);
-void launch_lu_swap(const NodeBatch& nb, int c0, int w, cudaStream_t st);
 void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncols, cudaStream_t st);
 // dinv: scratch for the diagonal-block inverses, 2 x t_pad x 16 doubles per internal node
 // max_ctas bounds the estimator's grid (it loops over the batch's nodes)

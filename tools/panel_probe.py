@@ -1,4 +1,4 @@
-"""Times one LU panel launch (k_lu_panel2 / KS_PANEL_V1=1 for the old one) on
+"""Times one LU panel launch (k_lu_panel2) on
 random nodes and prints CTA 0's phase clocks (ks_probe_panel)."""
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
