@@ -336,6 +336,15 @@ def run_ours(args) -> None:
     ph = np.mean(np.array(phases), axis=0).tolist() if phases else []
     cpu = cpu_sample(1) if not args.no_cpu else None
     B_solve = yardstick.solve_bytes(op, 1)
+    # DRAM bytes per factorization / per q=1 solve from the committed ncu capture
+    # (profiles/r01_dram_traffic.json: cold caches, an upper bound), config 3 only
+    traffic = {}
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_dram_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        if tj.get("config") == cfg.name:
+            traffic = tj
     line = {
         "metric": METRIC,
         "value": F / (ms_fac * 1e-3) / 1e12,
@@ -360,12 +369,14 @@ def run_ours(args) -> None:
         "level_ms": levels_ms,
         "yardstick": {"factor_tflop": F / 1e12, "solve_gb_q1": B_solve / 1e9},
         "roofline": {"bound": "tensor", "achieved": F / (ms_fac * 1e-3) / 1e12, "peak": fp64_peak,
-                     "unit": "TFLOP/s", "frac": F / (ms_fac * 1e-3) / 1e12 / fp64_peak, "traffic": None,
+                     "unit": "TFLOP/s", "frac": F / (ms_fac * 1e-3) / 1e12 / fp64_peak,
+                     "traffic": traffic.get("factor_bytes"), "traffic_source": traffic.get("source"),
                      "kernel": "whole factorization (DMMA GEMM + panel kernels); peak = cuBLAS DGEMM 8192^3 measured live (burst, best of 10)",
                      "peak_sustained": fp64_sustained, "frac_of_sustained": F / (ms_fac * 1e-3) / 1e12 / fp64_sustained,
                      "dgemm_sustained_clocks": clk_dgemm.summary()},
         "roofline_solve": {"bound": "hbm", "achieved": B_solve / (ms_sol * 1e-3) / 1e9, "peak": hbm_peak,
-                           "unit": "GB/s", "frac": B_solve / (ms_sol * 1e-3) / 1e9 / hbm_peak, "traffic": None},
+                           "unit": "GB/s", "frac": B_solve / (ms_sol * 1e-3) / 1e9 / hbm_peak,
+                           "traffic": traffic.get("solve_q1_bytes")},
         "e2e": {"value": F / (ms_e2e_fac * 1e-3) / 1e12, "unit": "TFLOP/s", "factor_ms": ms_e2e_fac,
                 "solve_ms": ms_e2e_sol, "h2d_bytes_per_step": h2d + b1.nbytes, "d2h_bytes_per_step": u2.nbytes,
                 "matches_device_run": same},
