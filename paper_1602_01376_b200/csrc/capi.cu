@@ -1007,7 +1007,6 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   const ks::DevTree dt = f->devtree();
   const ks::LeafBatch lb = f->leafbatch();
   const int nl = lb.count;
-  const int M = f->m_pad, S = f->s_pad, R = f->R;
   auto mark = [&](cudaEvent_t e) -> int {
     if (f->profiling) KS_CUDA(cudaEventRecord(e, st));
     return KS_OK;

@@ -433,7 +433,6 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel2(NodeBatch nb, int c0, in
   long long* clk = blockIdx.x == 0 ? g_panel_clk : nullptr;
   PANEL_STAMP(0);
   constexpr int NW = NT / 32;
-  constexpr int NONE = 0x7fffffff;
   constexpr int CB = 4;
   constexpr int FS = W + 2;
   static_assert(NW <= 32 && W % CB == 0, "panel shape");
@@ -706,7 +705,6 @@ __global__ void __launch_bounds__(STHREADS) k_hager(DevTree t, NodeBatch nb) {
   const int sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]];
   const int n = sl + sr;
   const double* A = nb.Aug + (int64_t)k * T * T;
-  const int* piv = nb.piv + (int64_t)k * TP;
   double* x = hv;
   double* y = hv + TP;
   double* w = hv + 2 * TP;

@@ -206,7 +206,7 @@ __global__ void __cluster_dims__(CN, 1, 1) __launch_bounds__(STHREADS)
   }
   if (!root) {  // c = P cc + L21aug y, rows of c split over the cluster
     double* c = sb.c + (int64_t)v * S * sb.q + q0;
-    const int r0 = rank * chunk, r1 = r0 + chunk;
+    const int r0 = rank * chunk;
     cta_gemv_rows<QC>(nb.Pn + (int64_t)k * S * TP + (int64_t)r0 * TP, TP, chunk, TP, cc, c + (int64_t)r0 * sb.q,
                       sb.q, false);
     __syncthreads();
