@@ -1184,8 +1184,8 @@ static int hager_ctas() {
   return e ? std::max(1, std::atoi(e)) : 96;
 }
 
-// KS_HAGER_FLUSH=n: launch the deferred wide-level estimates at the first
-// level with <= n nodes (default 0: the first narrow level)
+// KS_HAGER_FLUSH=n: launch the deferred estimates at the first level with <= n
+// nodes (default 0: the first narrow level, < 64 nodes)
 static int hager_flush_nodes() {
   const char* e = std::getenv("KS_HAGER_FLUSH");
   return e ? std::atoi(e) : 0;
@@ -1240,7 +1240,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
     const ks::NodeBatch nb = f->nodebatch((int)lev);
     const bool is_root_level = (f->levels[lev][0] == 0);
     const bool wide = nb.count >= 64;
-    if (!wide || nb.count <= hager_flush_nodes())
+    if (hager_flush_nodes() > 0 ? nb.count <= hager_flush_nodes() : !wide)
       if (int rc = flush()) return rc;
     const int G = wide ? n_groups() : 1;
     if (G == 1) {
@@ -1268,7 +1268,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
       KS_CUDA(cudaGetLastError());
     } else {
       deferred.push_back(lev);
-      if (!wide)
+      if (hager_flush_nodes() > 0 ? nb.count <= hager_flush_nodes() : !wide)
         if (int rc = flush()) return rc;
     }
     if (int rc2 = mark(f->ev_level[lev])) return rc2;
