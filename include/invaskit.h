@@ -80,7 +80,11 @@ int ks_create(const ks_problem* prob, int device, ks_factor** out);
  * called again on the same handle (e.g. a new lam); `stream` may be NULL. */
 int ks_factorize(ks_factor* f, double lam, void* stream);
 
-/* X = (K~ + lam I)^-1 B, B and X n x q row-major, tree order; q >= 0. */
+/* X = (K~ + lam I)^-1 B, B and X n x q row-major, tree order; q >= 0.
+ * Reentrant on one handle: every call runs in a workspace of its own, so
+ * concurrent calls from several threads / on several streams are safe (the
+ * reference's HierFactor is immutable and shared, solver.py:77-89). With
+ * device pointers the call is asynchronous on `stream`. */
 int ks_solve(ks_factor* f, const double* B, double* X, int64_t q, void* stream);
 
 /* ---- subtree sharding (one process per GPU) ----
@@ -175,7 +179,12 @@ int ks_test_gemm_cidx(int M, int N, int K, int batch, const double* A, const dou
                       int64_t lda, int64_t sa, int64_t ldb, int64_t sb, int64_t ldc, int64_t sc, int ta, int tb,
                       void* stream);
 
+/* Release the handle and its device memory (to the library's device pool). */
 void ks_destroy(ks_factor* f);
+
+/* Return the memory the library's private device pool caches for reuse by the
+ * next handle (up to KS_POOL_GB, default 32 GB) to the driver. */
+int ks_trim_pool(int device);
 
 /* Last error message of this thread (NUL-terminated, truncated to len). */
 int ks_last_error(char* buf, int64_t len);

@@ -19,7 +19,7 @@ from .errors import (
 from .problem import Problem, as_problem, from_arrays, from_compressed_kernel
 from .krr import krr_fit, krr_predict
 from .persist import load_factor, load_operator, load_points, save_factor, save_operator, save_points
-from .solver import GpuHierFactor, factorize, hss_matvec, solve, solve_many
+from .solver import GpuHierFactor, factorize, hss_matvec, release_cached_memory, solve, solve_many
 
 HierFactor = GpuHierFactor
 
@@ -36,6 +36,7 @@ __all__ = [
     "SingularMatrixError",
     "as_problem",
     "factorize",
+    "release_cached_memory",
     "from_arrays",
     "from_compressed_kernel",
     "hss_matvec",

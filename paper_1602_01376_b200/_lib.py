@@ -90,6 +90,7 @@ SIGNATURES = {
                      + [C.c_double, C.c_double, C.c_int, C.c_int, C.c_void_p]),
     "ks_test_gemm_cidx": (C.c_int, [C.c_int] * 4 + [C.c_void_p] * 4 + [C.c_int64] * 6 + [C.c_int, C.c_int, C.c_void_p]),
     "ks_destroy": (None, [C.c_void_p]),
+    "ks_trim_pool": (C.c_int, [C.c_int]),
     "ks_last_error": (C.c_int, [C.c_char_p, C.c_int64]),
     "ks_version": (C.c_char_p, []),
 }

@@ -2,6 +2,9 @@
 #pragma once
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -13,6 +16,29 @@
 namespace ks {
 
 constexpr int kWarp = 32;
+
+// Raise a kernel's dynamic shared-memory ceiling to at least `bytes` on the
+// current device. Cached per (device, kernel) -- the attribute is per device,
+// and the call is not free -- and thread-safe (solves may run concurrently).
+inline cudaError_t ensure_smem(const void* kern, size_t bytes, int carveout = -1) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> seen;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = seen.find({dev, kern});
+  if (it != seen.end() && bytes <= it->second) return cudaSuccess;
+  if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)) != cudaSuccess)
+    return e;
+  if (carveout >= 0 && it == seen.end()) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  seen[{dev, kern}] = bytes;
+  return cudaSuccess;
+}
+template <typename K>
+inline cudaError_t ensure_smem(K* kern, size_t bytes, int carveout = -1) {
+  return ensure_smem(reinterpret_cast<const void*>(kern), bytes, carveout);
+}
 
 // fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col). On sm_100a this is
 // DMMA.8x8x4 in SASS (the m16n8k{4,8,16} forms lower to sequences of it).

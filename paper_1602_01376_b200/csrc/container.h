@@ -91,6 +91,11 @@ struct KfReader {
     if (!get(magic, 8) || std::memcmp(magic, "KSINVASK", 8) != 0) { err = "not a KSINVASK file"; return false; }
     if (!get(&ver, 4) || ver != 1) { err = "unsupported container version"; return false; }
     if (!get(&kind, 4) || !get(&n, 8)) { err = "truncated header"; return false; }
+    const long start = std::ftell(fp);
+    std::fseek(fp, 0, SEEK_END);
+    const uint64_t fsize = (uint64_t)std::ftell(fp);
+    std::fseek(fp, start, SEEK_SET);
+    if (n > fsize / 24) { err = "bad entry count"; return false; }  // every entry header is >= 24 bytes
     for (uint64_t e = 0; e < n; ++e) {
       uint32_t nl = 0, dt = 0, res = 0;
       uint64_t cnt = 0;
@@ -102,6 +107,8 @@ struct KfReader {
       k.dtype = dt;
       k.count = cnt;
       k.offset = std::ftell(fp);
+      // element counts are bounded by the bytes left in the file (no overflow below)
+      if (k.offset < 0 || cnt > (fsize - (uint64_t)k.offset) / kf_size(dt)) { err = "truncated data"; return false; }
       const uint64_t bytes = cnt * kf_size(dt);
       const uint64_t padded = (bytes + 7) / 8 * 8;
       if (std::fseek(fp, (long)padded, SEEK_CUR) != 0) { err = "truncated data"; return false; }

@@ -234,11 +234,7 @@ __global__ void __launch_bounds__(256, 6) k_potrf64(LeafBatch lb, int j0, double
 
 void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStream_t st) {
   constexpr size_t smem = (64 * 65 + 64) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_potrf64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_smem(k_potrf64, smem);
   launch_pdl(k_potrf64, dim3(lb.count), dim3(256), smem, st, lb, j0, inv, info);
 }
 
@@ -580,11 +576,7 @@ __global__ void __launch_bounds__(NT, MINB) k_lu_panel2(NodeBatch nb, int c0, in
 template <int W, int RPT, int NT, int MINB = 1>
 static void launch_panel(const NodeBatch& nb, int c0, cudaStream_t st, const int* pend) {
   const size_t smem = (size_t)std::max(nb.t_pad - c0, nb.T - nb.t_pad) * (W + 2) * sizeof(double);
-  static size_t set = 0;
-  if (smem > set) {
-    cudaFuncSetAttribute(k_lu_panel2<W, RPT, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    set = smem;
-  }
+  ensure_smem(k_lu_panel2<W, RPT, NT, MINB>, smem);
   launch_pdl(k_lu_panel2<W, RPT, NT, MINB>, dim3(nb.count), dim3(NT), smem, st, nb, c0, pend[0], pend[1], pend[2],
              pend[3]);
 }
@@ -757,11 +749,7 @@ __global__ void __launch_bounds__(STHREADS) k_hager(DevTree t, NodeBatch nb) {
 
 static void launch_hager_blocked(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
   const size_t smem = sizeof(double) * (3 * nb.t_pad + SWARPS * 32) + sizeof(int) * nb.t_pad;
-  static size_t set = 0;
-  if (smem > set) {
-    cudaFuncSetAttribute(k_hager, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    set = smem;
-  }
+  ensure_smem(k_hager, smem);
   k_hager<<<nb.count, STHREADS, smem, st>>>(t, nb);
 }
 
@@ -1093,11 +1081,7 @@ static void launch_hager_own(const DevTree& t, const NodeBatch& nb, double* dinv
   if (COLMAJ) k_lu_transpose<<<dim3(nb.t_pad / 32, nb.t_pad / 32, nb.count), 256, 0, st>>>(nb, lut);
   size_t smem = sizeof(double) * (2 * (size_t)nb.t_pad * SB + nb.t_pad + 2 * NT / 32) + sizeof(int) * nb.t_pad;
   if (!COLMAJ && SB == 8 && NT == 512) smem = (smem + 15) / 16 * 16 + sizeof(double) * 2 * NT * 10;
-  static size_t set = 0;
-  if (smem > set) {
-    cudaFuncSetAttribute(k_hager_own<SB, NT, COLMAJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    set = smem;
-  }
+  ensure_smem(k_hager_own<SB, NT, COLMAJ>, smem);
   k_hager_own<SB, NT, COLMAJ><<<std::min(nb.count, max_ctas), NT, smem, st>>>(t, nb, dinv, lut);
 }
 
@@ -1345,6 +1329,8 @@ void launch_lu_merge(const NodeBatch& nb, int c0, int h, int w, cudaStream_t st)
 // random nodes of order T (pivot rows < tp), timed per launch with events;
 // clk receives CTA 0's clock64 stamps of the last launch (25 entries).
 // ---------------------------------------------------------------------------
+#include "../../include/invaskit_probe.h"
+
 extern "C" int ks_probe_panel(int T, int tp, int w, int count, int reps, double* ms, long long* clk) {
   using namespace ks;
   const size_t nA = (size_t)count * T * T;

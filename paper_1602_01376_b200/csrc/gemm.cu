@@ -12,12 +12,7 @@ cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, WM, WN, TA, TB, STAGES>;
   auto kern = k_gemm<BM, BN, WM, WN, TA, TB, STAGES, EPI>;
   constexpr size_t smem = (EPI == 2 && Cfg::SMEM_EPI2 > Cfg::SMEM) ? Cfg::SMEM_EPI2 : Cfg::SMEM;
-  static bool attr = false;  // per instantiation; set before first launch
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = ensure_smem(kern, smem)) return e;
   dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.batch);
   launch_pdl(kern, grid, dim3(Cfg::THREADS), smem, st, g);
   return cudaGetLastError();

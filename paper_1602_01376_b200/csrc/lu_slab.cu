@@ -538,11 +538,7 @@ bool lu_panel32_ok(const NodeBatch& nb) {
 
 void launch_lu_panel32(const NodeBatch& nb, int c0, cudaStream_t st) {
   const size_t smem = (size_t)(nb.T - c0) * 33 * sizeof(double);
-  static size_t set = 0;
-  if (smem > set) {
-    cudaFuncSetAttribute(k_lu_panel32<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    set = 200 * 1024;
-  }
+  ensure_smem(k_lu_panel32<512>, 200 * 1024);
   launch_pdl(k_lu_panel32<512>, dim3(nb.count), dim3(512), smem, st, nb, c0);
 }
 
@@ -554,17 +550,12 @@ int launch_slab_t(const NodeBatch& nb, double* H, int64_t hs, bool write_h, unsi
   constexpr int NT = 512;
   const size_t smem = ((size_t)nb.T * (SW + 1) + (size_t)PW * (PW + 1)) * sizeof(double);
   auto kern = k_lu_slab<SW, PW, RPT, NT>;
-  static size_t set = 0;
-  static int max_active = 0;
-  if (smem > set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
-    set = smem;
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
-    max_active = per_sm * sms;
-  }
+  if (ensure_smem(kern, smem) != cudaSuccess) return -1;
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+  const int max_active = per_sm * sms;  // co-resident CTAs: the cooperative launch's ceiling
   const int G = nb.T / SW;
   const int groups = std::min(nb.count, max_active / G);
   if (groups < 1) return -1;
@@ -622,6 +613,8 @@ int launch_lu_slab(const NodeBatch& nb, double* H, int64_t h_stride, bool write_
 }
 
 }  // namespace ks
+
+#include "../../include/invaskit_probe.h"
 
 // Probe hook: copies the stamps of the last traced level (KS_SLAB_TRACE=1).
 extern "C" int ks_slab_trace(long long* out, int64_t cap) {

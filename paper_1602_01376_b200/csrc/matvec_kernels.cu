@@ -193,7 +193,7 @@ static void chunks(int q, F f) {
 
 template <typename K>
 static void smem_attr(K kern, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (bytes > 48 * 1024) ensure_smem(kern, bytes);
 }
 
 #define KS_QC(KERN, GRID, BLOCK, SMEM, ...)                                   \

@@ -258,11 +258,7 @@ __global__ void __cluster_dims__(CN, 1, 1) __launch_bounds__(STHREADS)
 
 template <typename K>
 static void set_attr(K kern, size_t bytes) {
-  static size_t done = 0;
-  if (bytes > done) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    done = bytes;
-  }
+  ensure_smem(kern, bytes);
 }
 
 void launch_node_up_cluster(const NodeBatch& nb, const SolveBufs& sb, bool root, int q0, int qc, cudaStream_t st) {

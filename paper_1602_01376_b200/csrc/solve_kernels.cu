@@ -175,18 +175,7 @@ static void for_chunks(int q, F f) {
 
 template <typename K>
 static void set_smem(K kern, size_t bytes) {
-  // one cached ceiling per kernel instantiation (the attribute call is not free)
-  static thread_local std::vector<std::pair<const void*, size_t>> seen;
-  for (auto& e : seen)
-    if (e.first == (const void*)kern) {
-      if (bytes <= e.second) return;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      e.second = bytes;
-      return;
-    }
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  seen.push_back({(const void*)kern, bytes});
+  ensure_smem(kern, bytes, 100);
 }
 
 void launch_leaf_fwd(const LeafBatch& lb, const double* B, int64_t ldb, const SolveBufs& sb, cudaStream_t st) {

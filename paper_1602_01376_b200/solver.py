@@ -266,6 +266,16 @@ def hss_matvec(hf: GpuHierFactor, w):
     return Y[:, 0] if w.ndim == 1 else Y
 
 
+def release_cached_memory(device: int | None = None) -> None:
+    """Return the device memory the library caches between handles (its private
+    stream-ordered pool keeps up to KS_POOL_GB, default 32 GB, of freed factor
+    storage for the next factorize) to the driver, like torch.cuda.empty_cache."""
+    dev = _default_device() if device is None else int(device)
+    rc = _lib.load().ks_trim_pool(dev)
+    if rc:
+        _raise(rc)
+
+
 def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 

@@ -16,11 +16,13 @@ kernelsolve.hss_matvec (compress.py:352-411).
 from __future__ import annotations
 
 import hashlib
+import json
 import os
 import sys
 import time
 
 import numpy as np
+from dataclasses import asdict
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
@@ -46,6 +48,9 @@ CASES = {
     "cfg3s": (_cfg("cfg3", name="cfg3s", n=4096), 2),
     "cfg4s": (_cfg("cfg4", name="cfg4s", n=2048), 16),
     "cfg5s": (_cfg("cfg5", name="cfg5s", n=1024, leaf_size=256, max_rank=64), 1),
+    # config 5 at its own leaf/rank shape (m=2048, s=512, d=784, lambda=0.01):
+    # 4 leaves, 2 non-root internal nodes (t = 1024) and the root
+    "cfg5m": (_cfg("cfg5", name="cfg5m", n=8192), 1),
     # ragged tree: leaves on two adjacent depths, sizes 50/51/100 (tree.py:115-127)
     "ragged": (_cfg("cfg1", name="ragged", n=803, leaf_size=100, max_rank=32), 2),
     # a single leaf: the root is the whole problem (no skeletons at all)
@@ -114,10 +119,19 @@ def int_hash(arrs: dict) -> str:
     return h.hexdigest()
 
 
+# fixtures too large to carry their points: the loader regenerates them from
+# the recipe (bit-exact, checked against the stored sha256)
+NO_COORDS = {"cfg5m"}
+
+
 def make(case: str) -> None:
     cfg, q = CASES[case]
     ck, b, t_comp = build(cfg, q)
     arrs = marshal(ck)
+    if case in NO_COORDS:
+        c = np.ascontiguousarray(arrs.pop("coords"), dtype="<f8")
+        arrs["coords_sha256"] = np.array(hashlib.sha256(c.tobytes()).hexdigest())
+        arrs["gen_cfg"] = np.array(json.dumps(asdict(cfg)))
     arrs["lam"] = np.float64(cfg.lam)
     arrs["b"] = b
     arrs["int_hash"] = np.array(int_hash(arrs))
@@ -148,6 +162,8 @@ def make(case: str) -> None:
     # reduced matrices H of every non-root node (leaf: solver.py:135, internal: :163)
     hs, h_off, h_nodes = [], [0], []
     for v in range(len(ck.tree.nodes)):
+        if case in NO_COORDS and v in hf.leaf_factors and v != min(hf.leaf_factors):
+            continue  # keep the large fixture small: internal H plus the first leaf's
         if v in hf.leaf_factors and ck.tree.nodes[v].size < ck.n:
             P = ck.skeletons[v].coeff
             H = P @ ks.dense_solve(hf.leaf_factors[v].factor, P.T)

@@ -28,6 +28,17 @@ def test_library_exports_every_declared_symbol():
     assert b"sm_100a" in lib.ks_version()
 
 
+def test_library_exports_probe_hooks():
+    """tools/ probes bind the exports declared in include/invaskit_probe.h."""
+    from paper_1602_01376_b200 import _lib
+    lib = _lib.load()
+    txt = open(os.path.join(ROOT, "include", "invaskit_probe.h")).read()
+    names = sorted(set(re.findall(r"\b(ks_[a-z0-9_]+)\s*\(", txt)))
+    assert names == ["ks_probe_panel", "ks_slab_trace"]
+    for n in names:
+        assert hasattr(lib, n), n
+
+
 def test_library_is_sm100a_only():
     import subprocess
     so = os.path.join(ROOT, "paper_1602_01376_b200", "libinvaskit.so")

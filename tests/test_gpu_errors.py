@@ -1,0 +1,83 @@
+"""GPU runs of the reference's error and threshold semantics, through the
+public API over the C-ABI, against fixtures made by running the reference:
+
+* illcond.npz      cond(Z) ~ 2e10 at one node: the 1e10 warning
+                   (solver.py:183-188), z_cond, and the solution quality in
+                   that regime
+* illcond_hard.npz cond(Z) ~ 3e15 at node 2 (not the root):
+                   IllConditionedError(node_id, cond) (solver.py:150-152)
+* singular.npz     an exactly singular Z at node 1: SingularMatrixError
+                   (linalg.py:205-206)
+"""
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+
+def test_illcond_warnings_and_conditions(golden):
+    """cond(Z) up to 2e10, lambda = 1e-9. In this regime the reduced matrices
+    are sensitive to rounding: the reference's own round trip on its golden u
+    is 3.1 (roundtrip in the fixture), and any formulation of the same
+    algebra -- the reference's with its refinement steps, or a LAPACK one,
+    measured in DESIGN.md §2.1 -- differs from the reference's H at the
+    2e10 node by ~1e-3 (no formulation can match it more closely in fp64). So
+    the checks here are the ones the reference's semantics define: the same
+    nodes warned, in the same message format, the condition estimates to the
+    conditioning's accuracy, and a solution as good as the reference's."""
+    import paper_1602_01376_b200 as ks
+    g = golden("illcond")
+    hf = ks.factorize(g, float(g["lam"]))
+    try:
+        zc = hf.diagnostics["z_cond"]
+        assert sorted(zc) == g["z_cond_nodes"].tolist()
+        mine = np.array([zc[int(v)] for v in g["z_cond_nodes"]])
+        assert np.allclose(mine, g["z_cond"], rtol=0.2), np.max(np.abs(mine / g["z_cond"] - 1))
+        warned = [int(v) for v, c in zip(g["z_cond_nodes"], g["z_cond"]) if c > 1e10]
+        w = hf.diagnostics["warnings"]
+        assert len(w) == int(g["n_warnings"]) == len(warned) >= 1
+        for msg, v in zip(w, warned):  # the reference's message format (solver.py:184-188)
+            assert msg.startswith(f"node {v}: Z condition estimate ") and msg.endswith(
+                "exceeds 1e+10; results may lose accuracy"), msg
+        u = ks.solve_many(hf, g["b"])
+        r = ks.hss_matvec(hf, u) + float(g["lam"]) * u - g["b"]
+        assert np.linalg.norm(r) / np.linalg.norm(g["b"]) <= 2.0 * float(g["roundtrip"])
+    finally:
+        hf.close()
+
+
+def test_ill_conditioned_error_names_the_node(golden):
+    import paper_1602_01376_b200 as ks
+    g = golden("illcond_hard")
+    assert str(g["expect_error"]) == "IllConditionedError"
+    with pytest.raises(ks.IllConditionedError) as ei:
+        ks.factorize(g, float(g["lam"]))
+    assert ei.value.node_id == int(g["error_node"]) == 2
+    # Hager estimate of a Z whose pivot is ~1e-15: the reference's value within
+    # the rounding of that pivot (numpy subtracts a rounded product, DMMA fuses it)
+    assert ei.value.cond_estimate > 1e14
+    assert abs(np.log10(ei.value.cond_estimate / float(g["error_cond"]))) < 0.3
+
+
+def test_singular_matrix_error(golden):
+    import paper_1602_01376_b200 as ks
+    g = golden("singular")
+    assert str(g["expect_error"]) == "SingularMatrixError"
+    with pytest.raises(ks.SingularMatrixError, match="node 1"):
+        ks.factorize(g, float(g["lam"]))
+
+
+def test_error_leaves_the_library_usable(golden):
+    """After a failed factorization (handle released inside factorize), the
+    next factorization on the same device works."""
+    import paper_1602_01376_b200 as ks
+    with pytest.raises(ks.SingularMatrixError):
+        ks.factorize(golden("singular"), 0.0)
+    g = golden("cfg1")
+    hf = ks.factorize(g, float(g["lam"]))
+    try:
+        assert rel(ks.solve_many(hf, g["b"]), g["u"]) <= 1e-10
+    finally:
+        hf.close()

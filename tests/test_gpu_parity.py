@@ -7,8 +7,10 @@ from conftest import rel
 
 pytestmark = pytest.mark.gpu
 
-CASES = ["cfg1", "cfg2s", "cfg3s", "cfg4s", "cfg5s", "ragged", "single"]
-TOL = {"cfg5s": 1e-8}  # north_star: 1e-8 for the least-regularized config
+# cfg5m is config 5 at its own leaf/rank shape (m=2048, s=512, d=784, t=1024,
+# lambda=0.01) at N=8192; the others are configs 1-4 / shapes at reduced N
+CASES = ["cfg1", "cfg2s", "cfg3s", "cfg4s", "cfg5s", "cfg5m", "ragged", "single"]
+TOL = {"cfg5s": 1e-8, "cfg5m": 1e-8}  # north_star: 1e-8 for the least-regularized config
 
 
 @pytest.fixture(scope="module")
@@ -63,6 +65,23 @@ def test_leaf_cholesky_factor(gpu_factors):
     assert rel(L, g["leaf0_L"]) <= 1e-13
 
 
+@pytest.mark.parametrize("case", ["cfg3s", "cfg4s", "cfg5m"])
+def test_leaf_factor_matches_oracle(gpu_factors, case):
+    """The GPU leaf Cholesky factor at the BASELINE leaf sizes (m = 1024 / 512 /
+    2048) against the oracle's restatement of _cholesky (linalg.py:185-196),
+    itself pinned to the reference's factor (tests/test_oracle_golden.py)."""
+    from oracle import ks_oracle as O
+    g, hf = gpu_factors(case)
+    prob = O.Problem(g)
+    lam = float(g["lam"])
+    leaves = [v for v in range(g["node_begin"].size) if g["node_left"][v] < 0]
+    for v in (leaves[0], leaves[-1]):
+        ids = prob.node_points(v)
+        A = O.kernel_block(prob.coords, ids, ids, prob.h) + lam * np.eye(ids.size)
+        L_ref = O.cholesky(A)
+        assert rel(hf.leaf_factor(v), L_ref) <= 1e-13, (v, rel(hf.leaf_factor(v), L_ref))
+
+
 def test_multi_rhs(gpu_factors):
     import paper_1602_01376_b200 as ks
     g, hf = gpu_factors("cfg1")
@@ -90,7 +109,8 @@ def test_hss_matvec_matches_reference_operator(gpu_factors, case):
     assert np.linalg.norm(r) / np.linalg.norm(g["b"]) <= 1e-10
 
 
-@pytest.mark.parametrize("case,q", [("cfg1", 32), ("cfg1", 9), ("ragged", 8), ("cfg2s", 32), ("cfg3s", 16)])
+@pytest.mark.parametrize("case,q", [("cfg1", 32), ("cfg1", 9), ("ragged", 8), ("cfg2s", 32), ("cfg3s", 16),
+                                    ("cfg5m", 8)])
 def test_multi_rhs_paths_match_oracle(gpu_factors, case, q):
     """q >= 8 (even) runs the DMMA GEMM solve path, odd q the chunked path:
     both equal the oracle's telescoping solve column by column."""

@@ -9,7 +9,7 @@ import pytest
 from conftest import rel
 from oracle import ks_oracle as O
 
-SOLVE_CASES = ["cfg1", "cfg2s", "cfg3s", "cfg4s", "cfg5s", "ragged", "single"]
+SOLVE_CASES = ["cfg1", "cfg2s", "cfg3s", "cfg4s", "cfg5s", "cfg5m", "ragged", "single"]
 
 
 @pytest.fixture(scope="module")
@@ -64,6 +64,17 @@ def test_oracle_diagnostics(factored, case):
         assert np.allclose(mine, g["z_cond"], rtol=1e-6)
     assert of.diagnostics["fallback_nodes"] == g["fallback_nodes"].tolist()
     assert len(of.diagnostics["warnings"]) == int(g["n_warnings"])
+
+
+@pytest.mark.parametrize("case,exc", [("singular", O.Singular), ("illcond_hard", O.IllConditioned)])
+def test_oracle_error_paths(golden, case, exc):
+    """The oracle raises where the reference raised (tests/golden/make_error_golden.py)."""
+    g = golden(case)
+    with pytest.raises(exc) as ei:
+        O.factorize(O.Problem(g), float(g["lam"]))
+    if case == "illcond_hard":
+        assert ei.value.node_id == int(g["error_node"])
+        assert np.isclose(ei.value.cond_estimate, float(g["error_cond"]), rtol=1e-6)
 
 
 def test_oracle_leaf_factor(factored):
