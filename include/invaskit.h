@@ -147,6 +147,9 @@ int ks_get_leaf_factor(const ks_factor* f, int64_t node, double* out);
 
 /* Device bytes held by the handle. */
 int64_t ks_device_bytes(const ks_factor* f);
+/* Host -> device bytes ks_create / ks_create_shard copied: the operator inputs
+ * the handle reads (a shard skips the P blocks of the other shards' subtrees). */
+int64_t ks_upload_bytes(const ks_factor* f);
 /* Per-phase device times (ms) of the last ks_factorize / ks_solve, measured with
  * CUDA events on the launching stream when profiling is on:
  * [0] leaf assembly, [1] leaf Cholesky + L21, [2] leaf SYRK (H), [3] internal

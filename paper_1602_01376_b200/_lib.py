@@ -78,6 +78,7 @@ SIGNATURES = {
     "ks_get_node_h": (C.c_int, [C.c_void_p, C.c_int64, _f64p]),
     "ks_get_leaf_factor": (C.c_int, [C.c_void_p, C.c_int64, _f64p]),
     "ks_device_bytes": (C.c_int64, [C.c_void_p]),
+    "ks_upload_bytes": (C.c_int64, [C.c_void_p]),
     "ks_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "ks_get_phase_ms": (C.c_int, [C.c_void_p, _f64p, C.c_int]),
     "ks_get_level_ms": (C.c_int, [C.c_void_p, _f64p, C.c_int]),

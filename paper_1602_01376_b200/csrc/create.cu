@@ -278,6 +278,7 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     // the small tables first (pageable sources: staged before the call returns)
     auto put = [&](auto& buf, const auto& v) -> int {
       if (!v.empty()) KS_CUDA(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, u));
+      f->h2d_bytes += (int64_t)(v.size() * sizeof(v[0]));
       return KS_OK;
     };
     if (int rc = put(f->rank_d, rk)) return rc;
@@ -297,6 +298,7 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(cudaMemsetAsync(f->coords.p + (size_t)p->n * p->d, 0, sizeof(double) * f->m_pad * p->d, u));
     KS_CUDA(cudaMemcpyAsync(orig, p->coords, sizeof(double) * p->n * p->d, cudaMemcpyHostToDevice, u));
     KS_CUDA(cudaMemcpyAsync(pmd, p->perm, sizeof(int64_t) * p->n, cudaMemcpyHostToDevice, u));
+    f->h2d_bytes += (int64_t)(sizeof(double) * p->n * p->d + sizeof(int64_t) * p->n);
     ks::launch_gather_rows(orig, pmd, p->n, p->d, f->coords.p, u);
     ks::launch_row_sqnorms(f->coords.p, p->n + f->m_pad, p->d, f->xx.p, u);
     KS_CUDA(cudaFreeAsync(orig, u));
@@ -310,6 +312,7 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     auto flush = [&]() -> int {
       if (r1 > r0) KS_CUDA(cudaMemcpyAsync(f->coeff.p + r0, p->coeff + r0, sizeof(double) * (r1 - r0),
                                            cudaMemcpyHostToDevice, u));
+      if (r1 > r0) f->h2d_bytes += (int64_t)(sizeof(double) * (r1 - r0));
       r0 = r1 = -1;
       return KS_OK;
     };
@@ -346,8 +349,10 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
       if (int rc = flush()) return rc;
       KS_CUDA(cudaEventRecord(f->ev_up_level[lev], u));
     }
+    // a shard never reads the P of the other shards' subtrees (their H and c
+    // arrive through ks_node_exchange): only its own subtree and the top levels
     for (int64_t v = 0; v < nn; ++v)
-      if (!sent[v])
+      if (!sent[v] && (in_sub[v] || f->level[v] < f->shard_level))
         if (int rc = add(v)) return rc;
     if (int rc = flush()) return rc;
     KS_CUDA(cudaEventRecord(f->ev_up_all, u));

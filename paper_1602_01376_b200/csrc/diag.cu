@@ -193,6 +193,8 @@ int64_t ks_device_bytes(const ks_factor* f) {
   return b;
 }
 
+int64_t ks_upload_bytes(const ks_factor* f) { return f ? f->h2d_bytes : 0; }
+
 int ks_set_profiling(ks_factor* f, int on) {
   if (!f) return fail(KS_ERR_INVALID, "null handle");
   f->profiling = on != 0;

@@ -188,6 +188,7 @@ struct ks_factor {
   cudaEvent_t ev_up_coords = nullptr, ev_up_all = nullptr, ev_up_leaf[kLeafChunks] = {}, ev_up_sub[kLeafChunks] = {};
   std::vector<cudaEvent_t> ev_up_level;
   bool upload_pending = false;
+  int64_t h2d_bytes = 0;  // host -> device bytes ks_create copied (operator inputs this handle reads)
   // diagnostics
   std::vector<int> leaf_info_h, int_info_h;
   std::vector<double> cond_h;

@@ -118,12 +118,61 @@ class LibShard:
 # ---------------------------------------------------------------------------
 # orchestration (backend-agnostic)
 # ---------------------------------------------------------------------------
+def _err_info(exc: BaseException) -> tuple:
+    from . import errors as E
+
+    if isinstance(exc, E.IllConditionedError):
+        return ("IllConditionedError", int(exc.node_id), float(exc.cond_estimate))
+    return (type(exc).__name__, str(exc))
+
+
+def _rebuild(info: tuple, rank: int) -> BaseException:
+    from . import errors as E
+
+    name = info[0]
+    if name == "IllConditionedError":
+        return E.IllConditionedError(info[1], info[2])
+    cls = getattr(E, name, None)
+    msg = f"rank {rank}: {info[1]}"
+    if isinstance(cls, type) and issubclass(cls, Exception) and name != "IllConditionedError":
+        return cls(msg)
+    return E.KernelSolveError(f"rank {rank} failed with {name}: {info[1]}")
+
+
+def _agree(exc: BaseException | None, group=None) -> None:
+    """Collective status check before an exchange: if any rank failed in its
+    local phase, every rank raises the first failing rank's error (same type,
+    same node id / condition estimate) instead of blocking in the collective."""
+    import torch
+    import torch.distributed as dist
+
+    nccl = dist.get_backend(group) == "nccl"
+    flag = torch.tensor([0 if exc is None else 1], dtype=torch.int32,
+                        device=torch.device("cuda", torch.cuda.current_device()) if nccl else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    if int(flag.item()) == 0:
+        return
+    infos = [None] * dist.get_world_size(group)
+    dist.all_gather_object(infos, None if exc is None else _err_info(exc), group=group)
+    first = next(r for r, i in enumerate(infos) if i is not None)
+    if exc is not None and first == dist.get_rank(group):
+        raise exc
+    raise _rebuild(infos[first], first) from exc
+
+
 def factorize_sharded(backend, lam: float, group=None) -> None:
-    """Local subtree factorization, all-gather of the level-k H blocks, top levels."""
+    """Local subtree factorization, all-gather of the level-k H blocks, top levels.
+    A failure on any rank (e.g. IllConditionedError inside one subtree) is
+    raised on every rank (no rank is left waiting in the all-gather)."""
     import torch.distributed as dist
 
     lam = _check_lam(lam)
-    backend.factorize(lam)
+    err = None
+    try:
+        backend.factorize(lam)
+    except Exception as e:  # noqa: BLE001 -- re-raised on every rank by _agree
+        err = e
+    _agree(err, group)
     H = backend.export_h(backend.shard_root)
     world = len(backend.peers)
     Hs = [H.new_empty(H.shape) for _ in range(world)]
@@ -137,7 +186,11 @@ def factorize_sharded(backend, lam: float, group=None) -> None:
 def solve_many_sharded(backend, B, group=None, gather: bool = True):
     """Solve with the sharded factor. B: (n, q) tree order (torch tensor, any
     device) or the shard's own rows if gather is False. Returns the full X
-    (all-gathered to every rank) or the local rows."""
+    (all-gathered to every rank) or the local rows.
+
+    The subtree-root block c travels with one status row: a rank whose local
+    up pass failed still takes part in the all-gather (no rank blocks), and
+    after the down pass every rank raises that rank's error."""
     import torch
     import torch.distributed as dist
 
@@ -145,16 +198,28 @@ def solve_many_sharded(backend, B, group=None, gather: bool = True):
         raise ValueError("B must be n x q")
     q = B.shape[1]
     B_local = B[backend.begin:backend.end] if gather else B
-    backend.solve_up(B_local)
-    c = backend.export_c(backend.shard_root, q)
+    err = None
+    try:
+        backend.solve_up(B_local)
+        c = backend.export_c(backend.shard_root, q)
+    except Exception as e:  # noqa: BLE001 -- re-raised on every rank below
+        err = e
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+        c = torch.zeros(backend.s_pad, q, dtype=torch.float64, device=dev)
+    cst = torch.cat([c, c.new_full((1, q), 0.0 if err is None else 1.0)], dim=0)
     world = len(backend.peers)
-    cs = [c.new_empty(c.shape) for _ in range(world)]
-    dist.all_gather(cs, c, group=group)
-    for node, cn in zip(backend.peers, cs):
-        if node != backend.shard_root:
-            backend.import_c(node, cn)
-    backend.solve_top(q)
-    X_local = backend.solve_down(q)
+    cs = [cst.new_empty(cst.shape) for _ in range(world)]
+    dist.all_gather(cs, cst, group=group)
+    status = torch.stack([x[-1, 0] for x in cs])
+    X_local = None
+    if err is None:
+        for node, cn in zip(backend.peers, cs):
+            if node != backend.shard_root:
+                backend.import_c(node, cn[:-1].contiguous())
+        backend.solve_top(q)
+        X_local = backend.solve_down(q)
+    if float(status.max()) > 0.0:  # one host read per solve, after the device work is queued
+        _agree(err if err is not None else None, group)
     if not gather:
         return X_local
     sizes = [None] * world
@@ -168,65 +233,50 @@ def solve_many_sharded(backend, B, group=None, gather: bool = True):
 
 
 # ---------------------------------------------------------------------------
-# bench.py --gpus N (torchrun): strong scaling of config 3 over N GPUs
+# public multi-GPU entry points (one process per GPU, torch.distributed)
 # ---------------------------------------------------------------------------
-def bench_main(args, metric: str) -> None:
-    import json
-    import time
+class ShardedFactor:
+    """The subtree-sharded factor of one rank: `solve_many` is collective
+    (every rank calls it with the same B), and returns the full solution on
+    every rank (gather=True) or the rank's own rows of it."""
 
-    import torch
+    def __init__(self, backend, lam: float, group=None):
+        self.backend = backend
+        self.lam = lam
+        self.group = group
+
+    @property
+    def rows(self) -> tuple[int, int]:
+        return self.backend.begin, self.backend.end
+
+    def solve_many(self, B, gather: bool = True):
+        return solve_many_sharded(self.backend, B, self.group, gather)
+
+    def close(self) -> None:
+        self.backend.close()
+
+
+def factorize_distributed(ck, lam: float, threads: int = 1, *, group=None, device: int | None = None) -> ShardedFactor:
+    """factorize (solver.py:92) over the ranks of `group`: rank g factors the
+    g-th subtree at level log2(world) and the top levels redundantly. Every
+    rank must call it; an error on any rank is raised on all of them."""
     import torch.distributed as dist
 
-    from . import yardstick
-    from .configs import CONFIGS
-
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from producer import make_operator, make_rhs
-
-    cfg = CONFIGS[args.config]
-    op = make_operator(cfg, device="cuda")
-    # identical operator bits on every rank: rank 0's P wins
-    coeff = torch.from_numpy(op["coeff"]).cuda()
-    dist.broadcast(coeff, 0)
-    op["coeff"] = coeff.cpu().numpy()
-    del coeff
-    prob = as_problem(op)
-    root, peers = shard_for(prob, world, rank)
-    sh = LibShard(prob, root, local)
-    b = torch.from_numpy(make_rhs(cfg, op["perm"], 1)).cuda()
-    F = yardstick.factor_flops(op)
-    for _ in range(args.warmup):
-        factorize_sharded(sh, cfg.lam)
-        solve_many_sharded(sh, b, gather=False)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    dist.barrier()
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        ev[i][0].record()
-        factorize_sharded(sh, cfg.lam)
-        ev[i][1].record()
-        solve_many_sharded(sh, b, gather=False)
-        ev[i][2].record()
-    torch.cuda.synchronize()
-    dist.barrier()
-    tf = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
-    ts = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
-    t = torch.tensor([tf, ts], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    tf, ts = float(t[0]), float(t[1])
-    if rank == 0:
-        line = {
-            "metric": metric, "value": F / (tf * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tf + ts, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name} factor+solve q=1, subtree-sharded", "n": cfg.n, "d": cfg.d,
-                       "leaf": cfg.leaf_size, "rank": cfg.max_rank, "parallelism": f"subtree{world}"},
-            "factor_ms": tf, "solve_ms": ts,
-        }
-        print(json.dumps(line), flush=True)
-    sh.close()
-    dist.destroy_process_group()
+    del threads
+    lam = _check_lam(lam)
+    prob = as_problem(ck)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    root, _ = shard_for(prob, world, rank)
+    dev = int(os.environ.get("LOCAL_RANK", "0")) if device is None else int(device)
+    err, sh = None, None
+    try:
+        sh = LibShard(prob, root, dev)
+    except Exception as e:  # noqa: BLE001 -- re-raised on every rank by _agree
+        err = e
+    _agree(err, group)
+    try:
+        factorize_sharded(sh, lam, group)
+    except Exception:
+        sh.close()
+        raise
+    return ShardedFactor(sh, lam, group)
