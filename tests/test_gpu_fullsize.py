@@ -6,7 +6,10 @@ reference cannot run at these sizes; the oracle only at the mid size):
   right-hand side, bitwise run-to-run determinism, q-column equivalence;
 * config 2 recipe at N = 65,536 (its BASELINE size) against the CPU oracle on
   the same producer operator, whose kNN-guided skeletons reproduce the
-  reference's rank profile (74-128) and Z conditioning (4.5, F4).
+  reference's rank profile (74-128, SURVEY.md F3) and Z conditioning (4.5, F4);
+* configs 3 and 4 at their BASELINE sizes (N = 1,048,576 / 524,288) against the
+  LAPACK-backed oracle (oracle/ks_fast.py, pinned to the reference's goldens)
+  on the same producer operator (tests/fullsize_parity.py).
 """
 import numpy as np
 import pytest
@@ -86,3 +89,13 @@ def test_cfg2_fullsize_matches_oracle():
     ranks = op["rank"][1:]
     assert ranks.min() >= 64 and ranks.max() == cfg.max_rank  # variable ranks exercised (F3)
     hf.close()
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_fullsize_matches_fast_oracle(name):
+    import fullsize_parity
+
+    r = fullsize_parity.run(name)
+    assert r["u_rel_err"] <= r["tol_u"], r
+    assert r["H_top_levels_max_rel_err"] <= 1e-11, r
+    assert r["z_cond_max_rel_diff"] <= 1e-6, r

@@ -89,3 +89,31 @@ def test_oracle_matvec_roundtrip(factored):
     u = g["u"][:, 0]
     r = O.hss_matvec(prob, u) + float(g["lam"]) * u - g["b"][:, 0]
     assert np.linalg.norm(r) / np.linalg.norm(g["b"]) <= 1e-11
+
+
+# ---- the LAPACK-backed fast mode (oracle/ks_fast.py), same bar ----
+@pytest.mark.parametrize("case", SOLVE_CASES)
+def test_fast_oracle_matches_reference(golden, case):
+    from oracle import ks_fast as OF
+    g = golden(case)
+    ff = OF.factorize(O.Problem(g), float(g["lam"]))
+    u = OF.solve_many(ff, g["b"])
+    assert rel(u, g["u"]) <= 1e-12, rel(u, g["u"])
+    for i, v in enumerate(g["H_nodes"]):
+        H = g["H"][g["H_off"][i]:g["H_off"][i + 1]]
+        assert rel(ff.reduced[int(v)].ravel(), H) <= 1e-12, (int(v), rel(ff.reduced[int(v)].ravel(), H))
+    zc = OF.diagnostics(ff)["z_cond"]
+    assert sorted(zc) == g["z_cond_nodes"].tolist()
+    if zc:
+        assert np.allclose([zc[int(v)] for v in g["z_cond_nodes"]], g["z_cond"], rtol=1e-6)
+
+
+def test_fast_oracle_error_paths(golden):
+    from oracle import ks_fast as OF
+    g = golden("illcond_hard")
+    with pytest.raises(O.IllConditioned) as ei:
+        OF.factorize(O.Problem(g), float(g["lam"]))
+    assert ei.value.node_id == int(g["error_node"])
+    g = golden("singular")
+    with pytest.raises(O.Singular):
+        OF.factorize(O.Problem(g), float(g["lam"]))
