@@ -138,8 +138,9 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
   }
   f->m_pad = (int)roundup(m_max, 64);
   f->s_pad = (int)roundup(s_max, 64);
-  f->t_pad = 2 * f->s_pad;
-  f->T = 3 * f->s_pad;
+  f->t_pad = f->s_pad;     // node LU view: pivots among S = I - Y X's rows (kernels.cuh NodeBatch)
+  f->T = 2 * f->s_pad;
+  f->zt = 2 * f->s_pad;
   f->R = f->m_pad + f->s_pad;
   // LU panel width of the launch sequence: register panels of 16 columns (up to
   // 1024 candidate rows, 8 beyond). KS_PANEL_W=32 selects 32-column panels where
@@ -154,7 +155,7 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     if (w == 32 && ks::lu_panel32_ok(probe)) f->pw = 32;
     else if (w == 8) f->pw = 8;
   }
-  if (f->T > 2048) { delete f; return fail(KS_ERR_UNSUPPORTED, "skeleton rank %lld too large (max 682)", (long long)s_max); }
+  if (f->s_pad > 1024) { delete f; return fail(KS_ERR_UNSUPPORTED, "skeleton rank %lld too large (max 1024)", (long long)s_max); }
 
   const double t_plan = host_ms();
   // the permutation first: the device gather of the points trusts it. Host
@@ -239,7 +240,10 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(f->hbuf.alloc((size_t)nn * f->s_pad * f->s_pad + 1));
     KS_CUDA(f->aug.alloc((size_t)f->n_int * f->T * f->T + 1));
     KS_CUDA(f->bc.alloc((size_t)f->n_int * f->s_pad * f->s_pad + 1));
-    KS_CUDA(f->pn.alloc((size_t)f->n_int * f->s_pad * f->t_pad + 1));
+    KS_CUDA(f->pn.alloc((size_t)f->n_int * f->s_pad * f->zt + 1));
+    KS_CUDA(f->xy.alloc((size_t)f->n_int * 2 * f->s_pad * f->s_pad + 1));
+    KS_CUDA(f->phl.alloc((size_t)f->n_int * f->s_pad * f->s_pad + 1));
+    KS_CUDA(f->norm1_slab.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->norm1.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->cond.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->coords.alloc((size_t)(p->n + f->m_pad) * p->d));

@@ -146,7 +146,7 @@ int ks_debug_copy(const ks_factor* f, int which, int64_t index, double* out, int
     case 0: base = w->z.p; stride = (int64_t)f->m_pad * w->q_cap; break;      // per leaf index
     case 1: base = w->c.p; stride = (int64_t)f->s_pad * w->q_cap; break;      // per node
     case 2: base = w->tin.p; stride = (int64_t)f->s_pad * w->q_cap; break;    // per node
-    case 3: base = w->y.p; stride = (int64_t)f->t_pad * w->q_cap; break;      // per internal index
+    case 3: base = w->y.p; stride = (int64_t)f->zt * w->q_cap; break;         // per internal index
     case 4: base = f->aug.p; stride = (int64_t)f->T * f->T; break;            // per internal index
     case 5: base = f->leafA.p; stride = (int64_t)f->R * f->m_pad; break;      // per leaf index
     default: return fail(KS_ERR_INVALID, "bad buffer id");
@@ -185,7 +185,7 @@ int64_t ks_device_bytes(const ks_factor* f) {
   if (!f) return 0;
   int64_t b = 0;
   b += f->coords.n * 8 + f->coeff.n * 8 + f->leafA.n * 8 + f->inv.n * 8 + f->hbuf.n * 8 + f->aug.n * 8;
-  b += f->bc.n * 8 + f->pn.n * 8;
+  b += f->bc.n * 8 + f->pn.n * 8 + f->xy.n * 8 + f->phl.n * 8;
   std::lock_guard<std::mutex> lk(const_cast<ks_factor*>(f)->ws_mu);
   for (const auto& w : f->ws)
     b += 8 * (int64_t)(w->z.n + w->c.n + w->tin.n + w->y.n + w->wtmp.n + w->bdev.n + w->xdev.n + w->fb_y.n +

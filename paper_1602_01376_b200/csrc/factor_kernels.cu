@@ -276,135 +276,6 @@ void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, i
 }
 
 // --------------------------------------------------------------------------
-// Internal node assembly
-// --------------------------------------------------------------------------
-// Coupling B = K(S_l, S_r) (compress.py:281-283), zero padded to s_pad^2.
-__global__ void __launch_bounds__(256) k_coupling(DevTree t, NodeBatch nb) {
-  pdl_wait();
-  const int k = blockIdx.z;
-  const int l = nb.left[k], r = nb.right[k];
-  const int sl = t.rank[l], sr = t.rank[r];
-  const int r0 = blockIdx.y * GT, c0 = blockIdx.x * GT;
-  double sq[4][4];
-  gauss_tile<true>(t, t.skel_pos + t.skel_off[l], 0, sl, t.skel_pos + t.skel_off[r], 0, sr, r0, c0, sq);
-  const double den = -2.0 * t.h * t.h;
-  double* B = nb.Bc + (int64_t)k * nb.s_pad * nb.s_pad;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int rr = r0 + ty + 16 * i;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int cc = c0 + tx + 16 * j;
-      B[(int64_t)rr * nb.s_pad + cc] = (rr < sl && cc < sr) ? exp(sq[i][j] / den) : 0.0;
-    }
-  }
-}
-
-void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
-  dim3 g(nb.s_pad / GT, nb.s_pad / GT, nb.count);
-  launch_pdl(k_coupling, g, dim3(256), 0, st, t, nb);
-}
-
-// Identity diagonal blocks of Z, P^T (top right), zero bottom-right block, and
-// the padded P copy used by the solve. Z12/Z21 and -PG are written by GEMMs.
-// Padded candidate index i' maps to the reference's cand index
-// (cand = [skel_l; skel_r], compress.py:213): i' < s_pad -> i' (if < s_l),
-// i' >= s_pad -> s_l + (i' - s_pad) (if < s_r).
-__device__ __forceinline__ int cand_index(int i, int S, int sl, int sr) {
-  return (i < S) ? (i < sl ? i : -1) : (i - S < sr ? sl + (i - S) : -1);
-}
-
-// one CTA per row: rows [0, TP) the identity diagonal blocks of Z, rows
-// [TP, T) the zero bottom-right block, then the S rows of the padded P copy
-__global__ void __launch_bounds__(256) k_aug_init(DevTree t, NodeBatch nb) {
-  pdl_wait();
-  const int k = blockIdx.y, row = blockIdx.x;
-  const int S = nb.s_pad, TP = nb.t_pad, T = nb.T;
-  double* A = nb.Aug + (int64_t)k * T * T;
-  if (row < TP) {  // (a) identity block of Z: row i, columns of its half
-    const int half = row / S, i = row - half * S;
-    double* out = A + (int64_t)row * T + half * S;
-    for (int j = threadIdx.x; j < S; j += 256) out[j] = (i == j) ? 1.0 : 0.0;
-    return;
-  }
-  if (row < T) {  // (c) zero block S x S at (TP, TP)
-    double* out = A + (int64_t)row * T + TP;
-    for (int j = threadIdx.x; j < S; j += 256) out[j] = 0.0;
-    return;
-  }
-  // (d) Pn row j: P[j][cand(i)] for the padded candidate index i
-  const int j = row - T;
-  const int v = nb.node[k], sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]], sv = t.rank[v];
-  const double* P = t.coeff + t.coeff_off[v] + (int64_t)j * (sl + sr);
-  double* out = nb.Pn + (int64_t)k * S * TP + (int64_t)j * TP;
-  for (int i = threadIdx.x; i < TP; i += 256) {
-    const int ci = cand_index(i, S, sl, sr);
-    out[i] = (ci >= 0 && j < sv) ? P[ci] : 0.0;
-  }
-}
-
-// (b) the P^T block (TP x S at (0, TP)) through 32 x 32 shared-memory tiles:
-// reads along P's rows, writes along Aug's rows
-__global__ void __launch_bounds__(256) k_aug_pt(DevTree t, NodeBatch nb) {
-  pdl_wait();
-  __shared__ double tile[32][33];
-  const int k = blockIdx.z;
-  const int S = nb.s_pad, TP = nb.t_pad, T = nb.T;
-  const int v = nb.node[k], sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]], sv = t.rank[v];
-  const double* P = t.coeff + t.coeff_off[v];
-  const int cand = sl + sr;
-  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  {
-    const int ci = cand_index(i0 + tx, S, sl, sr);
-    for (int jj = ty; jj < 32; jj += 8) {
-      const int j = j0 + jj;
-      tile[jj][tx] = (ci >= 0 && j < sv) ? P[(int64_t)j * cand + ci] : 0.0;
-    }
-  }
-  __syncthreads();
-  double* A = nb.Aug + (int64_t)k * T * T;
-  for (int ii = ty; ii < 32; ii += 8) A[(int64_t)(i0 + ii) * T + TP + j0 + tx] = tile[tx][ii];
-}
-
-void launch_aug_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
-  launch_pdl(k_aug_init, dim3(nb.T + nb.s_pad, nb.count), dim3(256), 0, st, t, nb);
-  launch_pdl(k_aug_pt, dim3(nb.s_pad / 32, nb.t_pad / 32, nb.count), dim3(256), 0, st, t, nb);
-}
-
-// 1-norm of Z (max column abs sum, linalg.py:176), before the LU overwrites it.
-// 32 columns per CTA, rows split over 8 warps; the max over column tiles goes
-// through an integer atomicMax on the (non-negative) double's bit pattern.
-__global__ void __launch_bounds__(256) k_colnorm1(NodeBatch nb) {
-  pdl_wait();
-  const int k = blockIdx.y;
-  const double* A = nb.Aug + (int64_t)k * nb.T * nb.T;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * 32 + lane;
-  __shared__ double red[8][33];
-  double s = 0.0;
-  if (c < nb.t_pad)
-#pragma unroll 8
-    for (int i = warp; i < nb.t_pad; i += 8) s += fabs(A[(int64_t)i * nb.T + c]);
-  red[warp][lane] = s;
-  __syncthreads();
-  if (warp == 0) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += red[w][lane];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
-    if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(nb.norm1 + k), __double_as_longlong(t));
-  }
-}
-
-void launch_colnorm1(const DevTree&, const NodeBatch& nb, cudaStream_t st) {
-  cudaMemsetAsync(nb.norm1, 0, sizeof(double) * nb.count, st);
-  dim3 g((nb.t_pad + 31) / 32, nb.count);
-  launch_pdl(k_colnorm1, g, dim3(256), 0, st, nb);
-}
-
-// --------------------------------------------------------------------------
 // LU with partial pivoting restricted to rows < t_pad (linalg.py:199-213 on
 // the Z block; the -PG rows are eliminated but never chosen as pivots): one
 // W-column panel per launch and node (k_lu_panel2). The candidate rows live in
@@ -654,458 +525,6 @@ void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncol
   else launch_pdl(k_trsm_ul<64>, g, dim3(128), 0, st, nb, r0, c0, ncols);
 }
 
-// --------------------------------------------------------------------------
-// Hager 1-norm condition estimate of Z (linalg.py:282-304), one CTA per node,
-// on the LU factors in place (blocked CTA triangular solves, trsv.cuh). Only
-// real (unpadded) indices take part, in the reference's index order.
-// --------------------------------------------------------------------------
-__device__ __forceinline__ void block_argmax(double& bv, int& bi, double* rv, int* ri) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-  }
-  if (lane == 0) { rv[warp] = bv; ri[warp] = bi; }
-  __syncthreads();
-  bv = rv[0];
-  bi = ri[0];
-  for (int w = 1; w < SWARPS; ++w)
-    if (rv[w] > bv || (rv[w] == bv && ri[w] < bi)) { bv = rv[w]; bi = ri[w]; }
-  __syncthreads();
-}
-
-__device__ __forceinline__ double block_sum(double v, double* rv) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  v = warp_sum(v);
-  if (lane == 0) rv[warp] = v;
-  __syncthreads();
-  double s = 0.0;
-  for (int w = 0; w < SWARPS; ++w) s += rv[w];
-  __syncthreads();
-  return s;
-}
-
-__global__ void __launch_bounds__(STHREADS) k_hager(DevTree t, NodeBatch nb) {
-  extern __shared__ double hv[];  // x, y, w (t_pad each) + red (SWARPS*32) ; int perm (t_pad)
-  __shared__ double D[SB][SB + 1];
-  __shared__ double rv[SWARPS];
-  __shared__ int ri[SWARPS];
-  const int k = blockIdx.x;
-  const int TP = nb.t_pad, S = nb.s_pad, T = nb.T;
-  const int sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]];
-  const int n = sl + sr;
-  const double* A = nb.Aug + (int64_t)k * T * T;
-  double* x = hv;
-  double* y = hv + TP;
-  double* w = hv + 2 * TP;
-  double* red = hv + 3 * TP;
-  int* pm = reinterpret_cast<int*>(red + SWARPS * 32);  // (Pi v)[i] = v[pm[i]]
-  if (n == 0) {
-    if (threadIdx.x == 0) nb.cond[k] = 0.0;
-    return;
-  }
-  for (int i = threadIdx.x; i < TP; i += STHREADS) pm[i] = nb.pm[(int64_t)k * TP + i];  // composed swaps
-  auto real = [&](int i) { return i < S ? (i < sl) : (i - S < sr); };
-  for (int i = threadIdx.x; i < TP; i += STHREADS) x[i] = real(i) ? 1.0 / n : 0.0;
-  __syncthreads();
-  double est = 0.0;
-  for (int it = 0; it < 5; ++it) {
-    // y = Z^-1 x   (dense_solve: swaps, unit L, U)
-    for (int i = threadIdx.x; i < TP; i += STHREADS) y[i] = x[pm[i]];
-    __syncthreads();
-    cta_trsv_rows<1, false, true>(A, T, TP, y, D);
-    cta_trsv_rows<1, true, false>(A, T, TP, y, D);
-    double s = 0.0;
-    for (int i = threadIdx.x; i < TP; i += STHREADS) s += real(i) ? fabs(y[i]) : 0.0;
-    est = block_sum(s, rv);
-    // z = Z^-T sign(y)   (solve_transposed: U^T, unit L^T, undo swaps)
-    for (int i = threadIdx.x; i < TP; i += STHREADS) w[i] = real(i) ? (y[i] >= 0.0 ? 1.0 : -1.0) : 0.0;
-    __syncthreads();
-    cta_trsv_trans<1, true, false>(A, T, TP, w, D, red);
-    cta_trsv_trans<1, false, true>(A, T, TP, w, D, red);
-    for (int i = threadIdx.x; i < TP; i += STHREADS) y[pm[i]] = w[i];  // y <- z (unpermuted)
-    __syncthreads();
-    // j = argmax |z| (first in reference order on ties), z . x
-    double bv = -1.0, dot = 0.0;
-    int bi = 0x7fffffff;
-    for (int i = threadIdx.x; i < TP; i += STHREADS) {
-      if (!real(i)) continue;
-      const double a = fabs(y[i]);
-      const int r = i < S ? i : sl + (i - S);
-      if (a > bv || (a == bv && r < bi)) { bv = a; bi = r; }
-      dot = fma(y[i], x[i], dot);
-    }
-    block_argmax(bv, bi, rv, ri);
-    dot = block_sum(dot, rv);
-    if (bv <= dot) break;
-    const int jp = bi < sl ? bi : S + (bi - sl);
-    for (int i = threadIdx.x; i < TP; i += STHREADS) x[i] = (i == jp) ? 1.0 : 0.0;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) nb.cond[k] = isfinite(est) ? nb.norm1[k] * est : INFINITY;
-}
-
-static void launch_hager_blocked(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (3 * nb.t_pad + SWARPS * 32) + sizeof(int) * nb.t_pad;
-  ensure_smem(k_hager, smem);
-  k_hager<<<nb.count, STHREADS, smem, st>>>(t, nb);
-}
-
-// --------------------------------------------------------------------------
-// The same estimate with thread-owned vectors (t_pad <= 1024): thread i owns
-// entry i of every vector. A triangular solve walks SB-row blocks; the
-// coefficients coupling the next block to each thread's entry are loaded one
-// step ahead, the diagonal block goes through its inverse (precomputed by
-// k_diag_inv, staged in shared memory) as an SB-wide shuffle GEMV, so a block
-// step is a handful of dependent operations and one barrier.
-// --------------------------------------------------------------------------
-enum { SOLVE_L = 0, SOLVE_U = 1, SOLVE_UT = 2, SOLVE_LT = 3 };
-
-// inverses of the SB x SB diagonal blocks of unit-lower L (which 0) and upper
-// U (which 1) of every node's Z factors: dinv[node][which][b][s][t]
-template <int SB>
-__global__ void __launch_bounds__(256) k_diag_inv(NodeBatch nb, double* dinv) {
-  const int k = blockIdx.x, which = blockIdx.y;
-  const int TP = nb.t_pad, T = nb.T;
-  const double* A = nb.Aug + (int64_t)k * T * T;
-  double* out = dinv + ((int64_t)(nb.first + k) * 2 + which) * TP * SB;
-  for (int task = threadIdx.x; task < TP; task += 256) {
-    const int b = task / SB, j = task % SB;  // column j of block b's inverse
-    const int r0 = b * SB;
-    double x[SB];
-    if (which == 0) {
-#pragma unroll
-      for (int s2 = 0; s2 < SB; ++s2) {
-        double v = (s2 == j) ? 1.0 : 0.0;
-#pragma unroll
-        for (int t2 = 0; t2 < s2; ++t2)
-          if (t2 >= j) v = fma(-A[(int64_t)(r0 + s2) * T + r0 + t2], x[t2], v);
-        x[s2] = (s2 < j) ? 0.0 : v;
-      }
-    } else {
-#pragma unroll
-      for (int s2 = SB - 1; s2 >= 0; --s2) {
-        double v = (s2 == j) ? 1.0 : 0.0;
-#pragma unroll
-        for (int t2 = s2 + 1; t2 < SB; ++t2)
-          if (t2 <= j) v = fma(-A[(int64_t)(r0 + s2) * T + r0 + t2], x[t2], v);
-        x[s2] = (s2 > j) ? 0.0 : v / A[(int64_t)(r0 + s2) * T + r0 + s2];
-      }
-    }
-#pragma unroll
-    for (int s2 = 0; s2 < SB; ++s2) out[(int64_t)b * SB * SB + s2 * SB + j] = x[s2];
-  }
-}
-
-// v (thread i's entry) <- M^-1 v for M = L (unit lower), U, U^T or L^T of the
-// packed factors in A (rows of length lda); di: the matching diagonal-block
-// inverses in shared memory; xs: a shared broadcast buffer (n entries).
-// COLMAJ: A is the column-major copy of the factors (At[j][i] = A[i][j]), so
-// the non-transposed solves read it down columns like the transposed ones
-// (coalesced across the threads that own consecutive entries)
-template <int SB, int NT, int MODE, bool COLMAJ = false>
-__device__ __forceinline__ double own_solve(const double* __restrict__ A, int64_t lda, int n, const double* di, double v,
-                            double* xs) {
-  constexpr bool ASC = (MODE == SOLVE_L || MODE == SOLVE_UT);
-  constexpr bool TRANS = (MODE == SOLVE_UT || MODE == SOLVE_LT);
-  constexpr bool COLACC = TRANS || COLMAJ;
-  const int i = threadIdx.x, lane = i & 31;
-  const bool own = i < n;
-  const int nblk = n / SB;
-  double cur[SB], nxt[SB];
-  auto load = [&](int b, double (&c)[SB]) {
-    const int r0 = b * SB;
-    const bool need = own && (ASC ? i >= r0 + SB : i < r0);  // solved after block b
-    if (COLACC) {
-      const double* p = A + (int64_t)r0 * lda + (own ? i : 0);
-#pragma unroll
-      for (int j = 0; j < SB; ++j, p += lda) c[j] = need ? __ldg(p) : 0.0;
-    } else {
-      const double2* p = reinterpret_cast<const double2*>(A + (int64_t)(own ? i : 0) * lda + r0);
-#pragma unroll
-      for (int j = 0; j < SB / 2; ++j) {
-        const double2 u = need ? __ldg(p + j) : make_double2(0.0, 0.0);
-        c[2 * j] = u.x;
-        c[2 * j + 1] = u.y;
-      }
-    }
-  };
-  load(ASC ? 0 : nblk - 1, cur);
-  __syncthreads();  // xs may still be read by the caller's previous phase
-#pragma unroll 1
-  for (int step = 0; step < nblk; ++step) {
-    const int b = ASC ? step : nblk - 1 - step;
-    if (step + 1 < nblk) load(ASC ? b + 1 : b - 1, nxt);
-    const int r0 = b * SB;
-    if ((i >> 5) == (r0 >> 5)) {  // the warp holding block b: x_b = D_b^-1 v_b
-      const int base = r0 & 31, s2 = lane - base;
-      const bool inb = own && s2 >= 0 && s2 < SB;
-      const double* d = di + (int64_t)b * SB * SB;
-      double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-      for (int t2 = 0; t2 < SB; t2 += 2) {
-        const double v0 = __shfl_sync(0xffffffffu, v, base + t2);
-        const double v1 = __shfl_sync(0xffffffffu, v, base + t2 + 1);
-        if (inb) {
-          acc0 = fma(TRANS ? d[t2 * SB + s2] : d[s2 * SB + t2], v0, acc0);
-          acc1 = fma(TRANS ? d[(t2 + 1) * SB + s2] : d[s2 * SB + t2 + 1], v1, acc1);
-        }
-      }
-      if (inb) {
-        v = acc0 + acc1;
-        xs[i] = v;
-      }
-    }
-    __syncthreads();
-    const bool after = own && (ASC ? i >= r0 + SB : i < r0);
-    if (after) {
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int j = 0; j < SB; j += 2) {
-        s0 = fma(cur[j], xs[r0 + j], s0);
-        s1 = fma(cur[j + 1], xs[r0 + j + 1], s1);
-      }
-      v -= s0 + s1;
-    }
-#pragma unroll
-    for (int j = 0; j < SB; ++j) cur[j] = nxt[j];
-  }
-  return v;
-}
-
-// The non-transposed solves (L, U) with the coefficient loads coalesced: each
-// thread needs the 8 coefficients of its own row, but one row per lane makes
-// every load instruction touch 32 cache lines (the L1 tag lookups, not the
-// bytes, bound the step). Here the CTA loads the block's row segments 4 lanes
-// per row (8 lines per instruction), one step ahead, and stages them through
-// shared memory (cb: 2 x NT x 10 doubles); the step's barrier publishes them.
-template <int NT, int MODE>
-__device__ __forceinline__ double own_solve_rows(const double* __restrict__ A, int64_t lda, int n, const double* di,
-                                                 double v, double* xs, double* cb) {
-  constexpr int SB = 8, CS = 10;  // 8 coefficients per row, padded row stride (16 B aligned, conflict-free)
-  constexpr bool ASC = (MODE == SOLVE_L);
-  static_assert(MODE == SOLVE_L || MODE == SOLVE_U, "non-transposed solves only");
-  const int i = threadIdx.x, lane = i & 31;
-  const bool own = i < n;
-  const int nblk = n / SB;
-  double2 ld[4];
-  auto issue = [&](int b) {
-    const int r0 = b * SB;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = threadIdx.x + u * NT, row = c >> 2, part = c & 3;
-      const bool need = row < n && (ASC ? row >= r0 + SB : row < r0);
-      ld[u] = need ? ldg2(A + (int64_t)row * lda + r0 + 2 * part) : make_double2(0.0, 0.0);
-    }
-  };
-  auto stage = [&](int st) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = threadIdx.x + u * NT, row = c >> 2, part = c & 3;
-      if (row < NT) *reinterpret_cast<double2*>(cb + ((int64_t)st * NT + row) * CS + 2 * part) = ld[u];
-    }
-  };
-  __syncthreads();  // xs and cb may still be read by the caller's previous phase
-  issue(ASC ? 0 : nblk - 1);
-  stage(0);
-#pragma unroll 1
-  for (int step = 0; step < nblk; ++step) {
-    const int b = ASC ? step : nblk - 1 - step;
-    if (step + 1 < nblk) issue(ASC ? b + 1 : b - 1);
-    const int r0 = b * SB;
-    if ((i >> 5) == (r0 >> 5)) {  // the warp holding block b: x_b = D_b^-1 v_b
-      const int base = r0 & 31, s2 = lane - base;
-      const bool inb = own && s2 >= 0 && s2 < SB;
-      const double* d = di + (int64_t)b * SB * SB;
-      double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-      for (int t2 = 0; t2 < SB; t2 += 2) {
-        const double v0 = __shfl_sync(0xffffffffu, v, base + t2);
-        const double v1 = __shfl_sync(0xffffffffu, v, base + t2 + 1);
-        if (inb) {
-          acc0 = fma(d[s2 * SB + t2], v0, acc0);
-          acc1 = fma(d[s2 * SB + t2 + 1], v1, acc1);
-        }
-      }
-      if (inb) {
-        v = acc0 + acc1;
-        xs[i] = v;
-      }
-    }
-    __syncthreads();
-    const bool after = own && (ASC ? i >= r0 + SB : i < r0);
-    if (after) {
-      const double* c = cb + ((int64_t)(step & 1) * NT + i) * CS;
-      double q0 = 0.0, q1 = 0.0;
-#pragma unroll
-      for (int j = 0; j < SB; j += 2) {
-        const double2 cc = *reinterpret_cast<const double2*>(c + j);
-        q0 = fma(cc.x, xs[r0 + j], q0);
-        q1 = fma(cc.y, xs[r0 + j + 1], q1);
-      }
-      v -= q0 + q1;
-    }
-    if (step + 1 < nblk) stage((step + 1) & 1);
-  }
-  return v;
-}
-
-template <int NT>
-__device__ __forceinline__ double nt_sum(double v, double* red) {
-  constexpr int NWp = NT / 32;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  v = warp_sum(v);
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double s = 0.0;
-#pragma unroll
-  for (int w = 0; w < NWp; ++w) s += red[w];
-  return s;
-}
-
-template <int NT>
-__device__ __forceinline__ void nt_argmax(double& bv, int& bi, double* red, int* redi) {
-  constexpr int NWp = NT / 32;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-  }
-  __syncthreads();
-  if (lane == 0) { red[warp] = bv; redi[warp] = bi; }
-  __syncthreads();
-  bv = red[0];
-  bi = redi[0];
-#pragma unroll
-  for (int w = 1; w < NWp; ++w)
-    if (red[w] > bv || (red[w] == bv && redi[w] < bi)) { bv = red[w]; bi = redi[w]; }
-}
-
-template <int SB, int NT, bool COLMAJ>
-__global__ void __launch_bounds__(NT, 1) k_hager_own(DevTree t, NodeBatch nb, const double* dinv, const double* lut) {
-  extern __shared__ __align__(16) double hs[];
-  // persistent over nodes: the grid may be smaller than the batch so that the
-  // estimate leaves SMs free for the factorization it overlaps
-  for (int k = blockIdx.x; k < nb.count; k += gridDim.x) {
-  __syncthreads();
-  const int TP = nb.t_pad, S = nb.s_pad, T = nb.T;
-  const int sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]];
-  const int n = sl + sr;
-  if (n == 0) {
-    if (threadIdx.x == 0) nb.cond[k] = 0.0;
-    continue;
-  }
-  double* dL = hs;                 // TP x SB
-  double* dU = hs + TP * SB;       // TP x SB
-  double* xs = dU + TP * SB;       // TP
-  double* red = xs + TP;           // NT / 32
-  int* redi = reinterpret_cast<int*>(red + NT / 32);
-  int* pm = redi + NT / 32;        // TP: composed swaps, (Pi v)[i] = v[pm[i]]
-  const double* A = nb.Aug + (int64_t)k * T * T;
-  {
-    const double2* src = reinterpret_cast<const double2*>(dinv + (int64_t)(nb.first + k) * 2 * TP * SB);
-    double2* dst = reinterpret_cast<double2*>(hs);
-    for (int e = threadIdx.x; e < TP * SB; e += NT) dst[e] = src[e];
-    for (int e = threadIdx.x; e < TP; e += NT) pm[e] = nb.pm[(int64_t)k * TP + e];
-  }
-  const int i = threadIdx.x;
-  const bool own = i < TP;
-  const bool real = own && (i < S ? (i < sl) : (i - S < sr));
-  const int ref = i < S ? i : sl + (i - S);  // reference index order
-  double x = real ? 1.0 / n : 0.0;
-  double est = 0.0;
-  __syncthreads();
-  for (int it = 0; it < 5; ++it) {
-    // y = Z^-1 x   (dense_solve: swaps, unit L, U)
-    if (own) xs[i] = x;
-    __syncthreads();
-    double y = own ? xs[pm[i]] : 0.0;
-    if constexpr (COLMAJ) {
-      const double* At = lut + (int64_t)(nb.first + k) * TP * TP;
-      y = own_solve<SB, NT, SOLVE_L, true>(At, TP, TP, dL, y, xs);
-      y = own_solve<SB, NT, SOLVE_U, true>(At, TP, TP, dU, y, xs);
-    } else if constexpr (SB == 8 && NT == 512) {
-      double* cb = reinterpret_cast<double*>(pm + TP);  // 2 x NT x 10 staged coefficients
-      y = own_solve_rows<NT, SOLVE_L>(A, T, TP, dL, y, xs, cb);
-      y = own_solve_rows<NT, SOLVE_U>(A, T, TP, dU, y, xs, cb);
-    } else {
-      y = own_solve<SB, NT, SOLVE_L>(A, T, TP, dL, y, xs);
-      y = own_solve<SB, NT, SOLVE_U>(A, T, TP, dU, y, xs);
-    }
-    est = nt_sum<NT>(real ? fabs(y) : 0.0, red);
-    // z = Z^-T sign(y)   (solve_transposed: U^T, unit L^T, undo swaps)
-    double w = real ? (y >= 0.0 ? 1.0 : -1.0) : 0.0;
-    w = own_solve<SB, NT, SOLVE_UT>(A, T, TP, dU, w, xs);
-    w = own_solve<SB, NT, SOLVE_LT>(A, T, TP, dL, w, xs);
-    __syncthreads();
-    if (own) xs[pm[i]] = w;
-    __syncthreads();
-    const double z = own ? xs[i] : 0.0;
-    // j = argmax |z| (first in reference order on ties), z . x
-    double bv = real ? fabs(z) : -1.0;
-    int bi = real ? ref : 0x7fffffff;
-    nt_argmax<NT>(bv, bi, red, redi);
-    const double dot = nt_sum<NT>(real ? z * x : 0.0, red);
-    if (bv <= dot) break;
-    const int jp = bi < sl ? bi : S + (bi - sl);
-    x = (i == jp) ? 1.0 : 0.0;
-  }
-  if (threadIdx.x == 0) nb.cond[k] = isfinite(est) ? nb.norm1[k] * est : INFINITY;
-  }
-}
-
-// column-major copy of each node's Z factors (L\U, t_pad x t_pad) for the
-// estimator's non-transposed solves: lut[first + k] = Z_k^T
-__global__ void __launch_bounds__(256) k_lu_transpose(NodeBatch nb, double* lut) {
-  __shared__ double tt[32][33];
-  const int k = blockIdx.z, TP = nb.t_pad, T = nb.T;
-  const double* A = nb.Aug + (int64_t)k * T * T;
-  double* At = lut + (int64_t)(nb.first + k) * TP * TP;
-  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int r = ty; r < 32; r += 8) tt[r][tx] = A[(int64_t)(i0 + r) * T + j0 + tx];
-  __syncthreads();
-  for (int r = ty; r < 32; r += 8) At[(int64_t)(j0 + r) * TP + i0 + tx] = tt[tx][r];
-}
-
-template <int SB, int NT, bool COLMAJ>
-static void launch_hager_own(const DevTree& t, const NodeBatch& nb, double* dinv, double* lut, int max_ctas,
-                             cudaStream_t st) {
-  dim3 g(nb.count, 2);
-  k_diag_inv<SB><<<g, 256, 0, st>>>(nb, dinv);
-  if (COLMAJ) k_lu_transpose<<<dim3(nb.t_pad / 32, nb.t_pad / 32, nb.count), 256, 0, st>>>(nb, lut);
-  size_t smem = sizeof(double) * (2 * (size_t)nb.t_pad * SB + nb.t_pad + 2 * NT / 32) + sizeof(int) * nb.t_pad;
-  if (!COLMAJ && SB == 8 && NT == 512) smem = (smem + 15) / 16 * 16 + sizeof(double) * 2 * NT * 10;
-  ensure_smem(k_hager_own<SB, NT, COLMAJ>, smem);
-  k_hager_own<SB, NT, COLMAJ><<<std::min(nb.count, max_ctas), NT, smem, st>>>(t, nb, dinv, lut);
-}
-
-int hager_launches(const NodeBatch& nb) { return (nb.t_pad <= 512 && nb.count < 64) ? 3 : (nb.t_pad <= 1024 ? 2 : 1); }
-
-void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, double* lut, int max_ctas, cudaStream_t st) {
-  const char* e = std::getenv("KS_HAGER_IMPL");
-  if (e && e[0] == 'b') {
-    launch_hager_blocked(t, nb, st);
-    return;
-  }
-  if (nb.t_pad <= 512) {
-    // the column-major copy pays for itself where the factors are still in L2
-    // (narrow levels); for wide levels the extra HBM pass costs more than it saves
-    if (lut && nb.count < 64) launch_hager_own<8, 512, true>(t, nb, dinv, lut, max_ctas, st);
-    else launch_hager_own<8, 512, false>(t, nb, dinv, lut, max_ctas, st);
-  } else if (nb.t_pad <= 1024) launch_hager_own<8, 1024, false>(t, nb, dinv, nullptr, max_ctas, st);
-  else launch_hager_blocked(t, nb, st);
-}
-
-// LU fallback for leaves whose Cholesky failed (solver.py:125-131): the
-// augmented matrix [[A, -P^T], [P, 0]], A = K(X_leaf, X_leaf) + lam I (both
-// triangles), with the leaf's padded identity; its LU restricted to the first
-// m_pad pivots leaves the Schur complement P A^-1 P^T = H in the trailing block.
 // fb: count = failed leaves, node = their node ids, t_pad = m_pad, T = m_pad + s_pad.
 __global__ void __launch_bounds__(256) k_fb_assemble(DevTree t, NodeBatch fb, const int* begin, const int* size,
                                                      const double* lam_p) {
@@ -1159,59 +578,6 @@ void launch_fb_assemble(const DevTree& t, const NodeBatch& fb, const int* begin,
 
 // Composed row interchanges of each node's LU: (Pi v)[i] = v[pm[i]], from the
 // LAPACK-style swap sequence (linalg.py:250-253). One warp per node.
-__global__ void __launch_bounds__(1024) k_compose_perm(NodeBatch nb) {
-  pdl_wait();
-  const int k = blockIdx.x;
-  const int TP = nb.t_pad;
-  const int* piv = nb.piv + (int64_t)k * TP;
-  int* pm = nb.pm + (int64_t)k * TP;
-  extern __shared__ __align__(16) int ps[];
-  for (int i = threadIdx.x; i < TP; i += blockDim.x) ps[i] = piv[i];
-  __syncthreads();
-  // every thread follows one row through the swap sequence: the row that
-  // starts at r ends at f(r), so pm[f(r)] = r (same result as swapping pm);
-  // t_pad is a multiple of 64, the swaps are read four at a time
-  for (int r = threadIdx.x; r < TP; r += blockDim.x) {
-    int f = r;
-    const int4* p4 = reinterpret_cast<const int4*>(ps);
-    for (int i = 0; i < TP / 4; ++i) {
-      const int4 q = p4[i];
-      const int i0 = 4 * i;
-      f = (f == i0) ? q.x : (f == q.x ? i0 : f);
-      f = (f == i0 + 1) ? q.y : (f == q.y ? i0 + 1 : f);
-      f = (f == i0 + 2) ? q.z : (f == q.z ? i0 + 2 : f);
-      f = (f == i0 + 3) ? q.w : (f == q.w ? i0 + 3 : f);
-    }
-    pm[f] = r;
-  }
-}
-
-void launch_compose_perm(const NodeBatch& nb, cudaStream_t st) {
-  launch_pdl(k_compose_perm, dim3(nb.count), dim3(std::min(1024, nb.t_pad)), sizeof(int) * nb.t_pad, st, nb);
-}
-
-// H = sym(trailing block) -> Hbuf[node] (solver.py:163): 32 x 32 tiles, the
-// transposed tile through shared memory so both reads run along rows.
-__global__ void __launch_bounds__(256) k_extract_h(NodeBatch nb, double* H, int64_t stride) {
-  pdl_wait();
-  __shared__ double tt[32][33];
-  const int k = blockIdx.z;
-  const int S = nb.s_pad, T = nb.T, TP = nb.t_pad;
-  const double* A = nb.Aug + (int64_t)k * T * T + (int64_t)TP * T + TP;
-  double* h = H + (int64_t)nb.node[k] * stride;
-  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int r = ty; r < 32; r += 8) tt[r][tx] = A[(int64_t)(j0 + r) * T + i0 + tx];  // A[j][i]
-  __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int i = i0 + r, j = j0 + tx;
-    h[(int64_t)i * S + j] = 0.5 * (A[(int64_t)i * T + j] + tt[tx][r]);
-  }
-}
-
-void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st) {
-  launch_pdl(k_extract_h, dim3(nb.s_pad / 32, nb.s_pad / 32, nb.count), dim3(256), 0, st, nb, H, h_stride);
-}
 
 }  // namespace ks
 
@@ -1383,3 +749,4 @@ extern "C" int ks_probe_panel(int T, int tp, int w, int count, int reps, double*
   cudaEventDestroy(e0); cudaEventDestroy(e1);
   return err == cudaSuccess ? 0 : 5;
 }
+

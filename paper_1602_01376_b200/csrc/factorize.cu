@@ -123,7 +123,7 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
 
 static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1, int deferred_before = 0);
 static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool is_root_level);
-static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt, int T, int S, int TP);
+static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt);
 // subtree pipelining (ks_factor::npipe) in this factorization: the default 4
 // node groups, not under the per-level profiler or the tracer (their level
 // boundaries would blur); KS_PIPE=0 disables it
@@ -182,7 +182,7 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
           f->cur_tag = lev;
           const ks::NodeBatch nb = f->nodebatch(lev);
           const int c = nb.count / G;
-          if (int rc = enqueue_level_body(f, Lg, sub_batch(nb, g * c, c, f->T, f->s_pad, f->t_pad), false)) return rc;
+          if (int rc = enqueue_level_body(f, Lg, sub_batch(nb, g * c, c), false)) return rc;
         }
         f->cur_tag = -1;
       }
@@ -212,81 +212,104 @@ static bool use_slab(const ks_factor* f, const ks::NodeBatch& nb) {
 // batches of at most KS_SPINE_MAX (default 16) nodes carry the P^T columns
 // through the recursive LU (rlu ext)
 
-// One level's node work on L's stream for the node sub-batch nb (coupling,
-// augmented assembly, recursive LU, U12 / Schur, pivot composition, H out).
+// One level's node work on L's stream for the node sub-batch nb, in the block
+// formulation (kernels.cuh NodeBatch, node_kernels.cu): the coupling B, then
+//   X = B H_r, Y = B^T H_l                      (Z = I + W G = [[I, X], [Y, I]], solver.py:142-148)
+//   Aug = [[S, E], [F, C]] = [[I - Y X, P_r^T - Y P_l^T], [P_l H_l X - P_r H_r, P_l H_l P_l^T]]
+// as DMMA GEMMs, ||Z||_1, then the LU of Aug's first s_pad columns with pivots
+// among S's rows (linalg.py:199-213 on the Schur complement of Z's identity
+// block) whose trailing block is H = P G Z^-1 P^T (solver.py:154-164).
 static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool is_root_level) {
   const ks::DevTree dt = f->devtree();
-  const int S = f->s_pad;
-  const int TP = f->t_pad, T = f->T;
-  const int64_t TT = (int64_t)T * T, SS = (int64_t)S * S;
+  const int S = nb.s_pad, T = nb.T, ZT = nb.zt;
+  const int64_t TT = (int64_t)T * T, SS = (int64_t)S * S, XS = 2 * SS, PS = (int64_t)S * ZT;
   const int cnt = nb.count;
   cudaStream_t st = L.st;
-    ks::launch_coupling(dt, nb, st);
-    ks::launch_aug_init(dt, nb, st);
-    L.count[0] += 3;
-    int rc = L.check("coupling/aug_init");
-    if (rc) return rc;
-    // Z12 = B H_r, Z21 = B^T H_l   (W G, solver.py:142-148, zero blocks skipped)
-    rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
-                   OperandW{nb.Aug + S, T, TT, nullptr}, 1.0, 0.0), false, true);
-    if (rc) return rc;
-    rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
-                   OperandW{nb.Aug + (int64_t)S * T, T, TT, nullptr}, 1.0, 0.0), true, true);
-    if (rc) return rc;
-    // -P G = [-P_l H_l, -P_r H_r]
-    const int64_t PS = (int64_t)S * TP;
-    rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Pn, TP, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
-                   OperandW{nb.Aug + (int64_t)TP * T, T, TT, nullptr}, -1.0, 0.0), false, true);
-    if (rc) return rc;
-    rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Pn + S, TP, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
-                   OperandW{nb.Aug + (int64_t)TP * T + S, T, TT, nullptr}, -1.0, 0.0), false, true);
-    if (rc) return rc;
-    if (use_slab(f, nb)) {
-      // narrow level: the whole LU, U12, Schur block and H in one cooperative launch
-      KS_CUDA(cudaMemsetAsync(nb.norm1, 0, sizeof(double) * cnt, st));
-      unsigned* sy = f->lu_sync.p + (int64_t)4 * nb.first;
-      KS_CUDA(cudaMemsetAsync(sy, 0, sizeof(unsigned) * 4 * cnt, st));
-      if (ks::launch_lu_slab(nb, f->hbuf.p, SS, !is_root_level, sy, f->lu_sync.p + (int64_t)4 * f->n_int, st))
-        return fail(KS_ERR_CUDA, "persistent LU launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-      ++L.count[0];
-      if (int rc2 = L.check("lu_slab")) return rc2;
-      ks::launch_compose_perm(nb, st);
-      ++L.count[0];
-      KS_CUDA(cudaGetLastError());
-      return KS_OK;
-    }
-    ks::launch_colnorm1(dt, nb, st);
+  ks::launch_coupling(dt, nb, st);
+  ks::launch_aug2_init(dt, nb, st);  // S = I, E = P_r^T, the padded P copy
+  L.count[0] += 3;
+  int rc = L.check("coupling/aug2_init");
+  if (rc) return rc;
+  double* Xb = nb.XY;
+  double* Yb = nb.XY + SS;
+  double* Sb = nb.Aug;
+  double* Eb = nb.Aug + S;
+  double* Fb = nb.Aug + (int64_t)S * T;
+  double* Cb = nb.Aug + (int64_t)S * T + S;
+  // X = B H_r, Y = B^T H_l (H symmetric: read as the transposed operand)
+  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
+                      OperandW{Xb, S, XS, nullptr}, 1.0, 0.0), false, true, "zx")))
+    return rc;
+  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
+                      OperandW{Yb, S, XS, nullptr}, 1.0, 0.0), true, true, "zy")))
+    return rc;
+  // P_l H_l, and F = -P_r H_r
+  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Pn, ZT, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
+                      OperandW{nb.PHl, S, SS, nullptr}, 1.0, 0.0), false, true, "phl")))
+    return rc;
+  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Pn + S, ZT, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
+                      OperandW{Fb, T, TT, nullptr}, -1.0, 0.0), false, true, "phr")))
+    return rc;
+  // S -= Y X ; E -= Y P_l^T ; F += (P_l H_l) X ; C = (P_l H_l) P_l^T
+  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{Yb, S, XS, nullptr}, Operand{Xb, S, XS, nullptr},
+                      OperandW{Sb, T, TT, nullptr}, -1.0, 1.0), false, false, "s_yx")))
+    return rc;
+  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{Yb, S, XS, nullptr}, Operand{nb.Pn, ZT, PS, nullptr},
+                      OperandW{Eb, T, TT, nullptr}, -1.0, 1.0), false, true, "e_ypl")))
+    return rc;
+  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{Xb, S, XS, nullptr},
+                      OperandW{Fb, T, TT, nullptr}, 1.0, 1.0), false, false, "f_phx")))
+    return rc;
+  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{nb.Pn, ZT, PS, nullptr},
+                      OperandW{Cb, T, TT, nullptr}, 1.0, 0.0), false, true, "c_phpl")))
+    return rc;
+  ks::launch_znorm1(nb, st);  // ||Z||_1 for the condition estimate (linalg.py:176)
+  ++L.count[0];
+  if ((rc = L.check("znorm1"))) return rc;
+  if (use_slab(f, nb)) {
+    // narrow level: the whole LU, U12, Schur block and H in one cooperative launch
+    // (its own ||.||_1 of the slabs goes to a scratch word: Z's norm is znorm1's)
+    ks::NodeBatch sb = nb;
+    sb.norm1 = f->norm1_slab.p + nb.first;
+    KS_CUDA(cudaMemsetAsync(sb.norm1, 0, sizeof(double) * cnt, st));
+    unsigned* sy = f->lu_sync.p + (int64_t)4 * nb.first;
+    KS_CUDA(cudaMemsetAsync(sy, 0, sizeof(unsigned) * 4 * cnt, st));
+    if (ks::launch_lu_slab(sb, f->hbuf.p, SS, !is_root_level, sy, f->lu_sync.p + (int64_t)4 * f->n_int, st))
+      return fail(KS_ERR_CUDA, "persistent LU launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     ++L.count[0];
-    if (int rc2 = L.check("colnorm1")) return rc2;
-    // LU of the Z columns with pivots restricted to Z's rows
-    int pend[4] = {0, 0, 0, 0};
-    // ... with the P^T columns on the right spine of the recursion: U12 =
-    // L^-1 Pi P^T and the Schur complement H = P G Z^-1 P^T come out of it
-    // (small batches: fewer dependent launches; large batches keep the separate
-    // U12 TRSM and Schur GEMM, which run at a higher tensor-pipe rate)
-    const bool spine = nb.count <= f->knobs.spine_max;
-    rc = rlu(L, nb, 0, TP, f->pw, pend, spine ? S : 0);
-    if (rc) return rc;
-    if (!spine) {
-      rc = trsm_ul(L, nb, 0, TP, TP, S);
-      if (rc) return rc;
-      rc = L.gemm(mk(S, S, TP, cnt, Operand{nb.Aug + (int64_t)TP * T, T, TT, nullptr},
-                     Operand{nb.Aug + TP, T, TT, nullptr}, OperandW{nb.Aug + (int64_t)TP * T + TP, T, TT, nullptr},
-                     -1.0, 1.0), false, false);
-      if (rc) return rc;
-    }
+    if (int rc2 = L.check("lu_slab")) return rc2;
     ks::launch_compose_perm(nb, st);
     ++L.count[0];
-    if (!is_root_level) {
-      ks::launch_extract_h(nb, f->hbuf.p, SS, st);
-      ++L.count[0];
-      if (int rc2 = L.check("extract_h")) return rc2;
-    }
     KS_CUDA(cudaGetLastError());
+    return KS_OK;
+  }
+  // LU of S's columns with pivots restricted to S's rows. Small batches carry
+  // the E columns on the right spine of the recursion (U12 = L^-1 Pi E and the
+  // Schur block H come out of the merges: fewer dependent launches); large
+  // batches keep the separate U12 TRSM and Schur GEMM (higher tensor-pipe rate).
+  int pend[4] = {0, 0, 0, 0};
+  const int TP = nb.t_pad;
+  const bool spine = nb.count <= f->knobs.spine_max;
+  if ((rc = rlu(L, nb, 0, TP, f->pw, pend, spine ? S : 0))) return rc;
+  if (!spine) {
+    if ((rc = trsm_ul(L, nb, 0, TP, TP, S))) return rc;
+    if ((rc = L.gemm(mk(S, S, TP, cnt, Operand{Fb, T, TT, nullptr}, Operand{Eb, T, TT, nullptr},
+                        OperandW{Cb, T, TT, nullptr}, -1.0, 1.0), false, false, "schur")))
+      return rc;
+  }
+  ks::launch_compose_perm(nb, st);
+  ++L.count[0];
+  if (!is_root_level) {
+    ks::launch_extract_h(nb, f->hbuf.p, SS, st);
+    ++L.count[0];
+    if (int rc2 = L.check("extract_h")) return rc2;
+  }
+  KS_CUDA(cudaGetLastError());
   return KS_OK;
 }
 
-static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt, int T, int S, int TP) {
+static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt) {
+  const int S = nb.s_pad, T = nb.T, TP = nb.t_pad;
   ks::NodeBatch s = nb;
   s.count = cnt;
   s.first = nb.first + off;
@@ -294,8 +317,10 @@ static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt, int T,
   s.left = nb.left + off;
   s.right = nb.right + off;
   s.Aug = nb.Aug + (int64_t)off * T * T;
+  s.XY = nb.XY + (int64_t)off * 2 * S * S;
+  s.PHl = nb.PHl + (int64_t)off * S * S;
   s.Bc = nb.Bc + (int64_t)off * S * S;
-  s.Pn = nb.Pn + (int64_t)off * S * TP;
+  s.Pn = nb.Pn + (int64_t)off * S * nb.zt;
   s.piv = nb.piv + (int64_t)off * TP;
   s.norm1 = nb.norm1 + off;
   s.cond = nb.cond + off;
@@ -367,7 +392,7 @@ static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, 
         KS_CUDA(cudaStreamWaitEvent(f->gst[g], f->gfork, 0));
         const int o0 = (int)((int64_t)nb.count * g / G), o1 = (int)((int64_t)nb.count * (g + 1) / G);
         Launcher Lg{f, f->gst[g], &f->launches[0]};
-        if (int rc = enqueue_level_body(f, Lg, sub_batch(nb, o0, o1 - o0, f->T, f->s_pad, f->t_pad), is_root_level))
+        if (int rc = enqueue_level_body(f, Lg, sub_batch(nb, o0, o1 - o0), is_root_level))
           return rc;
         KS_CUDA(cudaEventRecord(f->gjoin[g], f->gst[g]));
         KS_CUDA(cudaStreamWaitEvent(st, f->gjoin[g], 0));

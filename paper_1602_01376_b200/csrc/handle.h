@@ -142,7 +142,9 @@ struct ks_factor {
   int64_t loc_begin = 0, loc_end = 0;   // tree-order rows owned by the shard
   std::vector<int64_t> peers;           // nodes at the shard level (all shards' roots)
   bool local_factored = false;
-  int m_pad = 0, s_pad = 0, t_pad = 0, T = 0, R = 0, pw = 32;
+  // padded shapes: leaf m_pad, rank s_pad; the node LU view has t_pad = s_pad pivot
+  // rows and order T = 2 s_pad; zt = 2 s_pad is the order of the padded Z
+  int m_pad = 0, s_pad = 0, t_pad = 0, T = 0, zt = 0, R = 0, pw = 32;
   // device tables
   ksr::DBuf<double> coords, xx;   // coords: n + m_pad rows (zero tail), tree order
   ksr::DBuf<int> rank_d, skel_pos;
@@ -155,6 +157,8 @@ struct ks_factor {
   ksr::DBuf<double> dinv;  // condition estimator: diagonal-block inverses of every node's Z factors
   ksr::DBuf<double> lut;   // condition estimator: column-major copies of every node's Z factors (t_pad <= 512)
   ksr::DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
+  ksr::DBuf<double> xy, phl;      // per internal node: X = B H_r and Y = B^T H_l; P_l H_l (the solve's up pass)
+  ksr::DBuf<double> norm1_slab;   // scratch for the persistent LU's own column norms
   // solve workspaces (solve.cu): a pool of per-call workspaces; the sharded
   // solve phases (ks_solve_up / top / down, ks_node_exchange) keep theirs across calls
   std::mutex ws_mu;
@@ -208,6 +212,9 @@ struct ks_factor {
     nb.s_pad = fb_T - m_pad;
     nb.t_pad = m_pad;
     nb.T = fb_T;
+    nb.zt = 0;
+    nb.XY = nullptr;
+    nb.PHl = nullptr;
     nb.Aug = fb_aug.p;
     nb.Bc = nullptr;
     nb.Pn = nullptr;
@@ -271,9 +278,12 @@ struct ks_factor {
     nb.s_pad = s_pad;
     nb.t_pad = t_pad;
     nb.T = T;
+    nb.zt = zt;
     nb.Aug = aug.p + (int64_t)first * T * T;
+    nb.XY = xy.p + (int64_t)first * 2 * s_pad * s_pad;
+    nb.PHl = phl.p + (int64_t)first * s_pad * s_pad;
     nb.Bc = bc.p + (int64_t)first * s_pad * s_pad;
-    nb.Pn = pn.p + (int64_t)first * s_pad * t_pad;
+    nb.Pn = pn.p + (int64_t)first * s_pad * zt;
     nb.piv = piv.p + (int64_t)first * t_pad;
     nb.norm1 = norm1.p + first;
     nb.cond = cond.p + first;
@@ -289,7 +299,7 @@ struct ks_factor {
     int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release();
     pm.release(); lu_scratch.release(); lu_sync.release(); dinv.release(); lut.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
-    norm1.release(); cond.release();
+    norm1.release(); cond.release(); xy.release(); phl.release(); norm1_slab.release();
     fb_aug.release(); fb_norm1.release(); fb_cond.release(); fb_piv.release(); fb_info.release();
     fb_moves.release(); fb_pm.release(); fb_node.release(); fb_begin.release(); fb_size.release();
     for (auto& w : ws) {

@@ -29,16 +29,28 @@ struct LeafBatch {
 };
 
 // Internal nodes of one level (contiguous internal indices).
+//
+// Block formulation of the node step: Z = I + W G =
+// [[I, X], [Y, I]] with X = B H_r, Y = B^T H_l (padded s_pad x s_pad each)
+// is eliminated with its identity (1,1) block as pivot, leaving
+// S = I - Y X, whose LU with partial pivoting is the only pivoted step; the
+// augmented matrix the LU kernels see is
+//     Aug = [[S, E], [F, C]]   (T = 2 s_pad, pivots among the first t_pad = s_pad rows)
+//     E = P_r^T - Y P_l^T,  F = P_l H_l X - P_r H_r,  C = P_l H_l P_l^T,
+// so after the LU its trailing block is C - F S^-1 E = P G Z^-1 P^T = H.
 struct NodeBatch {
   int count;
   int first;         // internal index of the batch's first node (per-node solve buffers)
   const int* node;   // node ids
   const int* left;   // child node ids
   const int* right;
-  int s_pad, t_pad, T;  // T = t_pad + s_pad (augmented order)
-  double* Aug;          // count x T x T (row-major), already offset to the level
+  int s_pad, t_pad, T;  // LU view: t_pad = s_pad pivot rows, T = t_pad + s_pad = 2 s_pad
+  int zt;               // order of the padded Z (2 s_pad): P's row length, the solve's per-node vector
+  double* Aug;          // count x T x T (row-major) [[S, E], [F, C]] -> LU, already offset to the level
+  double* XY;           // count x 2 x s_pad x s_pad: X = B H_r, then Y = B^T H_l
+  double* PHl;          // count x s_pad x s_pad: P_l H_l
   double* Bc;           // count x s_pad x s_pad coupling blocks
-  double* Pn;           // count x s_pad x t_pad padded P
+  double* Pn;           // count x s_pad x zt padded P
   int* piv;             // count x t_pad
   double* norm1;        // count
   double* cond;         // count
@@ -59,8 +71,10 @@ void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStr
 void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st);
 void launch_mirror_lower(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st);
 void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
-void launch_aug_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
-void launch_colnorm1(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
+// block formulation (node_kernels.cu): S = I and E = P_r^T blocks of Aug, the padded P copy
+void launch_aug2_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
+// ||Z||_1 from X and Y (linalg.py:176): max column abs sum of [[I, X], [Y, I]]
+void launch_znorm1(const NodeBatch& nb, cudaStream_t st);
 // pend (may be null): {row0, col0, rows, cols} of a U12 block waiting in nb.scratch
 void launch_lu_panel(const NodeBatch& nb, int c0, int w, cudaStream_t st, const int* pend = nullptr);
 void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncols, cudaStream_t st);
@@ -70,6 +84,8 @@ void launch_trsm_unit_lower(const NodeBatch& nb, int r0, int w, int c0, int ncol
 // Z's factors the estimator's non-transposed solves read (t_pad <= 512)
 void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, double* lut, int max_ctas, cudaStream_t st);
 int hager_launches(const NodeBatch& nb);
+// diagonal-block inverses of the LU factors (Hager solves), 2 x t_pad x 8 per node
+void launch_diag_inv(const NodeBatch& nb, double* dinv, cudaStream_t st);
 void launch_extract_h(const NodeBatch& nb, double* H, int64_t h_stride, cudaStream_t st);
 void launch_compose_perm(const NodeBatch& nb, cudaStream_t st);
 void launch_lu_merge(const NodeBatch& nb, int c0, int h, int w, cudaStream_t st);

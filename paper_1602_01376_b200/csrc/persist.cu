@@ -186,6 +186,8 @@ int ks_save_factor(const ks_factor* f, const ks_problem* p, const char* path) {
   if (!rc) rc = save_dev(w, "aug", f->aug, sp);
   if (!rc) rc = save_dev(w, "bc", f->bc, sp);
   if (!rc) rc = save_dev(w, "pn", f->pn, sp);
+  if (!rc) rc = save_dev(w, "xy", f->xy, sp);
+  if (!rc) rc = save_dev(w, "phl", f->phl, sp);
   if (!rc) rc = save_dev(w, "piv", f->piv, sp);
   if (!rc) rc = save_dev(w, "pm", f->pm, sp);
   if (!rc) rc = save_dev(w, "norm1", f->norm1, sp);
@@ -247,6 +249,8 @@ int ks_load_factor(const char* path, const ks_problem* p, int device, ks_factor*
   if (!rc) rc = load_dev(r, "aug", f->aug, sp);
   if (!rc) rc = load_dev(r, "bc", f->bc, sp);
   if (!rc) rc = load_dev(r, "pn", f->pn, sp);
+  if (!rc) rc = load_dev(r, "xy", f->xy, sp);
+  if (!rc) rc = load_dev(r, "phl", f->phl, sp);
   if (!rc) rc = load_dev(r, "piv", f->piv, sp);
   if (!rc) rc = load_dev(r, "pm", f->pm, sp);
   if (!rc) rc = load_dev(r, "norm1", f->norm1, sp);

@@ -23,8 +23,8 @@ int ws_fit(ks_factor* f, SolveWs* w, int64_t q) {
   KS_CUDA(w->z.alloc((size_t)f->leaf_nodes.size() * f->m_pad * q));
   KS_CUDA(w->c.alloc((size_t)std::max<int64_t>(f->n_nodes * f->s_pad * q, 1)));
   KS_CUDA(w->tin.alloc((size_t)std::max<int64_t>(f->n_nodes * f->s_pad * q, 1)));
-  KS_CUDA(w->y.alloc((size_t)std::max<int64_t>((int64_t)f->n_int * f->t_pad * q, 1)));
-  KS_CUDA(w->wtmp.alloc((size_t)std::max<int64_t>((int64_t)f->n_int * f->t_pad * q, 1)));
+  KS_CUDA(w->y.alloc((size_t)std::max<int64_t>((int64_t)f->n_int * f->zt * q, 1)));
+  KS_CUDA(w->wtmp.alloc((size_t)std::max<int64_t>((int64_t)f->n_int * f->zt * q, 1)));
   KS_CUDA(w->bdev.alloc((size_t)f->n * q));
   KS_CUDA(w->xdev.alloc((size_t)f->n * q));
   w->q_cap = q;
@@ -185,45 +185,65 @@ static int leaf_down_gemm(ks_factor* f, SolveWs* w, Launcher& L, double* Xd, int
   return KS_OK;
 }
 
-// up pass at one level: w = [B c_r; B^T c_l], y = L^-1 Pi w, c = P cc + L21aug y
+// up pass at one level (block formulation, kernels.cuh NodeBatch):
+//   r1 = B c_r (kept in y's first half), r2 = B^T c_l - Y r1, y2 = L^-1 Pi r2,
+//   c = P cc - (P_l H_l) r1 + L21 y2
 static int node_up_gemm(ks_factor* f, SolveWs* w, Launcher& L, const ks::NodeBatch& nb, bool root, int q) {
-  const int S = f->s_pad, TP = f->t_pad, T = f->T, cnt = nb.count;
-  const int64_t SS = (int64_t)S * S, TT = (int64_t)T * T, CS = (int64_t)S * q, YS = (int64_t)TP * q;
+  const int S = nb.s_pad, T = nb.T, ZT = nb.zt, cnt = nb.count;
+  const int64_t SS = (int64_t)S * S, XS = 2 * SS, TT = (int64_t)T * T, CS = (int64_t)S * q, YS = (int64_t)ZT * q;
+  const int64_t PS = (int64_t)S * ZT;
   double* wv = w->wtmp.p + (int64_t)nb.first * YS;
   double* y = w->y.p + (int64_t)nb.first * YS;
+  double* r1 = y;
+  double* y2 = y + (int64_t)S * q;
   int rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{w->c.p, q, CS, nb.right},
-                     OperandW{wv, q, YS, nullptr}, 1.0, 0.0), false, false);
+                     OperandW{r1, q, YS, nullptr}, 1.0, 0.0), false, false);
   if (rc) return rc;
   rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{w->c.p, q, CS, nb.left},
                  OperandW{wv + (int64_t)S * q, q, YS, nullptr}, 1.0, 0.0), true, false);
   if (rc) return rc;
+  rc = L.gemm(mk(S, q, S, cnt, Operand{nb.XY + SS, S, XS, nullptr}, Operand{r1, q, YS, nullptr},
+                 OperandW{wv + (int64_t)S * q, q, YS, nullptr}, -1.0, 1.0), false, false);
+  if (rc) return rc;
   ks::launch_permute_rows(nb, w->wtmp.p, w->y.p, q, L.st);
   ++*L.count;
-  if ((rc = gemm_trsm(L, false, true, nb.Aug, T, TT, y, q, YS, TP, q, cnt))) return rc;
+  if ((rc = gemm_trsm(L, false, true, nb.Aug, T, TT, y2, q, YS, S, q, cnt))) return rc;
   if (root) return KS_OK;
-  const int64_t PS = (int64_t)S * TP;
-  rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Pn, TP, PS, nullptr}, Operand{w->c.p, q, CS, nb.left},
+  rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Pn, ZT, PS, nullptr}, Operand{w->c.p, q, CS, nb.left},
                  OperandW{w->c.p, q, CS, nb.node}, 1.0, 0.0), false, false);
   if (rc) return rc;
-  rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Pn + S, TP, PS, nullptr}, Operand{w->c.p, q, CS, nb.right},
+  rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Pn + S, ZT, PS, nullptr}, Operand{w->c.p, q, CS, nb.right},
                  OperandW{w->c.p, q, CS, nb.node}, 1.0, 1.0), false, false);
   if (rc) return rc;
-  return L.gemm(mk(S, q, TP, cnt, Operand{nb.Aug + (int64_t)TP * T, T, TT, nullptr}, Operand{y, q, YS, nullptr},
+  rc = L.gemm(mk(S, q, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{r1, q, YS, nullptr},
+                 OperandW{w->c.p, q, CS, nb.node}, -1.0, 1.0), false, false);
+  if (rc) return rc;
+  return L.gemm(mk(S, q, S, cnt, Operand{nb.Aug + (int64_t)S * T, T, TT, nullptr}, Operand{y2, q, YS, nullptr},
                    OperandW{w->c.p, q, CS, nb.node}, 1.0, 1.0), false, false);
 }
 
-// down pass at one level: u = U^-1 (y + U12aug t); children get split(u)
+// down pass at one level: y2 += U12 t, r1 += P_l^T t (not at the root);
+// w2 = U^-1 y2, w1 = r1 - X w2; the children receive w1 and w2
 static int node_down_gemm(ks_factor* f, SolveWs* w, Launcher& L, const ks::NodeBatch& nb, bool root, int q) {
-  const int S = f->s_pad, TP = f->t_pad, T = f->T, cnt = nb.count;
-  const int64_t TT = (int64_t)T * T, CS = (int64_t)S * q, YS = (int64_t)TP * q;
+  const int S = nb.s_pad, T = nb.T, ZT = nb.zt, cnt = nb.count;
+  const int64_t SS = (int64_t)S * S, XS = 2 * SS, TT = (int64_t)T * T, CS = (int64_t)S * q, YS = (int64_t)ZT * q;
+  const int64_t PS = (int64_t)S * ZT;
   double* y = w->y.p + (int64_t)nb.first * YS;
+  double* r1 = y;
+  double* y2 = y + (int64_t)S * q;
   int rc;
   if (!root) {
-    rc = L.gemm(mk(TP, q, S, cnt, Operand{nb.Aug + TP, T, TT, nullptr}, Operand{w->tin.p, q, CS, nb.node},
-                   OperandW{y, q, YS, nullptr}, 1.0, 1.0), false, false);
+    rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Aug + S, T, TT, nullptr}, Operand{w->tin.p, q, CS, nb.node},
+                   OperandW{y2, q, YS, nullptr}, 1.0, 1.0), false, false);
+    if (rc) return rc;
+    rc = L.gemm(mk(S, q, S, cnt, Operand{nb.Pn, ZT, PS, nullptr}, Operand{w->tin.p, q, CS, nb.node},
+                   OperandW{r1, q, YS, nullptr}, 1.0, 1.0), true, false);
     if (rc) return rc;
   }
-  if ((rc = gemm_trsm(L, true, false, nb.Aug, T, TT, y, q, YS, TP, q, cnt))) return rc;
+  if ((rc = gemm_trsm(L, true, false, nb.Aug, T, TT, y2, q, YS, S, q, cnt))) return rc;
+  rc = L.gemm(mk(S, q, S, cnt, Operand{nb.XY, S, XS, nullptr}, Operand{y2, q, YS, nullptr},
+                 OperandW{r1, q, YS, nullptr}, -1.0, 1.0), false, false);
+  if (rc) return rc;
   ks::launch_split_u(nb, w->y.p, w->tin.p, q, L.st);
   ++*L.count;
   return KS_OK;

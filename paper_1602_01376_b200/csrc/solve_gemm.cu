@@ -104,14 +104,15 @@ void launch_leaf_scatter(const LeafBatch& lb, const double* Z, double* X, int64_
   k_leaf_scatter<<<g, 256, 0, st>>>(lb, Z, X, ldx, q);
 }
 
-// Y[k] = Pi W[k]: rows through the composed pivot permutation (t_pad x q blocks)
+// Y[k] = Pi W[k] for the second half of each node's 2 s_pad-row block (the S
+// rows of the block formulation): rows through S's composed pivot permutation
 __global__ void k_permute_rows(NodeBatch nb, const double* W, double* Y, int q) {
   const int k = blockIdx.y;
-  const int TP = nb.t_pad;
-  const int* pm = nb.pm + (int64_t)k * TP;
-  const double* w = W + (int64_t)(nb.first + k) * TP * q;
-  double* y = Y + (int64_t)(nb.first + k) * TP * q;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < TP * q; e += gridDim.x * blockDim.x)
+  const int S = nb.t_pad;
+  const int* pm = nb.pm + (int64_t)k * S;
+  const double* w = W + (int64_t)(nb.first + k) * nb.zt * q + (int64_t)S * q;
+  double* y = Y + (int64_t)(nb.first + k) * nb.zt * q + (int64_t)S * q;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < S * q; e += gridDim.x * blockDim.x)
     y[e] = w[(int64_t)pm[e / q] * q + e % q];
 }
 
@@ -123,8 +124,8 @@ void launch_permute_rows(const NodeBatch& nb, const double* W, double* Y, int q,
 // children's incoming blocks from the node's solved u = [u_l; u_r]
 __global__ void k_split_u(NodeBatch nb, const double* U, double* tin, int q) {
   const int k = blockIdx.y;
-  const int S = nb.s_pad, TP = nb.t_pad;
-  const double* u = U + (int64_t)(nb.first + k) * TP * q;
+  const int S = nb.s_pad;
+  const double* u = U + (int64_t)(nb.first + k) * nb.zt * q;
   double* tl = tin + (int64_t)nb.left[k] * S * q;
   double* tr = tin + (int64_t)nb.right[k] * S * q;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < S * q; e += gridDim.x * blockDim.x) {

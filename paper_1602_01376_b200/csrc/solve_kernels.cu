@@ -3,9 +3,11 @@
 // up/down form below visits every node once).
 //
 //   up   leaf  z = L^-1 b ;  c = L21 z                     (= P A^-1 b)
-//        node  w = [B c_r ; B^T c_l] ;  y = L^-1 Pi w ;  c = P cc + L21aug y
-//   down node  u = U^-1 (y + U12aug t) ;  t_l, t_r = split(u)
+//        node  r1 = B c_r ; y2 = L^-1 Pi (B^T c_l - Y r1) ; c = P cc - P_l H_l r1 + L21 y2
+//   down node  w2 = U^-1 (y2 + U12 t) ; w1 = r1 + P_l^T t - X w2 ; t_l, t_r = w1, w2
 //        leaf  x = L^-T (z - L21^T t)
+// (node factors in the block formulation of kernels.cuh NodeBatch: Z^-1 through
+// Z = [[I, 0], [Y, I]] [[I, X], [0, S]] and the LU of S)
 //
 // Every kernel streams its node's factor rows once, coalesced along rows, with
 // warp-shuffle reductions; right-hand sides are processed QC columns at a time.
@@ -71,91 +73,103 @@ __global__ void __launch_bounds__(STHREADS, 8) k_leaf_bwd(LeafBatch lb, double* 
 }
 
 // ---------------------------------------------------------------------------
-// internal node up: w = [B c_r; B^T c_l], y = L^-1 Pi w, c = P cc + L21aug y
+// internal node up (block formulation, kernels.cuh NodeBatch):
+//   r1 = B c_r ;  r2 = B^T c_l - Y r1 ;  y2 = L^-1 Pi r2
+//   y[node] = [r1; y2] ;  c = P cc - (P_l H_l) r1 + L21 y2
 // ---------------------------------------------------------------------------
 template <int QC>
 __global__ void __launch_bounds__(STHREADS) k_node_up(NodeBatch nb, SolveBufs sb, int q0, int root) {
   extern __shared__ double sm[];
-  const int S = nb.s_pad, TP = nb.t_pad, T = nb.T;
-  double* cc = sm;              // TP x QC
-  double* w = cc + TP * QC;     // TP x QC
-  double* red = w + TP * QC;    // SWARPS x 32 x QC
+  const int S = nb.s_pad, T = nb.T, ZT = nb.zt;
+  double* cc = sm;               // 2S x QC: [c_l; c_r]
+  double* r = cc + ZT * QC;      // 2S x QC: [r1; r2 -> y2]
+  double* tq = r + ZT * QC;      // S x QC: Y r1, then -r1
+  double* red = tq + S * QC;     // SWARPS x 32 x QC
   __shared__ double D[SB][SB + 1];
   const int k = blockIdx.x;
-  const int v = nb.node[k], l = nb.left[k], r = nb.right[k];
+  const int v = nb.node[k], l = nb.left[k], rr = nb.right[k];
   const double* cl = sb.c + (int64_t)l * S * sb.q;
-  const double* cr = sb.c + (int64_t)r * S * sb.q;
+  const double* cr = sb.c + (int64_t)rr * S * sb.q;
   for (int e = threadIdx.x; e < S * QC; e += STHREADS) {
     const int i = e / QC, q = e % QC;
     cc[e] = cl[(int64_t)i * sb.q + q0 + q];
     cc[S * QC + e] = cr[(int64_t)i * sb.q + q0 + q];
-    w[S * QC + e] = 0.0;
+    r[S * QC + e] = 0.0;
   }
   __syncthreads();
   const double* Bc = nb.Bc + (int64_t)k * S * S;
-  cta_gemv_rows<QC>(Bc, S, S, S, cc + S * QC, w, QC, false);      // B c_r
-  cta_gemv_cols<QC>(Bc, S, S, S, cc, w + S * QC, 1.0, red);       // B^T c_l
+  double* r1 = r;
+  double* r2 = r + S * QC;
+  cta_gemv_rows<QC>(Bc, S, S, S, cc + S * QC, r1, QC, false);   // B c_r
+  cta_gemv_cols<QC>(Bc, S, S, S, cc, r2, 1.0, red);              // B^T c_l
   __syncthreads();
-  {  // Pi w through the composed row interchanges (cc is free as scratch only after c)
-    const int* pm = nb.pm + (int64_t)k * TP;
-    double* tmp = red;  // reuse: needs TP*QC <= SWARPS*32*QC -> only when TP <= 256
-    if (TP <= SWARPS * 32) {
-      for (int e = threadIdx.x; e < TP * QC; e += STHREADS) tmp[e] = w[pm[e / QC] * QC + e % QC];
-      __syncthreads();
-      for (int e = threadIdx.x; e < TP * QC; e += STHREADS) w[e] = tmp[e];
-    } else if (threadIdx.x < QC) {
-      const int q = threadIdx.x;
-      const int* piv = nb.piv + (int64_t)k * TP;
-      for (int i = 0; i < TP; ++i) {
-        const int p = piv[i];
-        if (p != i) { const double t = w[i * QC + q]; w[i * QC + q] = w[p * QC + q]; w[p * QC + q] = t; }
-      }
-    }
+  const double* X = nb.XY + (int64_t)k * 2 * S * S;
+  const double* Y = X + (int64_t)S * S;
+  cta_gemv_rows<QC>(Y, S, S, S, r1, tq, QC, false);              // Y r1
+  __syncthreads();
+  for (int e = threadIdx.x; e < S * QC; e += STHREADS) r2[e] -= tq[e];
+  __syncthreads();
+  {  // Pi r2 through S's composed row interchanges (tq as scratch)
+    const int* pm = nb.pm + (int64_t)k * S;
+    for (int e = threadIdx.x; e < S * QC; e += STHREADS) tq[e] = r2[pm[e / QC] * QC + e % QC];
+    __syncthreads();
+    for (int e = threadIdx.x; e < S * QC; e += STHREADS) r2[e] = tq[e];
   }
   __syncthreads();
   const double* A = nb.Aug + (int64_t)k * T * T;
-  cta_trsv_rows<QC, false, true>(A, T, TP, w, D);
-  double* y = sb.y + (int64_t)(nb.first + k) * TP * sb.q;
-  for (int e = threadIdx.x; e < TP * QC; e += STHREADS) y[(e / QC) * sb.q + q0 + e % QC] = w[e];
+  cta_trsv_rows<QC, false, true>(A, T, S, r2, D);                // y2 = L^-1 Pi r2
+  double* y = sb.y + (int64_t)(nb.first + k) * ZT * sb.q;
+  for (int e = threadIdx.x; e < ZT * QC; e += STHREADS) y[(e / QC) * sb.q + q0 + e % QC] = r[e];
   if (!root) {
+    for (int e = threadIdx.x; e < S * QC; e += STHREADS) tq[e] = -r1[e];
     double* c = sb.c + (int64_t)v * S * sb.q + q0;
-    cta_gemv_rows<QC>(nb.Pn + (int64_t)k * S * TP, TP, S, TP, cc, c, sb.q, false);
+    cta_gemv_rows<QC>(nb.Pn + (int64_t)k * S * ZT, ZT, S, ZT, cc, c, sb.q, false);
     __syncthreads();
-    cta_gemv_rows<QC>(A + (int64_t)TP * T, T, S, TP, w, c, sb.q, true);
+    cta_gemv_rows<QC>(nb.PHl + (int64_t)k * S * S, S, S, S, tq, c, sb.q, true);
+    __syncthreads();
+    cta_gemv_rows<QC>(A + (int64_t)S * T, T, S, S, r2, c, sb.q, true);
   }
 }
 
 // ---------------------------------------------------------------------------
-// internal node down: u = U^-1 (y + U12aug t); children receive split(u)
+// internal node down: y2 += U12 t, r1 += P_l^T t (not at the root);
+//   w2 = U^-1 y2 ;  w1 = r1 - X w2 ;  the children receive w1 (left), w2 (right)
 // ---------------------------------------------------------------------------
 template <int QC>
 __global__ void __launch_bounds__(STHREADS) k_node_down(NodeBatch nb, SolveBufs sb, int q0, int root) {
   extern __shared__ double sm[];
-  const int S = nb.s_pad, TP = nb.t_pad, T = nb.T;
-  double* u = sm;             // TP x QC
-  double* tv = u + TP * QC;   // S x QC
+  const int S = nb.s_pad, T = nb.T, ZT = nb.zt;
+  double* u = sm;                 // 2S x QC: [r1; y2]
+  double* tv = u + ZT * QC;       // S x QC: incoming t, then X w2
+  double* red = tv + S * QC;      // SWARPS x 32 x QC
   __shared__ double D[SB][SB + 1];
   const int k = blockIdx.x;
   const int v = nb.node[k], l = nb.left[k], r = nb.right[k];
-  const double* y = sb.y + (int64_t)(nb.first + k) * TP * sb.q;
-  for (int e = threadIdx.x; e < TP * QC; e += STHREADS) u[e] = y[(e / QC) * sb.q + q0 + e % QC];
+  const double* y = sb.y + (int64_t)(nb.first + k) * ZT * sb.q;
+  for (int e = threadIdx.x; e < ZT * QC; e += STHREADS) u[e] = y[(e / QC) * sb.q + q0 + e % QC];
   if (!root) {
     const double* ti = sb.tin + (int64_t)v * S * sb.q;
     for (int e = threadIdx.x; e < S * QC; e += STHREADS) tv[e] = ti[(e / QC) * sb.q + q0 + e % QC];
   }
   __syncthreads();
   const double* A = nb.Aug + (int64_t)k * T * T;
+  double* u1 = u;
+  double* u2 = u + S * QC;
   if (!root) {
-    cta_gemv_rows<QC>(A + TP, T, TP, S, tv, u, QC, true);
+    cta_gemv_rows<QC>(A + S, T, S, S, tv, u2, QC, true);                      // y2 += U12 t
+    cta_gemv_cols<QC>(nb.Pn + (int64_t)k * S * ZT, ZT, S, S, tv, u1, 1.0, red);  // r1 += P_l^T t
     __syncthreads();
   }
-  cta_trsv_rows<QC, true, false>(A, T, TP, u, D);
+  cta_trsv_rows<QC, true, false>(A, T, S, u2, D);                             // w2 = U^-1 y2
+  const double* X = nb.XY + (int64_t)k * 2 * S * S;
+  cta_gemv_rows<QC>(X, S, S, S, u2, tv, QC, false);                           // X w2
+  __syncthreads();
   double* tl = sb.tin + (int64_t)l * S * sb.q;
   double* tr = sb.tin + (int64_t)r * S * sb.q;
   for (int e = threadIdx.x; e < S * QC; e += STHREADS) {
     const int i = e / QC, q = e % QC;
-    tl[(int64_t)i * sb.q + q0 + q] = u[e];
-    tr[(int64_t)i * sb.q + q0 + q] = u[S * QC + e];
+    tl[(int64_t)i * sb.q + q0 + q] = u1[e] - tv[e];
+    tr[(int64_t)i * sb.q + q0 + q] = u2[e];
   }
 }
 
@@ -298,7 +312,7 @@ void launch_node_up(const NodeBatch& nb, const SolveBufs& sb, bool root, cudaStr
       launch_node_up_cluster(nb, sb, root, q0, qc, st);
       return;
     }
-    const size_t smem = ((size_t)2 * nb.t_pad + SWARPS * 32) * qc * sizeof(double);
+    const size_t smem = ((size_t)2 * nb.zt + nb.s_pad + SWARPS * 32) * qc * sizeof(double);
 #define KS_CASE(QC)                                                                 \
   if (qc == QC) {                                                                   \
     set_smem(k_node_up<QC>, smem);                                                  \
@@ -315,7 +329,7 @@ void launch_node_down(const NodeBatch& nb, const SolveBufs& sb, bool root, cudaS
       launch_node_down_cluster(nb, sb, root, q0, qc, st);
       return;
     }
-    const size_t smem = ((size_t)nb.t_pad + nb.s_pad) * qc * sizeof(double);
+    const size_t smem = ((size_t)nb.zt + nb.s_pad + SWARPS * 32) * qc * sizeof(double);
 #define KS_CASE(QC)                                                                 \
   if (qc == QC) {                                                                   \
     set_smem(k_node_down<QC>, smem);                                                \
