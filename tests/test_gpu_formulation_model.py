@@ -7,7 +7,7 @@ from oracle import gpu_model as GM
 from oracle import ks_oracle as O
 
 
-@pytest.mark.parametrize("case", ["cfg1", "cfg2s", "ragged", "single", "cfg5s"])
+@pytest.mark.parametrize("case", ["cfg1", "cfg2s", "ragged", "single", "cfg5s", "cfg4s"])
 def test_model_matches_reference(golden, case):
     g = golden(case)
     prob = O.Problem(g)
