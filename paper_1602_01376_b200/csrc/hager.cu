@@ -263,45 +263,57 @@ __global__ void __launch_bounds__(256) k_lu_transpose(NodeBatch nb, double* lut)
 
 
 // out[r] = sum_j M[r][j] xin[j] for r < n (M row-major, ld n, n % 64 == 0):
-// a warp per row, 16-byte loads along the row, 4 rows in flight per warp
+// a warp per 4 rows, 16-byte loads along the rows; every load of a row group
+// is issued before the first FMA (up to 16 in flight per lane: the GEMV is
+// bound by the loads a single CTA keeps in flight, not by bandwidth)
 template <int NT>
 __device__ __forceinline__ void gemv_rows_smem(const double* __restrict__ M, int n, const double* xin, double* out) {
   constexpr int NW = NT / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int segs = n >> 6;  // 64-column segments: one double2 per lane each
   for (int r0 = warp * 4; r0 < n; r0 += NW * 4) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int c = 2 * lane; c < n; c += 64) {
-      const double x0 = xin[c], x1 = xin[c + 1];
+    for (int sg0 = 0; sg0 < segs; sg0 += 4) {
+      double2 a[4][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (r0 + u < n) {
-          const double2 a = ldg2(M + (int64_t)(r0 + u) * n + c);
-          acc[u] = fma(a.x, x0, fma(a.y, x1, acc[u]));
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+          a[u][g] = (sg0 + g < segs) ? ldg2(M + (int64_t)(r0 + u) * n + (sg0 + g) * 64 + 2 * lane)
+                                     : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        if (sg0 + g < segs) {
+          const int c = (sg0 + g) * 64 + 2 * lane;
+          const double x0 = xin[c], x1 = xin[c + 1];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u] = fma(a[u][g].x, x0, fma(a[u][g].y, x1, acc[u]));
         }
       }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const double v = warp_sum(acc[u]);
-      if (lane == 0 && r0 + u < n) out[r0 + u] = v;
+      if (lane == 0) out[r0 + u] = v;
     }
   }
 }
 
-// sum_r M[r][i] xin[r] for this thread's column i < n (coalesced across threads)
+// sum_r M[r][i] xin[r] for this thread's column i < n (coalesced across
+// threads), 16 loads in flight per thread
 __device__ __forceinline__ double gemv_col_own(const double* __restrict__ M, int n, const double* xin, int i) {
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (i < n) {
     const double* p = M + i;
-#pragma unroll 2
-    for (int r = 0; r < n; r += 4) {
-      a0 = fma(__ldg(p + (int64_t)r * n), xin[r], a0);
-      a1 = fma(__ldg(p + (int64_t)(r + 1) * n), xin[r + 1], a1);
-      a2 = fma(__ldg(p + (int64_t)(r + 2) * n), xin[r + 2], a2);
-      a3 = fma(__ldg(p + (int64_t)(r + 3) * n), xin[r + 3], a3);
+    for (int r = 0; r < n; r += 16) {
+      double a[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) a[u] = __ldg(p + (int64_t)(r + u) * n);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc[u & 3] = fma(a[u], xin[r + u], acc[u & 3]);
     }
   }
-  return (a0 + a1) + (a2 + a3);
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 // nb: the LU view (t_pad = s_pad = S, T = 2 S); dinv: the diagonal-block
