@@ -243,6 +243,8 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(f->pn.alloc((size_t)f->n_int * f->s_pad * f->zt + 1));
     KS_CUDA(f->xy.alloc((size_t)f->n_int * 2 * f->s_pad * f->s_pad + 1));
     KS_CUDA(f->phl.alloc((size_t)f->n_int * f->s_pad * f->s_pad + 1));
+    KS_CUDA(f->bt.alloc((size_t)f->n_int * f->s_pad * f->s_pad + 1));
+    KS_CUDA(f->pt.alloc((size_t)f->n_int * f->zt * f->s_pad + 1));
     KS_CUDA(f->norm1_slab.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->norm1.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->cond.alloc(std::max(f->n_int, 1)));

@@ -236,33 +236,40 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
   double* Eb = nb.Aug + S;
   double* Fb = nb.Aug + (int64_t)S * T;
   double* Cb = nb.Aug + (int64_t)S * T + S;
-  // X = B H_r, Y = B^T H_l (H symmetric: read as the transposed operand)
-  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
-                      OperandW{Xb, S, XS, nullptr}, 1.0, 0.0), false, true, "zx")))
-    return rc;
-  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
-                      OperandW{Yb, S, XS, nullptr}, 1.0, 0.0), true, true, "zy")))
-    return rc;
-  // P_l H_l, and F = -P_r H_r
-  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Pn, ZT, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
-                      OperandW{nb.PHl, S, SS, nullptr}, 1.0, 0.0), false, true, "phl")))
-    return rc;
-  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.Pn + S, ZT, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
-                      OperandW{Fb, T, TT, nullptr}, -1.0, 0.0), false, true, "phr")))
-    return rc;
-  // S -= Y X ; E -= Y P_l^T ; F += (P_l H_l) X ; C = (P_l H_l) P_l^T
-  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{Yb, S, XS, nullptr}, Operand{Xb, S, XS, nullptr},
-                      OperandW{Sb, T, TT, nullptr}, -1.0, 1.0), false, false, "s_yx")))
-    return rc;
-  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{Yb, S, XS, nullptr}, Operand{nb.Pn, ZT, PS, nullptr},
-                      OperandW{Eb, T, TT, nullptr}, -1.0, 1.0), false, true, "e_ypl")))
-    return rc;
-  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{Xb, S, XS, nullptr},
-                      OperandW{Fb, T, TT, nullptr}, 1.0, 1.0), false, false, "f_phx")))
-    return rc;
-  if ((rc = L.gemm(mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{nb.Pn, ZT, PS, nullptr},
-                      OperandW{Cb, T, TT, nullptr}, 1.0, 0.0), false, true, "c_phpl")))
-    return rc;
+  // stage 1 (independent products, one launch; H is exactly symmetric, so it
+  // is read row-major as the right factor):
+  //   X = B H_r,  Y = B^T H_l,  P_l H_l,  F = -P_r H_r
+  // stage 2 (one launch):
+  //   S -= Y X,  E -= Y P_l^T,  F += (P_l H_l) X,  C = (P_l H_l) P_l^T
+  {
+    ks::GemmGroup g1{};
+    g1.count = 4;
+    g1.p[0] = mk(S, S, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
+                 OperandW{Xb, S, XS, nullptr}, 1.0, 0.0);
+    g1.p[1] = mk(S, S, S, cnt, Operand{nb.BcT, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
+                 OperandW{Yb, S, XS, nullptr}, 1.0, 0.0);
+    g1.p[2] = mk(S, S, S, cnt, Operand{nb.Pn, ZT, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
+                 OperandW{nb.PHl, S, SS, nullptr}, 1.0, 0.0);
+    g1.p[3] = mk(S, S, S, cnt, Operand{nb.Pn + S, ZT, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
+                 OperandW{Fb, T, TT, nullptr}, -1.0, 0.0);
+    ++L.count[0];
+    if (cudaError_t e = ks::gemm_group(g1, st)) return fail(KS_ERR_CUDA, "assembly stage 1: %s", cudaGetErrorString(e));
+    if ((rc = L.check("assembly1"))) return rc;
+    const int64_t PTS = (int64_t)ZT * S;
+    ks::GemmGroup g2{};
+    g2.count = 4;
+    g2.p[0] = mk(S, S, S, cnt, Operand{Yb, S, XS, nullptr}, Operand{Xb, S, XS, nullptr}, OperandW{Sb, T, TT, nullptr},
+                 -1.0, 1.0);
+    g2.p[1] = mk(S, S, S, cnt, Operand{Yb, S, XS, nullptr}, Operand{nb.PT, S, PTS, nullptr},
+                 OperandW{Eb, T, TT, nullptr}, -1.0, 1.0);
+    g2.p[2] = mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{Xb, S, XS, nullptr},
+                 OperandW{Fb, T, TT, nullptr}, 1.0, 1.0);
+    g2.p[3] = mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{nb.PT, S, PTS, nullptr},
+                 OperandW{Cb, T, TT, nullptr}, 1.0, 0.0);
+    ++L.count[0];
+    if (cudaError_t e = ks::gemm_group(g2, st)) return fail(KS_ERR_CUDA, "assembly stage 2: %s", cudaGetErrorString(e));
+    if ((rc = L.check("assembly2"))) return rc;
+  }
   ks::launch_znorm1(nb, st);  // ||Z||_1 for the condition estimate (linalg.py:176)
   ++L.count[0];
   if ((rc = L.check("znorm1"))) return rc;
@@ -320,6 +327,8 @@ static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt) {
   s.XY = nb.XY + (int64_t)off * 2 * S * S;
   s.PHl = nb.PHl + (int64_t)off * S * S;
   s.Bc = nb.Bc + (int64_t)off * S * S;
+  s.BcT = nb.BcT + (int64_t)off * S * S;
+  s.PT = nb.PT + (int64_t)off * nb.zt * S;
   s.Pn = nb.Pn + (int64_t)off * S * nb.zt;
   s.piv = nb.piv + (int64_t)off * TP;
   s.norm1 = nb.norm1 + off;

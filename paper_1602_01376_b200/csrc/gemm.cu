@@ -54,7 +54,33 @@ cudaError_t dispatch(const GemmArgs& g, cudaStream_t st) {
   return launch<64, 64, 2, 2, TA, TB, 4>(g, st);
 }
 
+template <int BM, int BN, int WM, int WN, int STAGES>
+cudaError_t launch_group(const GemmGroup& gg, cudaStream_t st) {
+  using Cfg = GemmCfg<BM, BN, WM, WN, false, false, STAGES>;
+  auto kern = k_gemm_group<BM, BN, WM, WN, false, false, STAGES>;
+  if (cudaError_t e = ensure_smem(kern, Cfg::SMEM)) return e;
+  const GemmArgs& g = gg.p[0];
+  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.batch * gg.count);
+  launch_pdl(kern, grid, dim3(Cfg::THREADS), Cfg::SMEM, st, gg);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t gemm_group(const GemmGroup& gg, cudaStream_t st) {
+  if (gg.count < 1 || gg.count > kGroupMax) return cudaErrorInvalidValue;
+  const GemmArgs& g = gg.p[0];
+  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
+  for (int i = 0; i < gg.count; ++i) {
+    const GemmArgs& q = gg.p[i];
+    if (q.M != g.M || q.N != g.N || q.K != g.K || q.batch != g.batch || q.tri) return cudaErrorInvalidValue;
+    if (((q.M | q.N | q.K) & 1) || q.K <= 0 || ((q.A.ld | q.B.ld | q.C.ld) & 1)) return cudaErrorInvalidValue;
+  }
+  // the same shape choice as gemm() for these products (K = s_pad < 512)
+  const long tiles = (long)((g.M + 127) / 128) * ((g.N + 63) / 64) * g.batch * gg.count;
+  if (g.K >= 512 && tiles >= 2 * 148) return launch_group<128, 64, 2, 2, 3>(gg, st);
+  return launch_group<64, 64, 2, 2, 4>(gg, st);
+}
 
 cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st) {
   if ((g.K & 1) || (g.A.ld & 1) || (g.C.ld & 1)) return cudaErrorInvalidValue;

@@ -90,17 +90,13 @@ __device__ __forceinline__ void load_tile(double* dst, const double* src, int64_
   }
 }
 
+// One BM x BN output tile (m0, n0) of batch entry b.
 template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES, int EPI = 0>
-__global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
+__device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int n0, double* smem) {
   using Cfg = GemmCfg<BM, BN, WM, WN, TA, TB, STAGES>;
   constexpr int BK = Cfg::BK;
-  extern __shared__ __align__(16) double smem[];
-  pdl_wait();
   double* As = smem;
   double* Bs = smem + STAGES * Cfg::A_STAGE;
-
-  const int b = blockIdx.z;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   if (g.tri && n0 >= m0 + BM) return;
   const double* A = g.A.at(b);
   const double* B = g.B.at(b);
@@ -332,6 +328,32 @@ __global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
   }
 }
 
+template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES, int EPI = 0>
+__global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
+  extern __shared__ __align__(16) double smem[];
+  pdl_wait();
+  gemm_tile<BM, BN, WM, WN, TA, TB, STAGES, EPI>(g, blockIdx.z, blockIdx.y * BM, blockIdx.x * BN, smem);
+}
+
+// Up to kGroupMax independent batched GEMMs of the same shape (M, N, K, batch)
+// and transposes in one launch: grid.z = batch x problems. The node assembly
+// of the block formulation issues its four independent products per stage
+// this way (factorize.cu), one launch instead of four dependent ones.
+constexpr int kGroupMax = 4;
+struct GemmGroup {
+  GemmArgs p[kGroupMax];
+  int count;
+};
+
+template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
+__global__ void __launch_bounds__(WM* WN * 32) k_gemm_group(GemmGroup gg) {
+  extern __shared__ __align__(16) double smem[];
+  pdl_wait();
+  const int batch = gg.p[0].batch;
+  const int pi = blockIdx.z / batch, b = blockIdx.z - pi * batch;
+  gemm_tile<BM, BN, WM, WN, TA, TB, STAGES, 0>(gg.p[pi], b, blockIdx.y * BM, blockIdx.x * BN, smem);
+}
+
 // Host launcher: picks a tile shape for the problem; all dims must be even,
 // leading dimensions even and base pointers 16-byte aligned.
 cudaError_t gemm(const GemmArgs& g, bool ta, bool tb, cudaStream_t st);
@@ -342,6 +364,9 @@ cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st);
 cudaError_t gemm_small_tile(const GemmArgs& g, cudaStream_t st);
 // Panel update with the panel TRSM folded in (EPI == 2): N must be 64, op(B) = B^T.
 cudaError_t gemm_update_trsm(const GemmArgs& g, cudaStream_t st);
+// gg.count problems of one shape (M, N, K, batch, alpha/beta per problem), no
+// transposes, EPI 0, in one launch.
+cudaError_t gemm_group(const GemmGroup& gg, cudaStream_t st);
 // Gaussian cross-kernel row sums (EPI == 3), op(B) = B^T: partial sums per
 // 64-column tile; returns the number of column tiles through *tiles.
 cudaError_t gemm_krr(const GemmArgs& g, int* tiles, cudaStream_t st);

@@ -158,6 +158,7 @@ struct ks_factor {
   ksr::DBuf<double> lut;   // condition estimator: column-major copies of every node's Z factors (t_pad <= 512)
   ksr::DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
   ksr::DBuf<double> xy, phl;      // per internal node: X = B H_r and Y = B^T H_l; P_l H_l (the solve's up pass)
+  ksr::DBuf<double> bt, pt;       // per internal node: B^T, P^T (operands of the assembly GEMMs)
   ksr::DBuf<double> norm1_slab;   // scratch for the persistent LU's own column norms
   // solve workspaces (solve.cu): a pool of per-call workspaces; the sharded
   // solve phases (ks_solve_up / top / down, ks_node_exchange) keep theirs across calls
@@ -215,6 +216,8 @@ struct ks_factor {
     nb.zt = 0;
     nb.XY = nullptr;
     nb.PHl = nullptr;
+    nb.BcT = nullptr;
+    nb.PT = nullptr;
     nb.Aug = fb_aug.p;
     nb.Bc = nullptr;
     nb.Pn = nullptr;
@@ -283,6 +286,8 @@ struct ks_factor {
     nb.XY = xy.p + (int64_t)first * 2 * s_pad * s_pad;
     nb.PHl = phl.p + (int64_t)first * s_pad * s_pad;
     nb.Bc = bc.p + (int64_t)first * s_pad * s_pad;
+    nb.BcT = bt.p + (int64_t)first * s_pad * s_pad;
+    nb.PT = pt.p + (int64_t)first * zt * s_pad;
     nb.Pn = pn.p + (int64_t)first * s_pad * zt;
     nb.piv = piv.p + (int64_t)first * t_pad;
     nb.norm1 = norm1.p + first;
@@ -299,7 +304,8 @@ struct ks_factor {
     int_node.release(); int_left.release(); int_right.release(); int_info.release(); piv.release(); moves.release();
     pm.release(); lu_scratch.release(); lu_sync.release(); dinv.release(); lut.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
-    norm1.release(); cond.release(); xy.release(); phl.release(); norm1_slab.release();
+    norm1.release(); cond.release(); xy.release(); phl.release(); norm1_slab.release(); bt.release();
+    pt.release();
     fb_aug.release(); fb_norm1.release(); fb_cond.release(); fb_piv.release(); fb_info.release();
     fb_moves.release(); fb_pm.release(); fb_node.release(); fb_begin.release(); fb_size.release();
     for (auto& w : ws) {

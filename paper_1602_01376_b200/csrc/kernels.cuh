@@ -50,6 +50,8 @@ struct NodeBatch {
   double* XY;           // count x 2 x s_pad x s_pad: X = B H_r, then Y = B^T H_l
   double* PHl;          // count x s_pad x s_pad: P_l H_l
   double* Bc;           // count x s_pad x s_pad coupling blocks
+  double* BcT;          // count x s_pad x s_pad, B^T
+  double* PT;           // count x zt x s_pad, P^T (rows [0, s_pad): P_l^T, then P_r^T)
   double* Pn;           // count x s_pad x zt padded P
   int* piv;             // count x t_pad
   double* norm1;        // count

@@ -21,17 +21,20 @@
 
 namespace ks {
 
-// Coupling B = K(S_l, S_r) (compress.py:281-283), zero padded to s_pad^2.
+// Coupling B = K(S_l, S_r) (compress.py:281-283) and its transpose, zero
+// padded to s_pad^2: grid.z = 2 x nodes, the second half evaluates
+// K(S_r, S_l) into B^T (the difference form is symmetric bit for bit).
 __global__ void __launch_bounds__(256) k_coupling(DevTree t, NodeBatch nb) {
   pdl_wait();
-  const int k = blockIdx.z;
-  const int l = nb.left[k], r = nb.right[k];
+  const bool tr = blockIdx.z >= (unsigned)nb.count;
+  const int k = tr ? blockIdx.z - nb.count : blockIdx.z;
+  const int l = tr ? nb.right[k] : nb.left[k], r = tr ? nb.left[k] : nb.right[k];
   const int sl = t.rank[l], sr = t.rank[r];
   const int r0 = blockIdx.y * GT, c0 = blockIdx.x * GT;
   double sq[4][4];
   gauss_tile<true>(t, t.skel_pos + t.skel_off[l], 0, sl, t.skel_pos + t.skel_off[r], 0, sr, r0, c0, sq);
   const double den = -2.0 * t.h * t.h;
-  double* B = nb.Bc + (int64_t)k * nb.s_pad * nb.s_pad;
+  double* B = (tr ? nb.BcT : nb.Bc) + (int64_t)k * nb.s_pad * nb.s_pad;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -45,10 +48,9 @@ __global__ void __launch_bounds__(256) k_coupling(DevTree t, NodeBatch nb) {
 }
 
 void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
-  dim3 g(nb.s_pad / GT, nb.s_pad / GT, nb.count);
+  dim3 g(nb.s_pad / GT, nb.s_pad / GT, 2 * nb.count);
   launch_pdl(k_coupling, g, dim3(256), 0, st, t, nb);
 }
-
 
 // Padded candidate index i' of a node's P row maps to the reference's cand
 // index (cand = [skel_l; skel_r], compress.py:213): i' < s_pad -> i' (if < s_l),
@@ -79,8 +81,9 @@ __global__ void __launch_bounds__(256) k_aug2_init(DevTree t, NodeBatch nb) {
   }
 }
 
-// E = P_r^T (S x S at (0, S); the GEMMs then subtract Y P_l^T) through 32 x 32
-// shared-memory tiles: reads along P's rows, writes along Aug's rows
+// P^T (zt x S: rows [0, S) P_l^T, rows [S, 2S) P_r^T) and E = P_r^T (S x S at
+// (0, S) of Aug; the GEMMs then subtract Y P_l^T) through 32 x 32 shared-memory
+// tiles: reads along P's rows, writes along P^T's and Aug's rows
 __global__ void __launch_bounds__(256) k_aug2_pt(DevTree t, NodeBatch nb) {
   pdl_wait();
   __shared__ double tile[32][33];
@@ -89,23 +92,27 @@ __global__ void __launch_bounds__(256) k_aug2_pt(DevTree t, NodeBatch nb) {
   const int v = nb.node[k], sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]], sv = t.rank[v];
   const double* P = t.coeff + t.coeff_off[v];
   const int cand = sl + sr;
-  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;  // j: P row (parent skeleton), i: right-child index
+  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;  // j: P row (parent skeleton), i: padded cand index
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   {
-    const int i = i0 + tx;
+    const int ci = cand_index(i0 + tx, S, sl, sr);
     for (int jj = ty; jj < 32; jj += 8) {
       const int j = j0 + jj;
-      tile[jj][tx] = (i < sr && j < sv) ? P[(int64_t)j * cand + sl + i] : 0.0;
+      tile[jj][tx] = (ci >= 0 && j < sv) ? P[(int64_t)j * cand + ci] : 0.0;
     }
   }
   __syncthreads();
-  double* A = nb.Aug + (int64_t)k * T * T;
-  for (int ii = ty; ii < 32; ii += 8) A[(int64_t)(i0 + ii) * T + S + j0 + tx] = tile[tx][ii];
+  double* PT = nb.PT + (int64_t)k * nb.zt * S;
+  for (int ii = ty; ii < 32; ii += 8) PT[(int64_t)(i0 + ii) * S + j0 + tx] = tile[tx][ii];
+  if (i0 >= S) {
+    double* A = nb.Aug + (int64_t)k * T * T;
+    for (int ii = ty; ii < 32; ii += 8) A[(int64_t)(i0 - S + ii) * T + S + j0 + tx] = tile[tx][ii];
+  }
 }
 
 void launch_aug2_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
   launch_pdl(k_aug2_init, dim3(2 * nb.s_pad, nb.count), dim3(256), 0, st, t, nb);
-  launch_pdl(k_aug2_pt, dim3(nb.s_pad / 32, nb.s_pad / 32, nb.count), dim3(256), 0, st, t, nb);
+  launch_pdl(k_aug2_pt, dim3(nb.s_pad / 32, nb.zt / 32, nb.count), dim3(256), 0, st, t, nb);
 }
 
 // ||Z||_1 = max column abs sum of [[I, X], [Y, I]] (linalg.py:176): the columns
