@@ -119,22 +119,34 @@ void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, const double* l
 }
 
 // --------------------------------------------------------------------------
-// 64x64 diagonal-block Cholesky + triangular inverse (one CTA per leaf).
+// 64x64 diagonal-block Cholesky + triangular inverse (one CTA per leaf),
+// blocked by 16 columns so the critical path is ~20 barriers instead of one
+// per column:
+//   for each 16-column block kb: warp 0 factors the 16x16 diagonal block in
+//   registers (shuffles, _cholesky's column order within the block,
+//   linalg.py:185-196) and inverts it; all threads then form the block's rows
+//   below (L21 = A21 L11^-T) and update the trailing lower triangle;
+//   finally the off-diagonal blocks of X = L^-1 by block rows.
 // Failure (pivot <= 0 or non-finite) records the first bad column + 1, as
-// _cholesky raises NotSPDError at linalg.py:190-192.
+// _cholesky raises NotSPDError at linalg.py:190-192 (the block stays finite).
+// X lives transposed in the strict upper triangle of the tile (x[i][j] at
+// a[j][i], i > j) with its diagonal in xd.
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 6) k_potrf64(LeafBatch lb, int j0, double* inv, int* info) {
+__device__ __forceinline__ double potrf_x(const double (*a)[65], const double* xd, int r, int c) {
+  return r == c ? xd[r] : (r > c ? a[c][r] : 0.0);
+}
+
+__global__ void __launch_bounds__(256, 4) k_potrf64(LeafBatch lb, int j0, double* inv, int* info) {
   pdl_wait();
   const int leaf = blockIdx.x;
   double* A = lb.A + (int64_t)leaf * lb.a_stride + (int64_t)j0 * lb.m_pad + j0;
   const int64_t ld = lb.m_pad;
-  // one 64 x 65 tile: L in the lower triangle, X = L^-1 (also lower) stored
-  // transposed in the strict upper triangle (x[i][j] at a[j][i], i > j) with its
-  // diagonal in xd: 34 KB, so six CTAs share an SM
   extern __shared__ double potrf_sm[];
   double(*a)[65] = reinterpret_cast<double(*)[65]>(potrf_sm);
   double* xd = potrf_sm + 64 * 65;
+  double(*t)[17] = reinterpret_cast<double(*)[17]>(xd + 64);  // 48 x 17 scratch
   __shared__ int bad;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   {  // all 16 loads per thread in flight
     double v[16];
 #pragma unroll
@@ -147,81 +159,118 @@ __global__ void __launch_bounds__(256, 6) k_potrf64(LeafBatch lb, int j0, double
       const int e = threadIdx.x + u * 256, r = e >> 6, c = e & 63;
       a[r][c] = v[u];
     }
-    if (threadIdx.x < 64) xd[threadIdx.x] = 1.0;
   }
   if (threadIdx.x == 0) bad = 0x7fffffff;
   __syncthreads();
-  // symmetric right-looking elimination, one barrier per column:
-  //   a[i][j] -= a[i][k] a[j][k] / p_k  (k < j <= i),  p_k = a[k][k] at step k;
-  // afterwards L[k][k] = sqrt(p_k), L[i][k] = a[i][k] / sqrt(p_k)
-  // (_cholesky, linalg.py:185-196; a non-positive p_k is NotSPDError, :190-192)
-  // 1/p_k leaves the chain: the next pivot p_{k+1} = a[k+1][k+1] - a[k+1][k]^2/p_k
-  // is formed (by the thread that also writes it) and inverted at the start of
-  // step k, while the other threads update; rpiv[k] holds 1/p_k
-  __shared__ double rpiv[64];
-  if (threadIdx.x == 0) {
-    double p0 = a[0][0];
-    if (!(p0 > 0.0) || !isfinite(p0)) p0 = 1.0;  // recorded below; keep the block finite
-    rpiv[0] = 1.0 / p0;
-  }
-  __syncthreads();
-  for (int k = 0; k < 63; ++k) {
-    const double rp = rpiv[k];
-    const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
-    if (threadIdx.x == 0) {  // the same arithmetic as the (k+1, k+1) update below
-      const double l1 = a[k + 1][k] * rp;
-      double pn = fma(-l1, a[k + 1][k], a[k + 1][k + 1]);
-      if (!(pn > 0.0) || !isfinite(pn)) pn = 1.0;
-      rpiv[k + 1] = 1.0 / pn;
-    }
-    // 16 x 16 thread grid over the trailing lower triangle, no index division
-    for (int i = k + 1 + ti; i < 64; i += 16) {
-      const double li = a[i][k] * rp;
-      for (int j = k + 1 + tj; j <= i; j += 16) a[i][j] = fma(-li, a[j][k], a[i][j]);
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x < 64) {
-    const double p = a[threadIdx.x][threadIdx.x];
-    if (!(p > 0.0) || !isfinite(p)) atomicMin(&bad, (int)threadIdx.x);
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < 64 * 64; e += 256) {  // scale columns (diagonal last)
-    const int r = e >> 6, c = e & 63;
-    if (c >= r) continue;
-    double p = a[c][c];
-    if (!(p > 0.0) || !isfinite(p)) p = 1.0;
-    a[r][c] = a[r][c] / sqrt(p);
-  }
-  __syncthreads();
-  if (threadIdx.x < 64) {
-    double p = a[threadIdx.x][threadIdx.x];
-    if (!(p > 0.0) || !isfinite(p)) p = 1.0;
-    a[threadIdx.x][threadIdx.x] = sqrt(p);
-  }
-  __syncthreads();
-  // X = L^-1 right-looking: rows below k lose L[i][k] X[k] / L[k][k], then row
-  // k is scaled; one barrier per step. x[i][j] (i > j) lives at a[j][i].
-  if (threadIdx.x < 64) rpiv[threadIdx.x] = 1.0 / a[threadIdx.x][threadIdx.x];  // 1 / L[k][k], all at once
-  __syncthreads();
-  for (int k = 0; k < 64; ++k) {
-    const double rk = rpiv[k];
-    const int cols = k + 1;
-    const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
-    for (int i = k + 1 + ti; i < 64; i += 16) {
-      const double li = a[i][k] * rk;
-      for (int j = tj; j < cols; j += 16) {
-        const double xkj = (j == k) ? xd[k] : a[j][k];
-        a[j][i] = fma(-li, xkj, a[j][i]);
+#pragma unroll 1
+  for (int kb = 0; kb < 64; kb += 16) {
+    if (warp == 0) {
+      // (1) the 16 x 16 diagonal block: lane i < 16 owns row kb + i
+      double r[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) r[k] = (lane < 16 && k <= lane) ? a[kb + lane][kb + k] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        double p = __shfl_sync(0xffffffffu, r[j], j);
+        if (!(p > 0.0) || !isfinite(p)) {
+          if (lane == 0) atomicMin(&bad, kb + j);
+          p = 1.0;
+        }
+        const double lj = sqrt(p), rl = 1.0 / lj;
+        if (lane == j) r[j] = lj;
+        else if (lane > j) r[j] *= rl;
+#pragma unroll
+        for (int k = j + 1; k < 16; ++k) {
+          const double lkj = __shfl_sync(0xffffffffu, r[j], k);
+          if (lane >= k && lane < 16) r[k] = fma(-r[j], lkj, r[k]);
+        }
+      }
+      if (lane < 16) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k <= lane) a[kb + lane][kb + k] = r[k];
+      }
+      __syncwarp();
+      // inverse of the diagonal block: lane c < 16 solves column c of L11 x = e_c
+      if (lane < 16) {
+        const int c = lane;
+        double x[16];
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr) {
+          double s = (rr == c) ? 1.0 : 0.0;
+#pragma unroll
+          for (int k = 0; k < rr; ++k)
+            if (k >= c) s = fma(-a[kb + rr][kb + k], x[k], s);
+          x[rr] = (rr >= c) ? s / a[kb + rr][kb + rr] : 0.0;
+        }
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr) {
+          if (rr == c) xd[kb + c] = x[rr];
+          else if (rr > c) a[kb + c][kb + rr] = x[rr];
+        }
       }
     }
     __syncthreads();
-    if (threadIdx.x < cols) {
-      if (threadIdx.x == k) xd[k] *= rk;
-      else a[threadIdx.x][k] *= rk;
+    const int nr = 48 - kb;  // rows below the block
+    if (nr > 0) {
+      // (2) L21 = A21 L11^-T: t[r][j] = sum_{k <= j} A[kb+16+r][kb+k] X11[j][k]
+      for (int e = threadIdx.x; e < nr * 16; e += 256) {
+        const int rr = e >> 4, j = e & 15;
+        const double* ar = a[kb + 16 + rr] + kb;
+        double s = 0.0;
+        for (int k = 0; k <= j; ++k) s = fma(ar[k], potrf_x(a, xd, kb + j, kb + k), s);
+        t[rr][j] = s;
+      }
+      __syncthreads();
+      // (3) trailing lower triangle: a[r][c] -= sum_k L[r][k] L[c][k]; L21 back into a
+      for (int e = threadIdx.x; e < nr * nr; e += 256) {
+        const int rr = e / nr, cc = e - rr * nr;
+        if (cc > rr) continue;
+        double s = a[kb + 16 + rr][kb + 16 + cc];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) s = fma(-t[rr][k], t[cc][k], s);
+        a[kb + 16 + rr][kb + 16 + cc] = s;
+      }
+      for (int e = threadIdx.x; e < nr * 16; e += 256) a[kb + 16 + (e >> 4)][kb + (e & 15)] = t[e >> 4][e & 15];
+      __syncthreads();
     }
   }
-  __syncthreads();
+  // (4) off-diagonal blocks of X = L^-1 by block rows:
+  //     X[bi][bj] = -X[bi][bi] sum_{k = bj..bi-1} L[bi][k] X[k][bj]
+#pragma unroll 1
+  for (int bi = 1; bi < 4; ++bi) {
+    double(*tt)[16] = reinterpret_cast<double(*)[16]>(&t[0][0]);  // bi x 16 x 16 (<= 768 doubles)
+    for (int e = threadIdx.x; e < bi * 256; e += 256) {
+      const int bj = e >> 8, rl = (e >> 4) & 15, cl = e & 15;
+      const int r = bi * 16 + rl, c = bj * 16 + cl;
+      double s = 0.0;
+      for (int k = c; k < bi * 16; ++k) s = fma(a[r][k], potrf_x(a, xd, k, c), s);
+      tt[bj * 16 + rl][cl] = s;
+    }
+    __syncthreads();
+    double xo[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int e = threadIdx.x + u * 256;
+      xo[u] = 0.0;
+      if (e < bi * 256) {
+        const int bj = e >> 8, rl = (e >> 4) & 15, cl = e & 15;
+        double s = 0.0;
+        for (int m = 0; m <= rl; ++m) s = fma(potrf_x(a, xd, bi * 16 + rl, bi * 16 + m), tt[bj * 16 + m][cl], s);
+        xo[u] = -s;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int e = threadIdx.x + u * 256;
+      if (e < bi * 256) {
+        const int bj = e >> 8, rl = (e >> 4) & 15, cl = e & 15;
+        a[bj * 16 + cl][bi * 16 + rl] = xo[u];  // X[r][c] at a[c][r]
+      }
+    }
+    __syncthreads();
+  }
   double* iv = inv + ((int64_t)leaf * (lb.m_pad / 64) + j0 / 64) * 64 * 64;
 #pragma unroll 4
   for (int e = threadIdx.x; e < 64 * 64; e += 256) {
@@ -233,7 +282,7 @@ __global__ void __launch_bounds__(256, 6) k_potrf64(LeafBatch lb, int j0, double
 }
 
 void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStream_t st) {
-  constexpr size_t smem = (64 * 65 + 64) * sizeof(double);
+  constexpr size_t smem = (64 * 65 + 64 + 48 * 17) * sizeof(double);
   ensure_smem(k_potrf64, smem);
   launch_pdl(k_potrf64, dim3(lb.count), dim3(256), smem, st, lb, j0, inv, info);
 }
