@@ -245,6 +245,12 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(f->phl.alloc((size_t)f->n_int * f->s_pad * f->s_pad + 1));
     KS_CUDA(f->bt.alloc((size_t)f->n_int * f->s_pad * f->s_pad + 1));
     KS_CUDA(f->pt.alloc((size_t)f->n_int * f->zt * f->s_pad + 1));
+    // GEMM-form coupling where the dimension makes it worth it (2 s^2 d per node)
+    f->dk = (p->d >= 32) ? (int)roundup(p->d, 2) : 0;
+    if (f->dk) {
+      KS_CUDA(f->xs.alloc((size_t)f->n_int * f->zt * f->dk + 1));
+      KS_CUDA(f->xn.alloc((size_t)f->n_int * f->zt + 1));
+    }
     KS_CUDA(f->norm1_slab.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->norm1.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->cond.alloc(std::max(f->n_int, 1)));

@@ -329,6 +329,10 @@ static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt) {
   s.Bc = nb.Bc + (int64_t)off * S * S;
   s.BcT = nb.BcT + (int64_t)off * S * S;
   s.PT = nb.PT + (int64_t)off * nb.zt * S;
+  if (nb.XS) {
+    s.XS = nb.XS + (int64_t)off * nb.zt * nb.dk;
+    s.XN = nb.XN + (int64_t)off * nb.zt;
+  }
   s.Pn = nb.Pn + (int64_t)off * S * nb.zt;
   s.piv = nb.piv + (int64_t)off * TP;
   s.norm1 = nb.norm1 + off;

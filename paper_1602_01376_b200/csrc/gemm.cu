@@ -54,10 +54,10 @@ cudaError_t dispatch(const GemmArgs& g, cudaStream_t st) {
   return launch<64, 64, 2, 2, TA, TB, 4>(g, st);
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES>
+template <int BM, int BN, int WM, int WN, int STAGES, bool TB = false, int EPI = 0>
 cudaError_t launch_group(const GemmGroup& gg, cudaStream_t st) {
-  using Cfg = GemmCfg<BM, BN, WM, WN, false, false, STAGES>;
-  auto kern = k_gemm_group<BM, BN, WM, WN, false, false, STAGES>;
+  using Cfg = GemmCfg<BM, BN, WM, WN, false, TB, STAGES>;
+  auto kern = k_gemm_group<BM, BN, WM, WN, false, TB, STAGES, EPI>;
   if (cudaError_t e = ensure_smem(kern, Cfg::SMEM)) return e;
   const GemmArgs& g = gg.p[0];
   dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.batch * gg.count);
@@ -80,6 +80,18 @@ cudaError_t gemm_group(const GemmGroup& gg, cudaStream_t st) {
   const long tiles = (long)((g.M + 127) / 128) * ((g.N + 63) / 64) * g.batch * gg.count;
   if (g.K >= 512 && tiles >= 2 * 148) return launch_group<128, 64, 2, 2, 3>(gg, st);
   return launch_group<64, 64, 2, 2, 4>(gg, st);
+}
+
+cudaError_t gemm_group_coupling(const GemmGroup& gg, cudaStream_t st) {
+  if (gg.count < 1 || gg.count > kGroupMax) return cudaErrorInvalidValue;
+  const GemmArgs& g = gg.p[0];
+  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
+  for (int i = 0; i < gg.count; ++i) {
+    const GemmArgs& q = gg.p[i];
+    if (q.M != g.M || q.N != g.N || q.K != g.K || q.batch != g.batch) return cudaErrorInvalidValue;
+    if (((q.M | q.N | q.K) & 1) || q.K <= 0 || ((q.A.ld | q.B.ld | q.C.ld) & 1)) return cudaErrorInvalidValue;
+  }
+  return launch_group<64, 64, 2, 2, 4, true, 4>(gg, st);
 }
 
 cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st) {

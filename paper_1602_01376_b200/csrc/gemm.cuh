@@ -47,6 +47,20 @@ struct KrrEpi {
   double den;        // 1 / (-2 h h)
 };
 
+//   4  coupling block B = K(S_l, S_r) from the Gram product of gathered skeleton
+//      coordinates (kernels.py:107-111 in GEMM form, compress.py:281-283):
+//      C[r][c] = exp(max(xa_r + xb_c - 2G, 0) / (-2 h h)) for r < rank(na[b]),
+//      c < rank(nb[b]), else 0 (the zero padding to s_pad).
+struct CoupEpi {
+  const double* xa;   // squared norms of the A rows, per batch entry (stride xs)
+  const double* xb;   // squared norms of the B rows
+  int64_t xs;
+  const int* na;      // per batch: the node whose rank bounds the rows
+  const int* nbn;     // per batch: the node whose rank bounds the columns
+  const int* rank;    // ranks by node id
+  double den;         // 1 / (-2 h h)
+};
+
 struct GemmArgs {
   int M, N, K, batch;
   Operand A, B;
@@ -56,6 +70,7 @@ struct GemmArgs {
   GaussEpi ge;
   Operand E;  // EPI == 2: right factor of the epilogue product
   KrrEpi ke;  // EPI == 3
+  CoupEpi ce;  // EPI == 4
 };
 
 template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
@@ -251,6 +266,32 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
     }
     return;
   }
+  if constexpr (EPI == 4) {
+    double cf[12];
+    exp_coeffs(cf);
+    const int ra = g.ce.rank[g.ce.na[b]], rb = g.ce.rank[g.ce.nbn[b]];
+    const double* xa = g.ce.xa + (int64_t)b * g.ce.xs;
+    const double* xb = g.ce.xb + (int64_t)b * g.ce.xs;
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; ++i) {
+      const int r = m0 + wm0 + i * 8 + gq;
+      if (r >= g.M) continue;
+      const double xr = (r < ra) ? xa[r] : 0.0;
+#pragma unroll
+      for (int j = 0; j < Cfg::NT; ++j) {
+        const int c = n0 + wn0 + j * 8 + 2 * tq;
+        if (c >= g.N) continue;
+        double o[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int cc = c + u;
+          o[u] = (r < ra && cc < rb) ? exp_neg(fmax(xr + xb[cc] - 2.0 * acc[i][j][u], 0.0) * g.ce.den, cf) : 0.0;
+        }
+        *reinterpret_cast<double2*>(C + (int64_t)r * g.C.ld + c) = make_double2(o[0], o[1]);
+      }
+    }
+    return;
+  }
   double den = 0.0, lam = 0.0;
   int bsz = 0, bbeg = 0;
   if (EPI == 1) {
@@ -345,13 +386,13 @@ struct GemmGroup {
   int count;
 };
 
-template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
+template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES, int EPI = 0>
 __global__ void __launch_bounds__(WM* WN * 32) k_gemm_group(GemmGroup gg) {
   extern __shared__ __align__(16) double smem[];
   pdl_wait();
   const int batch = gg.p[0].batch;
   const int pi = blockIdx.z / batch, b = blockIdx.z - pi * batch;
-  gemm_tile<BM, BN, WM, WN, TA, TB, STAGES, 0>(gg.p[pi], b, blockIdx.y * BM, blockIdx.x * BN, smem);
+  gemm_tile<BM, BN, WM, WN, TA, TB, STAGES, EPI>(gg.p[pi], b, blockIdx.y * BM, blockIdx.x * BN, smem);
 }
 
 // Host launcher: picks a tile shape for the problem; all dims must be even,
@@ -367,6 +408,9 @@ cudaError_t gemm_update_trsm(const GemmArgs& g, cudaStream_t st);
 // gg.count problems of one shape (M, N, K, batch, alpha/beta per problem), no
 // transposes, EPI 0, in one launch.
 cudaError_t gemm_group(const GemmGroup& gg, cudaStream_t st);
+// Coupling blocks (EPI == 4): op(B) = B^T (the gathered skeleton coordinates
+// of both operands row-major, K = the padded dimension).
+cudaError_t gemm_group_coupling(const GemmGroup& gg, cudaStream_t st);
 // Gaussian cross-kernel row sums (EPI == 3), op(B) = B^T: partial sums per
 // 64-column tile; returns the number of column tiles through *tiles.
 cudaError_t gemm_krr(const GemmArgs& g, int* tiles, cudaStream_t st);

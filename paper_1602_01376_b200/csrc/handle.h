@@ -159,6 +159,8 @@ struct ks_factor {
   ksr::DBuf<double> leafA, inv, hbuf, aug, bc, pn, norm1, cond;
   ksr::DBuf<double> xy, phl;      // per internal node: X = B H_r and Y = B^T H_l; P_l H_l (the solve's up pass)
   ksr::DBuf<double> bt, pt;       // per internal node: B^T, P^T (operands of the assembly GEMMs)
+  ksr::DBuf<double> xs, xn;       // GEMM-form coupling (large d): gathered skeleton coordinates, norms
+  int dk = 0;                     // their padded dimension (0: difference-form coupling kernel)
   ksr::DBuf<double> norm1_slab;   // scratch for the persistent LU's own column norms
   // solve workspaces (solve.cu): a pool of per-call workspaces; the sharded
   // solve phases (ks_solve_up / top / down, ks_node_exchange) keep theirs across calls
@@ -218,6 +220,9 @@ struct ks_factor {
     nb.PHl = nullptr;
     nb.BcT = nullptr;
     nb.PT = nullptr;
+    nb.XS = nullptr;
+    nb.XN = nullptr;
+    nb.dk = 0;
     nb.Aug = fb_aug.p;
     nb.Bc = nullptr;
     nb.Pn = nullptr;
@@ -288,6 +293,9 @@ struct ks_factor {
     nb.Bc = bc.p + (int64_t)first * s_pad * s_pad;
     nb.BcT = bt.p + (int64_t)first * s_pad * s_pad;
     nb.PT = pt.p + (int64_t)first * zt * s_pad;
+    nb.XS = dk ? xs.p + (int64_t)first * zt * dk : nullptr;
+    nb.XN = dk ? xn.p + (int64_t)first * zt : nullptr;
+    nb.dk = dk;
     nb.Pn = pn.p + (int64_t)first * s_pad * zt;
     nb.piv = piv.p + (int64_t)first * t_pad;
     nb.norm1 = norm1.p + first;
@@ -305,7 +313,7 @@ struct ks_factor {
     pm.release(); lu_scratch.release(); lu_sync.release(); dinv.release(); lut.release();
     leafA.release(); inv.release(); hbuf.release(); aug.release(); bc.release(); pn.release();
     norm1.release(); cond.release(); xy.release(); phl.release(); norm1_slab.release(); bt.release();
-    pt.release();
+    pt.release(); xs.release(); xn.release();
     fb_aug.release(); fb_norm1.release(); fb_cond.release(); fb_piv.release(); fb_info.release();
     fb_moves.release(); fb_pm.release(); fb_node.release(); fb_begin.release(); fb_size.release();
     for (auto& w : ws) {

@@ -52,6 +52,9 @@ struct NodeBatch {
   double* Bc;           // count x s_pad x s_pad coupling blocks
   double* BcT;          // count x s_pad x s_pad, B^T
   double* PT;           // count x zt x s_pad, P^T (rows [0, s_pad): P_l^T, then P_r^T)
+  double* XS;           // count x zt x dk: gathered skeleton coordinates [left; right] (GEMM-form coupling), or null
+  double* XN;           // count x zt: their squared norms
+  int dk;               // padded dimension of XS (even)
   double* Pn;           // count x s_pad x zt padded P
   int* piv;             // count x t_pad
   double* norm1;        // count

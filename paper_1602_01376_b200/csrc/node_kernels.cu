@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #include "gauss.cuh"
+#include "gemm.cuh"
 #include "kernels.cuh"
 
 namespace ks {
@@ -47,7 +48,61 @@ __global__ void __launch_bounds__(256) k_coupling(DevTree t, NodeBatch nb) {
   }
 }
 
+// GEMM form for large d: the skeleton coordinates of both children gathered
+// into XS (zt rows of dk per node: [left; right], zero padded) with their
+// squared norms, then B = K(S_l, S_r) and B^T = K(S_r, S_l) as one grouped
+// DMMA Gram GEMM with the Gaussian epilogue (gemm.cuh EPI 4). The two products
+// sum the same terms in the same order, so B^T is B transposed bit for bit.
+__global__ void __launch_bounds__(256) k_gather_skel(DevTree t, NodeBatch nb) {
+  pdl_wait();
+  const int k = blockIdx.y, row = blockIdx.x;  // row < zt
+  const int S = nb.s_pad, dk = nb.dk;
+  const bool right = row >= S;
+  const int v = right ? nb.right[k] : nb.left[k], i = right ? row - S : row;
+  const int rk = t.rank[v];
+  double* out = nb.XS + ((int64_t)k * nb.zt + row) * dk;
+  __shared__ double red[8];
+  double s = 0.0;
+  if (i < rk) {
+    const double* x = t.coords + (int64_t)t.skel_pos[t.skel_off[v] + i] * t.d;
+    for (int c = threadIdx.x; c < dk; c += 256) {
+      const double xv = c < t.d ? x[c] : 0.0;
+      out[c] = xv;
+      s = fma(xv, xv, s);
+    }
+  } else {
+    for (int c = threadIdx.x; c < dk; c += 256) out[c] = 0.0;
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < 8; ++w) tot += red[w];
+    nb.XN[(int64_t)k * nb.zt + row] = tot;
+  }
+}
+
 void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
+  if (nb.XS) {
+    launch_pdl(k_gather_skel, dim3(nb.zt, nb.count), dim3(256), 0, st, t, nb);
+    const int S = nb.s_pad, dk = nb.dk;
+    const int64_t XSS = (int64_t)nb.zt * dk, SS = (int64_t)S * S;
+    GemmGroup gg{};
+    gg.count = 2;
+    for (int p = 0; p < 2; ++p) {
+      GemmArgs& g = gg.p[p];
+      g.M = S; g.N = S; g.K = dk; g.batch = nb.count;
+      g.A = Operand{nb.XS + (p ? (int64_t)S * dk : 0), dk, XSS, nullptr};
+      g.B = Operand{nb.XS + (p ? 0 : (int64_t)S * dk), dk, XSS, nullptr};
+      g.C = OperandW{p ? nb.BcT : nb.Bc, S, SS, nullptr};
+      g.alpha = 1.0; g.beta = 0.0; g.tri = 0;
+      g.ce = CoupEpi{nb.XN + (p ? S : 0), nb.XN + (p ? 0 : S), nb.zt, p ? nb.right : nb.left,
+                     p ? nb.left : nb.right, t.rank, 1.0 / (-2.0 * t.h * t.h)};
+    }
+    gemm_group_coupling(gg, st);
+    return;
+  }
   dim3 g(nb.s_pad / GT, nb.s_pad / GT, 2 * nb.count);
   launch_pdl(k_coupling, g, dim3(256), 0, st, t, nb);
 }

@@ -47,11 +47,8 @@ def main():
 
     cfg = CONFIGS[os.environ.get("CFG", "cfg3")]
     path = f"/tmp/ks_op_{cfg.name}.ksop"
-    if not os.path.exists(path):
-        import paper_1602_01376_b200 as ks
-        from producer import make_operator
-
-        ks.save_operator(make_operator(cfg, device="cuda"), path)
+    if not os.path.exists(path):  # in a child process: its GPU memory is gone before the workers run
+        subprocess.run([sys.executable, __file__, "--produce", cfg.name, path], check=True, timeout=1800)
     for setting in sys.argv[1:] or [""]:
         env = dict(os.environ)
         for kv in setting.split():
@@ -66,5 +63,11 @@ def main():
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "--worker":
         worker(sys.argv[2], float(sys.argv[3]), 7)
+    elif len(sys.argv) > 1 and sys.argv[1] == "--produce":
+        import paper_1602_01376_b200 as ks
+        from paper_1602_01376_b200.configs import CONFIGS
+        from producer import make_operator
+
+        ks.save_operator(make_operator(CONFIGS[sys.argv[2]], device="cuda"), sys.argv[3])
     else:
         main()
