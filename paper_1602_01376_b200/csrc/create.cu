@@ -305,8 +305,8 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     if (int rc = put(f->int_right, iright)) return rc;
     double* orig = nullptr;
     int64_t* pmd = nullptr;
-    KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&orig), sizeof(double) * p->n * p->d, u));
-    KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pmd), sizeof(int64_t) * p->n, u));
+    KS_CUDA(pool_alloc_async(reinterpret_cast<void**>(&orig), sizeof(double) * p->n * p->d, u));
+    KS_CUDA(pool_alloc_async(reinterpret_cast<void**>(&pmd), sizeof(int64_t) * p->n, u));
     KS_CUDA(cudaMemsetAsync(f->coords.p + (size_t)p->n * p->d, 0, sizeof(double) * f->m_pad * p->d, u));
     KS_CUDA(cudaMemcpyAsync(orig, p->coords, sizeof(double) * p->n * p->d, cudaMemcpyHostToDevice, u));
     KS_CUDA(cudaMemcpyAsync(pmd, p->perm, sizeof(int64_t) * p->n, cudaMemcpyHostToDevice, u));

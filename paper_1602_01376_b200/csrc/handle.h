@@ -71,6 +71,7 @@ double host_ms();
 
 // ---- device memory: the stream-ordered pool of the handle's device ----
 cudaError_t pool_alloc(void** p, size_t bytes);
+cudaError_t pool_alloc_async(void** p, size_t bytes, cudaStream_t st);  // stream-ordered, caller frees with cudaFreeAsync
 void pool_free(void* p);
 void pool_trim();  // give unused pool memory back to the driver (ks_destroy)
 

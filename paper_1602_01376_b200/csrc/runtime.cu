@@ -78,13 +78,14 @@ double host_ms() {
 
 // ---- device memory ----
 // Handle buffers come from a PRIVATE stream-ordered pool per device (not the
-// device's default pool, which other libraries share). It keeps up to
-// KS_POOL_GB (default 32, fractional values allowed) GB of freed memory, so a
-// handle created after another one was destroyed (a new factorize call on the
-// same shapes) reuses its memory instead of going back to the driver; the
-// cache is returned by ks_trim_pool() (Python: release_cached_memory()), or on
-// every ks_destroy with KS_POOL_GB=0. Frees keep the device-wide
-// synchronization cudaFree implies (buffers may be in use on any stream).
+// device's default pool, which other libraries share). Like torch's caching
+// allocator it keeps freed memory for the next handle by default (a new
+// factorize call on the same shapes then maps no new memory: at config 5,
+// ~80 GB of fresh mappings cost ~1 s); KS_POOL_GB caps what it keeps
+// (fractional values allowed; 0 returns everything on every ks_destroy), and
+// ks_trim_pool() (Python: release_cached_memory()) returns the cache to the
+// driver. Frees keep the device-wide synchronization cudaFree implies
+// (buffers may be in use on any stream).
 namespace {
 constexpr int kMaxDev = 64;
 std::mutex g_pool_mu;
@@ -92,7 +93,8 @@ cudaMemPool_t g_pool[kMaxDev] = {};
 
 double pool_keep_gb() {
   const char* env = std::getenv("KS_POOL_GB");
-  const double gb = env ? std::atof(env) : 32.0;
+  if (!env || !env[0]) return -1.0;  // keep everything
+  const double gb = std::atof(env);
   return gb > 0.0 ? gb : 0.0;
 }
 
@@ -110,7 +112,8 @@ cudaError_t pool_get(cudaMemPool_t* out) {
     props.location.id = dev;
     cudaMemPool_t pool;
     if ((e = cudaMemPoolCreate(&pool, &props)) != cudaSuccess) return e;
-    uint64_t keep = (uint64_t)(pool_keep_gb() * (double)(1ull << 30));
+    const double gb = pool_keep_gb();
+    uint64_t keep = gb < 0.0 ? UINT64_MAX : (uint64_t)(gb * (double)(1ull << 30));
     if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) return e;
     g_pool[dev] = pool;
   }
@@ -118,6 +121,13 @@ cudaError_t pool_get(cudaMemPool_t* out) {
   return cudaSuccess;
 }
 }  // namespace
+
+cudaError_t pool_alloc_async(void** p, size_t bytes, cudaStream_t st) {
+  cudaMemPool_t pool;
+  cudaError_t e = pool_get(&pool);
+  if (e != cudaSuccess) return e;
+  return cudaMallocFromPoolAsync(p, bytes, pool, st);
+}
 
 cudaError_t pool_alloc(void** p, size_t bytes) {
   cudaMemPool_t pool;
@@ -296,7 +306,7 @@ void ks_destroy(ks_factor* f) {
   for (auto e : f->ev_up_level)
     if (e) cudaEventDestroy(e);
   delete f;
-  if (pool_keep_gb() <= 0.0) pool_trim();
+  if (pool_keep_gb() == 0.0) pool_trim();
 }
 
 }  // extern "C"

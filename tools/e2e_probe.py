@@ -26,6 +26,7 @@ def main():
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     op = make_operator(cfg, device="cuda")
+    torch.cuda.empty_cache()  # the producer's cached blocks would crowd the library's pool
     pin, h2d = _pinned_problem(torch, op)
     prob = ks.from_arrays(pin)
     b = torch.from_numpy(make_rhs(cfg, op["perm"], 1)).pin_memory().numpy()
@@ -37,7 +38,8 @@ def main():
         h = C.c_void_p()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        assert lib.ks_create(C.byref(cp), 0, C.byref(h)) == 0
+        rc = lib.ks_create(C.byref(cp), 0, C.byref(h))
+        assert rc == 0, _lib.last_error()
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         assert lib.ks_factorize(h, cfg.lam, None) == 0
