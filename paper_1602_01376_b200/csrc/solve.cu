@@ -130,26 +130,52 @@ static int gemm_trsm(Launcher& L, bool upper, bool unit, const double* A, int64_
   return gemm_trsm(L, upper, unit, A, lda, sa, B, ldb, sb, h, ncols, batch);
 }
 
-// up pass at the leaves: z = L^-1 b (64-row blocks: GEMM update, then the block's
-// stored inverse), c = L21 z
+// Leaf triangular solves on q right-hand sides, recursively by row halves so
+// the off-diagonal updates are large GEMMs (rows [r0+h, r0+n) against the
+// solved half) instead of 64-row strips; 64-row diagonal blocks go through
+// their stored inverses (inv, from the leaf factorization).
+static int leaf_fwd_rec(ks_factor* f, SolveWs* w, Launcher& L, int r0, int n, int q) {
+  const int nl = (int)f->leaf_nodes.size(), M = f->m_pad;
+  const int64_t AS = (int64_t)f->R * M, ZS = (int64_t)M * q;
+  if (n == 64)
+    return L.gemm(mk(64, q, 64, nl, Operand{f->inv.p + (int64_t)(r0 / 64) * 4096, 64, (int64_t)M * 64, nullptr},
+                     Operand{w->z.p + (int64_t)r0 * q, q, ZS, nullptr}, OperandW{w->z.p + (int64_t)r0 * q, q, ZS, nullptr},
+                     1.0, 0.0), false, false);
+  const int h = (int)roundup(n / 2, 64);
+  if (int rc = leaf_fwd_rec(f, w, L, r0, h, q)) return rc;
+  // z[r0+h, r0+n) -= L[r0+h : r0+n, r0 : r0+h] z[r0, r0+h)
+  if (int rc = L.gemm(mk(n - h, q, h, nl, Operand{f->leafA.p + (int64_t)(r0 + h) * M + r0, M, AS, nullptr},
+                         Operand{w->z.p + (int64_t)r0 * q, q, ZS, nullptr},
+                         OperandW{w->z.p + (int64_t)(r0 + h) * q, q, ZS, nullptr}, -1.0, 1.0), false, false))
+    return rc;
+  return leaf_fwd_rec(f, w, L, r0 + h, n - h, q);
+}
+
+static int leaf_bwd_rec(ks_factor* f, SolveWs* w, Launcher& L, int r0, int n, int q) {
+  const int nl = (int)f->leaf_nodes.size(), M = f->m_pad;
+  const int64_t AS = (int64_t)f->R * M, ZS = (int64_t)M * q;
+  if (n == 64)
+    return L.gemm(mk(64, q, 64, nl, Operand{f->inv.p + (int64_t)(r0 / 64) * 4096, 64, (int64_t)M * 64, nullptr},
+                     Operand{w->z.p + (int64_t)r0 * q, q, ZS, nullptr}, OperandW{w->z.p + (int64_t)r0 * q, q, ZS, nullptr},
+                     1.0, 0.0), true, false);
+  const int h = (int)roundup(n / 2, 64);
+  if (int rc = leaf_bwd_rec(f, w, L, r0 + h, n - h, q)) return rc;
+  // z[r0, r0+h) -= L[r0+h : r0+n, r0 : r0+h]^T z[r0+h, r0+n)
+  if (int rc = L.gemm(mk(h, q, n - h, nl, Operand{f->leafA.p + (int64_t)(r0 + h) * M + r0, M, AS, nullptr},
+                         Operand{w->z.p + (int64_t)(r0 + h) * q, q, ZS, nullptr},
+                         OperandW{w->z.p + (int64_t)r0 * q, q, ZS, nullptr}, -1.0, 1.0), true, false))
+    return rc;
+  return leaf_bwd_rec(f, w, L, r0, h, q);
+}
+
+// up pass at the leaves: z = L^-1 b, c = L21 z
 static int leaf_up_gemm(ks_factor* f, SolveWs* w, Launcher& L, const double* Bd, int q) {
   const ks::LeafBatch lb = f->leafbatch();
   const int nl = lb.count, M = f->m_pad, S = f->s_pad;
   const int64_t AS = lb.a_stride, ZS = (int64_t)M * q;
   ks::launch_leaf_gather(lb, Bd, q, w->z.p, q, L.st);
   ++*L.count;
-  for (int r0 = 0; r0 < M; r0 += 64) {
-    int rc;
-    if (r0 > 0) {
-      rc = L.gemm(mk(64, q, r0, nl, Operand{f->leafA.p + (int64_t)r0 * M, M, AS, nullptr}, Operand{w->z.p, q, ZS, nullptr},
-                     OperandW{w->z.p + (int64_t)r0 * q, q, ZS, nullptr}, -1.0, 1.0), false, false);
-      if (rc) return rc;
-    }
-    rc = L.gemm(mk(64, q, 64, nl, Operand{f->inv.p + (int64_t)(r0 / 64) * 4096, 64, (int64_t)M * 64, nullptr},
-                   Operand{w->z.p + (int64_t)r0 * q, q, ZS, nullptr}, OperandW{w->z.p + (int64_t)r0 * q, q, ZS, nullptr},
-                   1.0, 0.0), false, false);
-    if (rc) return rc;
-  }
+  if (int rc = leaf_fwd_rec(f, w, L, 0, M, q)) return rc;
   if (S > 0 && f->n_nodes > 1)
     return L.gemm(mk(S, q, M, nl, Operand{f->leafA.p + (int64_t)M * M, M, AS, nullptr}, Operand{w->z.p, q, ZS, nullptr},
                      OperandW{w->c.p, q, (int64_t)S * q, lb.node}, 1.0, 0.0), false, false);
@@ -161,25 +187,13 @@ static int leaf_down_gemm(ks_factor* f, SolveWs* w, Launcher& L, double* Xd, int
   const ks::LeafBatch lb = f->leafbatch();
   const int nl = lb.count, M = f->m_pad, S = f->s_pad;
   const int64_t AS = lb.a_stride, ZS = (int64_t)M * q;
-  int rc;
   if (S > 0 && f->n_nodes > 1) {
-    rc = L.gemm(mk(M, q, S, nl, Operand{f->leafA.p + (int64_t)M * M, M, AS, nullptr},
-                   Operand{w->tin.p, q, (int64_t)S * q, lb.node}, OperandW{w->z.p, q, ZS, nullptr}, -1.0, 1.0),
-                true, false);
-    if (rc) return rc;
+    if (int rc = L.gemm(mk(M, q, S, nl, Operand{f->leafA.p + (int64_t)M * M, M, AS, nullptr},
+                           Operand{w->tin.p, q, (int64_t)S * q, lb.node}, OperandW{w->z.p, q, ZS, nullptr}, -1.0, 1.0),
+                        true, false))
+      return rc;
   }
-  for (int r0 = M - 64; r0 >= 0; r0 -= 64) {
-    if (r0 + 64 < M) {
-      rc = L.gemm(mk(64, q, M - r0 - 64, nl, Operand{f->leafA.p + (int64_t)(r0 + 64) * M + r0, M, AS, nullptr},
-                     Operand{w->z.p + (int64_t)(r0 + 64) * q, q, ZS, nullptr},
-                     OperandW{w->z.p + (int64_t)r0 * q, q, ZS, nullptr}, -1.0, 1.0), true, false);
-      if (rc) return rc;
-    }
-    rc = L.gemm(mk(64, q, 64, nl, Operand{f->inv.p + (int64_t)(r0 / 64) * 4096, 64, (int64_t)M * 64, nullptr},
-                   Operand{w->z.p + (int64_t)r0 * q, q, ZS, nullptr}, OperandW{w->z.p + (int64_t)r0 * q, q, ZS, nullptr},
-                   1.0, 0.0), true, false);
-    if (rc) return rc;
-  }
+  if (int rc = leaf_bwd_rec(f, w, L, 0, M, q)) return rc;
   ks::launch_leaf_scatter(lb, w->z.p, Xd, q, q, L.st);
   ++*L.count;
   return KS_OK;
