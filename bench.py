@@ -466,9 +466,9 @@ def run_ours(args) -> None:
     cpu = cpu_baseline() if not args.no_cpu else None
     B_solve = yardstick.solve_bytes(op, 1)
     # DRAM bytes per factorization / per q=1 solve from the committed ncu capture
-    # (profiles/r01_dram_traffic.json: cold caches, an upper bound), config 3 only
+    # (profiles/r02_dram_traffic.json: cold caches, an upper bound), config 3 only
     traffic = {}
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_dram_traffic.json")
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_dram_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             tj = json.load(fh)
