@@ -1,4 +1,6 @@
 // Tile-shape selection and instantiation of the batched DMMA GEMM.
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 
 #include "gemm.cuh"
@@ -7,11 +9,58 @@ namespace ks {
 
 namespace {
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+bool tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("KS_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// 3-D map (K, rows, batch) of a row-major operand with K contiguous; boxes of
+// 16 x box_rows with the 128-byte swizzle (gemm.cuh swz128)
+bool encode_operand(CUtensorMap* m, const Operand& o, int rows, int K, int batch, int box_rows) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
+  if (!enc || o.idx || !o.ptr) return false;
+  if ((reinterpret_cast<uintptr_t>(o.ptr) & 15) || (o.ld & 1) || o.ld < K) return false;
+  int64_t bstride = o.stride;
+  if (batch == 1 && bstride == 0) bstride = o.ld * rows;
+  if (bstride <= 0 || (bstride & 1)) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)o.ld * 8, (cuuint64_t)bstride * 8};
+  const cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(o.ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES, int EPI = 0>
-cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
+cudaError_t launch(const GemmArgs& g0, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, WM, WN, TA, TB, STAGES>;
   auto kern = k_gemm<BM, BN, WM, WN, TA, TB, STAGES, EPI>;
   constexpr size_t smem = (EPI == 2 && Cfg::SMEM_EPI2 > Cfg::SMEM) ? Cfg::SMEM_EPI2 : Cfg::SMEM;
+  static_assert(Cfg::SMEM >= (size_t)STAGES * (BM + BN) * Cfg::BK * 8 + 1024 + 8 * STAGES, "TMA ring fits");
+  GemmArgs g = g0;
+  g.use_tma = 0;
+  if constexpr (!TA && TB) {  // TMA tiles where both operands are strided batches
+    if (tma_enabled() && encode_operand(&g.tma_a, g.A, g.M, g.K, g.batch, BM) &&
+        encode_operand(&g.tma_b, g.B, g.N, g.K, g.batch, BN))
+      g.use_tma = 1;
+  }
   if (cudaError_t e = ensure_smem(kern, smem)) return e;
   dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.batch);
   launch_pdl(kern, grid, dim3(Cfg::THREADS), smem, st, g);

@@ -13,6 +13,8 @@
 // is bank-conflict free: a leading dimension == 4 (mod 16) doubles.
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace ks {
@@ -71,6 +73,11 @@ struct GemmArgs {
   Operand E;  // EPI == 2: right factor of the epilogue product
   KrrEpi ke;  // EPI == 3
   CoupEpi ce;  // EPI == 4
+  // TMA operand tiles (set by the host launcher for op(A) = A, op(B) = B^T with
+  // strided, 16-byte aligned batches): 3-D tensor maps (K, rows, batch), boxes
+  // of 16 x rows, 128-byte swizzle
+  int use_tma;
+  CUtensorMap tma_a, tma_b;
 };
 
 template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES>
@@ -88,6 +95,36 @@ struct GemmCfg {
   static constexpr size_t SMEM_EPI2 = (size_t)(BM + BN) * T_LD * sizeof(double);
   static_assert(A_LD % 16 == 4 && B_LD % 16 == 4, "conflict-free fragment loads need ld = 4 mod 16");
 };
+
+// ---- TMA (cp.async.bulk.tensor) + mbarrier helpers ----
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_inval(uint32_t bar) { asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar)); }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// box (16 doubles of K) x rows at (k0, r0, batch) of the 3-D map into dst (1024-byte aligned)
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int k0, int r0, int b, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(k0), "r"(r0), "r"(b), "r"(bar)
+      : "memory");
+}
+// element (r, k) of a 16-wide row-major tile stored with the 128-byte swizzle
+// (16-byte chunk c of row r at chunk c ^ (r & 7)), in doubles from the tile base
+__device__ __forceinline__ int swz128(int r, int k) { return r * 16 + ((((k >> 1) ^ (r & 7)) << 1) | (k & 1)); }
 
 template <int ROWS, int COLS, int LD, int THREADS>
 __device__ __forceinline__ void load_tile(double* dst, const double* src, int64_t ld, int r0, int c0,
@@ -128,6 +165,66 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
     for (int j = 0; j < Cfg::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int KT = (g.K + BK - 1) / BK;
+  bool tma_done = false;
+  if constexpr (!TA && TB) {
+    if (g.use_tma) {
+      // TMA ring: thread 0 arms a stage's mbarrier with its byte count and issues
+      // the A and B boxes; every warp waits on the barrier's phase, computes, and
+      // the barrier at the top of the next step frees the stage for its refill.
+      const uint32_t sbase = (smem_u32(smem) + 1023u) & ~1023u;
+      constexpr uint32_t A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8;
+      const uint32_t bar0 = sbase + STAGES * (A_BYTES + B_BYTES);
+      const double* sgen = smem + (sbase - smem_u32(smem)) / 8;  // generic pointer of sbase
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) mbar_init(bar0 + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      __syncthreads();
+      auto issue_tma = [&](int stage, int kt) {
+        const uint32_t bar = bar0 + 8 * stage;
+        mbar_expect_tx(bar, A_BYTES + B_BYTES);
+        tma_load_3d(sbase + stage * (A_BYTES + B_BYTES), &g.tma_a, kt * BK, m0, b, bar);
+        tma_load_3d(sbase + stage * (A_BYTES + B_BYTES) + A_BYTES, &g.tma_b, kt * BK, n0, b, bar);
+      };
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES - 1; ++s)
+          if (s < KT) issue_tma(s, s);
+      }
+      for (int kt = 0; kt < KT; ++kt) {
+        const int stage = kt % STAGES;
+        __syncthreads();  // every warp is done with the stage refilled below
+        if (threadIdx.x == 0) {
+          const int nk = kt + STAGES - 1;
+          if (nk < KT) issue_tma(nk % STAGES, nk);
+        }
+        mbar_wait(bar0 + 8 * stage, (uint32_t)((kt / STAGES) & 1));
+        const double* as = sgen + stage * (A_BYTES + B_BYTES) / 8;
+        const double* bs = as + A_BYTES / 8;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+          double af[Cfg::MT], bf[Cfg::NT];
+#pragma unroll
+          for (int i = 0; i < Cfg::MT; ++i) af[i] = as[swz128(wm0 + i * 8 + gq, kk + tq)];
+#pragma unroll
+          for (int j = 0; j < Cfg::NT; ++j) bf[j] = bs[swz128(wn0 + j * 8 + gq, kk + tq)];
+#pragma unroll
+          for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+            for (int j = 0; j < Cfg::NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+      }
+      __syncthreads();  // all stages consumed: the barriers' memory may be reused
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) mbar_inval(bar0 + 8 * s);
+      }
+      __syncthreads();
+      tma_done = true;
+    }
+  }
+  if (!tma_done) {
   auto issue = [&](int stage, int kt) {
     const int k0 = kt * BK;
     double* as = As + stage * Cfg::A_STAGE;
@@ -178,7 +275,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
     }
   }
   cp_async_wait<0>();
-
+  }
   const double alpha = g.alpha, beta = g.beta;
   if constexpr (EPI == 2) {
     constexpr int TL = Cfg::T_LD;
@@ -370,7 +467,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
 }
 
 template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES, int EPI = 0>
-__global__ void __launch_bounds__(WM* WN * 32) k_gemm(GemmArgs g) {
+__global__ void __launch_bounds__(WM* WN * 32) k_gemm(const __grid_constant__ GemmArgs g) {
   extern __shared__ __align__(16) double smem[];
   pdl_wait();
   gemm_tile<BM, BN, WM, WN, TA, TB, STAGES, EPI>(g, blockIdx.z, blockIdx.y * BM, blockIdx.x * BN, smem);
@@ -387,7 +484,7 @@ struct GemmGroup {
 };
 
 template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES, int EPI = 0>
-__global__ void __launch_bounds__(WM* WN * 32) k_gemm_group(GemmGroup gg) {
+__global__ void __launch_bounds__(WM* WN * 32) k_gemm_group(const __grid_constant__ GemmGroup gg) {
   extern __shared__ __align__(16) double smem[];
   pdl_wait();
   const int batch = gg.p[0].batch;
