@@ -363,7 +363,7 @@ def run_ours(args) -> None:
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or args.sharded:
         return run_multi(args)
     torch.cuda.set_device(local)
     cfg = CONFIGS[args.config]
@@ -578,7 +578,9 @@ def run_multi(args) -> None:
     if torch.cuda.device_count() <= local:
         raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but only {torch.cuda.device_count()} visible GPU(s)")
     torch.cuda.set_device(local)
-    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    # the transport NCCL picks (NVLS, P2P over NVLink) goes to a log file, summarized in the JSON line
+    if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+        os.environ["NCCL_DEBUG"] = "INFO"
     os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/ks_nccl.%h.%p.log")
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[args.config]
@@ -719,6 +721,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--ref-worker", default=None, help=argparse.SUPPRESS)
+    # the sharded (multi-GPU) code path on a single rank (under torchrun with 1 process): a check of
+    # run_multi where only one GPU is available
+    ap.add_argument("--sharded", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.ref_worker:
         ref_worker(args.ref_worker, args.steps, args.warmup)
