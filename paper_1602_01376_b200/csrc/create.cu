@@ -263,6 +263,9 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_join2, cudaEventDisableTiming));
     KS_CUDA(cudaStreamCreateWithFlags(&f->cap, cudaStreamNonBlocking));
     for (auto& g : f->gst) KS_CUDA(cudaStreamCreateWithFlags(&g, cudaStreamNonBlocking));
+    for (auto& g : f->hst) KS_CUDA(cudaStreamCreateWithFlags(&g, cudaStreamNonBlocking));
+    for (auto& e : f->hfork) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : f->hjoin) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     KS_CUDA(cudaEventCreateWithFlags(&f->gfork, cudaEventDisableTiming));
     for (auto& e : f->gjoin) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : f->ev_phase) KS_CUDA(cudaEventCreate(&e));

@@ -155,11 +155,14 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   // group waits only for the uploads of its own P blocks
   if (f->upload_pending) KS_CUDA(cudaStreamWaitEvent(st, f->ev_up_coords, 0));
   if (int rc = L.check("start")) return rc;
-  bool pipe = false;
+  bool pipe = false, early = false;
+  int n_early = 0;
   if (int rc = mark(f->ev_phase[1])) return rc;
   {
     const int G = (nl >= 2 * 64) ? n_groups(f) : 1;
     pipe = pipelined(f, G);
+    early = pipe && f->knobs.hager_early && !trace_on();
+    n_early = early ? G : 0;
     if (G > 1) {
       KS_CUDA(cudaEventRecord(f->gfork, st));
       for (int g = 0; g < G; ++g) KS_CUDA(cudaStreamWaitEvent(f->gst[g], f->gfork, 0));
@@ -182,7 +185,14 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
           f->cur_tag = lev;
           const ks::NodeBatch nb = f->nodebatch(lev);
           const int c = nb.count / G;
-          if (int rc = enqueue_level_body(f, Lg, sub_batch(nb, g * c, c), false)) return rc;
+          const ks::NodeBatch sb = sub_batch(nb, g * c, c);
+          if (int rc = enqueue_level_body(f, Lg, sb, false)) return rc;
+          if (early) {  // this subtree's estimates at once, beside its next level
+            KS_CUDA(cudaEventRecord(f->hfork[g], gs));
+            KS_CUDA(cudaStreamWaitEvent(f->hst[g], f->hfork[g], 0));
+            ks::launch_hager(dt, sb, f->dinv.p, f->lut.p, std::max(1, f->knobs.hager_ctas / G), f->hst[g]);
+            L.count[0] += ks::hager_launches(sb);
+          }
         }
         f->cur_tag = -1;
       }
@@ -198,7 +208,12 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   if (int rc = mark(f->ev_phase[3])) return rc;
   // ---- the shard's internal levels, deepest first (the pipelined ones are
   // done; their condition estimates are still to be launched) ----
-  if (int rc = enqueue_levels(f, st, L, pipe ? f->npipe : 0, f->n_local_levels, pipe ? f->npipe : 0)) return rc;
+  if (int rc = enqueue_levels(f, st, L, pipe ? f->npipe : 0, f->n_local_levels, (pipe && !early) ? f->npipe : 0))
+    return rc;
+  for (int g = 0; g < n_early; ++g) {
+    KS_CUDA(cudaEventRecord(f->hjoin[g], f->hst[g]));
+    KS_CUDA(cudaStreamWaitEvent(st, f->hjoin[g], 0));
+  }
   if (int rc = mark(f->ev_phase[4])) return rc;
   return KS_OK;
 }

@@ -59,6 +59,7 @@ struct Knobs {
   int hager_ctas = 96;         // KS_HAGER_CTAS: CTAs of the deferred wide-level estimates
   int hager_flush = 0;         // KS_HAGER_FLUSH: start the deferred estimates at levels <= n nodes
   bool hager_split = true;     // KS_HAGER_SPLIT=0: narrow-level estimates queue with the wide ones
+  bool hager_early = false;    // KS_HAGER_EARLY=1: a pipelined level's estimates right after each subtree's level
   bool force_leaf_lu = false;  // KS_FORCE_LEAF_LU=1: test hook, every leaf takes the LU path
   int graph = 1;               // KS_GRAPH: 1 graph replay from the 2nd factorization, 2 always, 0 never
 };
@@ -178,6 +179,9 @@ struct ks_factor {
   static constexpr int kGroups = 8;  // stream slots; KS_GROUPS picks how many are used (default 8)
   cudaStream_t gst[kGroups] = {};
   cudaEvent_t gfork = nullptr, gjoin[kGroups] = {};
+  // per-group condition-estimate streams (KS_HAGER_EARLY)
+  cudaStream_t hst[kGroups] = {};
+  cudaEvent_t hfork[kGroups] = {}, hjoin[kGroups] = {};
   cudaEvent_t ev_phase[5] = {};
   std::vector<cudaEvent_t> ev_level;
   cudaGraphExec_t graph_exec = nullptr;

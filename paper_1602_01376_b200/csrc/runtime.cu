@@ -52,6 +52,7 @@ Knobs read_knobs() {
   k.hager_ctas = std::max(1, env_int("KS_HAGER_CTAS", k.hager_ctas));
   k.hager_flush = env_int("KS_HAGER_FLUSH", k.hager_flush);
   k.hager_split = env_flag("KS_HAGER_SPLIT", k.hager_split);
+  k.hager_early = env_flag("KS_HAGER_EARLY", k.hager_early);
   k.force_leaf_lu = env_flag("KS_FORCE_LEAF_LU", false);
   k.graph = env_int("KS_GRAPH", k.graph);
   return k;
@@ -286,6 +287,12 @@ void ks_destroy(ks_factor* f) {
   if (f->cap) cudaStreamDestroy(f->cap);
   for (auto g : f->gst)
     if (g) cudaStreamDestroy(g);
+  for (auto g : f->hst)
+    if (g) cudaStreamDestroy(g);
+  for (auto e : f->hfork)
+    if (e) cudaEventDestroy(e);
+  for (auto e : f->hjoin)
+    if (e) cudaEventDestroy(e);
   if (f->gfork) cudaEventDestroy(f->gfork);
   for (auto e : f->gjoin)
     if (e) cudaEventDestroy(e);
