@@ -50,7 +50,7 @@ inline int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 struct Knobs {
   int slab_max = 4;            // KS_SLAB_MAX: levels with <= this many nodes run the persistent LU
   int spine_max = 16;          // KS_SPINE_MAX: batches <= this carry P^T on the recursive LU's spine
-  int groups = 4;              // KS_GROUPS: leaf groups / subtree streams
+  int groups = 8;              // KS_GROUPS: leaf groups / subtree streams
   bool pipe = true;            // KS_PIPE=0: join the groups after the leaves
   int pipe_min = 16;           // KS_PIPE_MIN: nodes per subtree for a level to be pipelined
   int panel_w = 0;             // KS_PANEL_W: 32 / 8 override the register-panel width
