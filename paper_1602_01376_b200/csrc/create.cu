@@ -341,13 +341,20 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
       r1 = a1;
       return KS_OK;
     };
+    // every leaf's P first (the leaf phase is the bulk of the work: with the
+    // uploads gating it, it should start everywhere as early as possible), then
+    // the pipelined levels' P subtree by subtree, then the remaining levels
+    // (measured at config 3: end-to-end factorize 83 -> 79.5 ms; the reverse
+    // subtree order measured 81.5 ms)
     for (int c = 0; c < ks_factor::kLeafChunks; ++c) {
       const size_t l0 = nl * c / ks_factor::kLeafChunks, l1 = nl * (c + 1) / ks_factor::kLeafChunks;
       for (size_t li = l0; li < l1; ++li)
         if (int rc = add(f->leaf_nodes[li])) return rc;
       if (int rc = flush()) return rc;
       KS_CUDA(cudaEventRecord(f->ev_up_leaf[c], u));
-      // with subtree pipelining: then this subtree's nodes of the pipelined levels
+    }
+    for (int c = 0; c < ks_factor::kLeafChunks; ++c) {
+      // with subtree pipelining: this subtree's nodes of the pipelined levels
       for (int lev = 0; lev < f->npipe; ++lev) {
         const auto& lv = f->levels[lev];
         const size_t c0 = lv.size() * c / ks_factor::kLeafChunks, c1 = lv.size() * (c + 1) / ks_factor::kLeafChunks;
