@@ -30,22 +30,24 @@ bool tma_enabled() {
   return on;
 }
 
-// 3-D map (K, rows, batch) of a row-major operand with K contiguous; boxes of
-// 16 x box_rows with the 128-byte swizzle (gemm.cuh swz128)
-bool encode_operand(CUtensorMap* m, const Operand& o, int rows, int K, int batch, int box_rows) {
+// 3-D map (cols, rows, batch) of a row-major operand: boxes of box_cols x
+// box_rows. cols = K with 16-wide boxes and the 128-byte swizzle (gemm.cuh
+// swz128) for A and B^T; cols = N with 8-wide unswizzled boxes for B.
+bool encode_operand(CUtensorMap* m, const Operand& o, int rows, int cols, int batch, int box_cols, int box_rows,
+                    bool swizzle) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
   if (!enc || o.idx || !o.ptr) return false;
-  if ((reinterpret_cast<uintptr_t>(o.ptr) & 15) || (o.ld & 1) || o.ld < K) return false;
+  if ((reinterpret_cast<uintptr_t>(o.ptr) & 15) || (o.ld & 1) || o.ld < cols) return false;
   int64_t bstride = o.stride;
   if (batch == 1 && bstride == 0) bstride = o.ld * rows;
   if (bstride <= 0 || (bstride & 1)) return false;
-  const cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)batch};
   const cuuint64_t strides[2] = {(cuuint64_t)o.ld * 8, (cuuint64_t)bstride * 8};
-  const cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
   const cuuint32_t es[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(o.ptr), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int BM, int BN, int WM, int WN, bool TA, bool TB, int STAGES, int EPI = 0>
@@ -56,9 +58,10 @@ cudaError_t launch(const GemmArgs& g0, cudaStream_t st) {
   static_assert(Cfg::SMEM >= (size_t)STAGES * (BM + BN) * Cfg::BK * 8 + 1024 + 8 * STAGES, "TMA ring fits");
   GemmArgs g = g0;
   g.use_tma = 0;
-  if constexpr (!TA && TB) {  // TMA tiles where both operands are strided batches
-    if (tma_enabled() && encode_operand(&g.tma_a, g.A, g.M, g.K, g.batch, BM) &&
-        encode_operand(&g.tma_b, g.B, g.N, g.K, g.batch, BN))
+  if constexpr (!TA) {  // TMA tiles where both operands are strided batches
+    if (tma_enabled() && encode_operand(&g.tma_a, g.A, g.M, g.K, g.batch, 16, BM, true) &&
+        (TB ? encode_operand(&g.tma_b, g.B, g.N, g.K, g.batch, 16, BN, true)
+            : encode_operand(&g.tma_b, g.B, g.K, g.N, g.batch, 8, 16, false)))
       g.use_tma = 1;
   }
   if (cudaError_t e = ensure_smem(kern, smem)) return e;
@@ -109,8 +112,15 @@ cudaError_t launch_group(const GemmGroup& gg, cudaStream_t st) {
   auto kern = k_gemm_group<BM, BN, WM, WN, false, TB, STAGES, EPI>;
   if (cudaError_t e = ensure_smem(kern, Cfg::SMEM)) return e;
   const GemmArgs& g = gg.p[0];
+  GemmGroup gt = gg;
+  for (int i = 0; i < gt.count; ++i) {  // TMA per problem where both operands are strided batches
+    GemmArgs& q = gt.p[i];
+    q.use_tma = tma_enabled() && encode_operand(&q.tma_a, q.A, q.M, q.K, q.batch, 16, BM, true) &&
+                (TB ? encode_operand(&q.tma_b, q.B, q.N, q.K, q.batch, 16, BN, true)
+                    : encode_operand(&q.tma_b, q.B, q.K, q.N, q.batch, 8, 16, false));
+  }
   dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.batch * gg.count);
-  launch_pdl(kern, grid, dim3(Cfg::THREADS), Cfg::SMEM, st, gg);
+  launch_pdl(kern, grid, dim3(Cfg::THREADS), Cfg::SMEM, st, gt);
   return cudaGetLastError();
 }
 

@@ -73,9 +73,10 @@ struct GemmArgs {
   Operand E;  // EPI == 2: right factor of the epilogue product
   KrrEpi ke;  // EPI == 3
   CoupEpi ce;  // EPI == 4
-  // TMA operand tiles (set by the host launcher for op(A) = A, op(B) = B^T with
-  // strided, 16-byte aligned batches): 3-D tensor maps (K, rows, batch), boxes
-  // of 16 x rows, 128-byte swizzle
+  // TMA operand tiles (set by the host launcher for op(A) = A with strided,
+  // 16-byte aligned batches): 3-D tensor maps; A and B^T as (K, rows, batch)
+  // with boxes of 16 x rows and the 128-byte swizzle, B (K x N) as (N, K,
+  // batch) with unswizzled boxes of 8 x 16
   int use_tma;
   CUtensorMap tma_a, tma_b;
 };
@@ -166,7 +167,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
 
   const int KT = (g.K + BK - 1) / BK;
   bool tma_done = false;
-  if constexpr (!TA && TB) {
+  if constexpr (!TA) {
     if (g.use_tma) {
       // TMA ring: thread 0 arms a stage's mbarrier with its byte count and issues
       // the A and B boxes; every warp waits on the barrier's phase, computes, and
@@ -185,7 +186,14 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
         const uint32_t bar = bar0 + 8 * stage;
         mbar_expect_tx(bar, A_BYTES + B_BYTES);
         tma_load_3d(sbase + stage * (A_BYTES + B_BYTES), &g.tma_a, kt * BK, m0, b, bar);
-        tma_load_3d(sbase + stage * (A_BYTES + B_BYTES) + A_BYTES, &g.tma_b, kt * BK, n0, b, bar);
+        if constexpr (TB) {
+          tma_load_3d(sbase + stage * (A_BYTES + B_BYTES) + A_BYTES, &g.tma_b, kt * BK, n0, b, bar);
+        } else {  // B is K x N: BN / 8 boxes of 8 columns x 16 rows, unswizzled
+#pragma unroll
+          for (int q = 0; q < BN / 8; ++q)
+            tma_load_3d(sbase + stage * (A_BYTES + B_BYTES) + A_BYTES + q * 8 * BK * 8, &g.tma_b, n0 + q * 8, kt * BK, b,
+                        bar);
+        }
       };
       if (threadIdx.x == 0) {
 #pragma unroll
@@ -208,7 +216,12 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
 #pragma unroll
           for (int i = 0; i < Cfg::MT; ++i) af[i] = as[swz128(wm0 + i * 8 + gq, kk + tq)];
 #pragma unroll
-          for (int j = 0; j < Cfg::NT; ++j) bf[j] = bs[swz128(wn0 + j * 8 + gq, kk + tq)];
+          for (int j = 0; j < Cfg::NT; ++j) {
+            const int c = wn0 + j * 8 + gq, k = kk + tq;
+            // TB: N x 16 rows, 128-byte swizzle; else 8-column boxes [c / 8][k][c % 8]
+            // (64-byte rows: the warp's four k rows fill two distinct bank halves twice)
+            bf[j] = TB ? bs[swz128(c, k)] : bs[(c >> 3) * (8 * BK) + k * 8 + (c & 7)];
+          }
 #pragma unroll
           for (int i = 0; i < Cfg::MT; ++i)
 #pragma unroll
