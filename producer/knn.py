@@ -45,11 +45,13 @@ def knn(X: torch.Tensor, k: int, chunk: int = 1024, extra: int = 8):
 
 
 def sample_rows(pos: torch.Tensor, perm: torch.Tensor, begin: int, end: int, nbr: torch.Tensor,
-                dist: torch.Tensor, n_samples: int, gen: torch.Generator) -> torch.Tensor:
+                dist: torch.Tensor, n_samples: int, seed: int, node_id: int) -> torch.Tensor:
     """compress.py:145-193 for one node: exterior neighbors of the node's points,
     ordered by distance (ties to the smaller id), deduplicated keeping the first
-    occurrence, cut at min(n_samples, n - size); a seeded uniform exterior draw
-    fills up the rest."""
+    occurrence, cut at min(n_samples, n - size); the fill-up is the reference's
+    own draw, generator(seed, 0x726F77, node_id).choice(pool, need, replace=False)
+    over the ascending exterior pool (compress.py:185-191), on the host."""
+    from paper_1602_01376_b200.rng import generator
     n = perm.numel()
     size = end - begin
     budget = min(n_samples, n - size)
@@ -77,7 +79,7 @@ def sample_rows(pos: torch.Tensor, perm: torch.Tensor, begin: int, end: int, nbr
         pool_mask = torch.ones(n, dtype=torch.bool, device=perm.device)
         pool_mask[owned] = False
         pool_mask[chosen] = False
-        pool = torch.nonzero(pool_mask).flatten()
-        pick = torch.randperm(pool.numel(), generator=gen, device=perm.device)[:need]
-        chosen = torch.cat([chosen, pool[pick]])
+        pool = torch.nonzero(pool_mask).flatten().cpu().numpy()
+        extra = generator(seed, 0x726F77, node_id).choice(pool, size=need, replace=False)
+        chosen = torch.cat([chosen, torch.from_numpy(extra.astype(np.int64)).to(perm.device)])
     return chosen

@@ -118,8 +118,7 @@ def skeletonize(coords: np.ndarray, tree: dict, h: float, max_rank: int, tol: fl
             if sampling == "knn":
                 rl = []
                 for v in vs:
-                    gen.manual_seed(seed * 1_000_003 + v)
-                    rl.append(sample_rows(pos_t, perm_t, int(begin[v]), int(end[v]), nbr, dist, budget, gen))
+                    rl.append(sample_rows(pos_t, perm_t, int(begin[v]), int(end[v]), nbr, dist, budget, seed, v))
                 rows = torch.stack(rl)
             else:
                 gen.manual_seed(seed * 1_000_003 + lev * 7919 + nc)
