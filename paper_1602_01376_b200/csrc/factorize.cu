@@ -19,7 +19,9 @@ namespace {
 // the trapezoid [[A], [P]].
 // wait_p: on the first factorization, the upload milestone of these leaves' P
 // blocks (the Gaussian blocks need only the points, so they start before it)
-static int enqueue_leaf_assemble(ks_factor* f, Launcher& L, int l0, int l1, cudaEvent_t wait_p = nullptr) {
+// defer_p: the P rows are copied later (enqueue_leaf_chol's split form)
+static int enqueue_leaf_assemble(ks_factor* f, Launcher& L, int l0, int l1, cudaEvent_t wait_p = nullptr,
+                                 bool defer_p = false) {
   if (l1 <= l0) return KS_OK;
   const ks::DevTree dt = f->devtree();
   const ks::LeafBatch all = f->leafbatch();
@@ -38,8 +40,10 @@ static int enqueue_leaf_assemble(ks_factor* f, Launcher& L, int l0, int l1, cuda
     ++L.count[0];
     cudaError_t e = ks::gemm_gauss(g, L.st);
     if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf gauss gemm: %s", cudaGetErrorString(e));
-    if (wait_p) KS_CUDA(cudaStreamWaitEvent(L.st, wait_p, 0));
-    ks::launch_leaf_copy_p(dt, lb, L.st);
+    if (!defer_p) {
+      if (wait_p) KS_CUDA(cudaStreamWaitEvent(L.st, wait_p, 0));
+      ks::launch_leaf_copy_p(dt, lb, L.st);
+    }
   } else {
     if (wait_p) KS_CUDA(cudaStreamWaitEvent(L.st, wait_p, 0));
     ks::launch_leaf_assemble(dt, lb, f->lam_dev.p, L.st);
@@ -50,7 +54,14 @@ static int enqueue_leaf_assemble(ks_factor* f, Launcher& L, int l0, int l1, cuda
 
 // KS_UNFUSED_LEAF_TRSM=1: separate update and TRSM GEMMs per leaf panel (A/B check)
 
-static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
+// split (the first factorization, while the leaves' P is still on its way):
+// the panels factor the m x m block A alone (rows [0, m)), the P rows are
+// copied in once their upload milestone wait_p has passed, and then L21 =
+// P L^-T is formed panel by panel from the stored diagonal inverses (the same
+// left-looking update + TRSM epilogue, on the P rows only). The Cholesky of
+// every leaf then needs only the points and overlaps the upload of P.
+static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1, bool split = false,
+                             cudaEvent_t wait_p = nullptr) {
   const ks::LeafBatch all = f->leafbatch();
   ks::LeafBatch lb = all;
   lb.count = l1 - l0;
@@ -66,6 +77,7 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
   int* info = f->leaf_info.p + l0;
   cudaStream_t st = L.st;
   const bool fused = !f->knobs.unfused_leaf_trsm;
+  const int R_eff = split ? M : R;  // rows the panels carry
   for (int j0 = 0; j0 < M; j0 += 64) {
     const Operand Einv{inv + (int64_t)(j0 / 64) * 64 * 64, 64, (int64_t)M * 64, nullptr};
     if (j0 > 0) {  // left-looking update of the panel (all rows, or just its diagonal block)
@@ -78,20 +90,20 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
         if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf diagonal update: %s", cudaGetErrorString(e));
         if (int rc = L.check("leaf_update_diag")) return rc;
       } else {
-        int rc = L.gemm(mk(R - j0, 64, j0, nl, A, B, C, -1.0, 1.0), false, true, "leaf_update");
+        int rc = L.gemm(mk(R_eff - j0, 64, j0, nl, A, B, C, -1.0, 1.0), false, true, "leaf_update");
         if (rc) return rc;
       }
     }
     ks::launch_potrf64(lb, j0, inv, info, st);
     ++L.count[0];
     if (int rc = L.check("potrf64")) return rc;
-    if (R - j0 - 64 > 0) {
+    if (R_eff - j0 - 64 > 0) {
       OperandW C{leafA + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
       if (fused && j0 > 0) {
         // rows below the diagonal block: update and TRSM (x L_jj^-T) in one GEMM
         Operand A{leafA + (int64_t)(j0 + 64) * M, M, AS, nullptr};
         Operand B{leafA + (int64_t)j0 * M, M, AS, nullptr};
-        GemmArgs g = mk(R - j0 - 64, 64, j0, nl, A, B, C, -1.0, 1.0);
+        GemmArgs g = mk(R_eff - j0 - 64, 64, j0, nl, A, B, C, -1.0, 1.0);
         g.E = Einv;
         ++L.count[0];
         cudaError_t e = ks::gemm_update_trsm(g, st);
@@ -99,8 +111,32 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1) {
         if (int rc = L.check("leaf_update_trsm")) return rc;
       } else {
         Operand A{leafA + (int64_t)(j0 + 64) * M + j0, M, AS, nullptr};
-        int rc = L.gemm(mk(R - j0 - 64, 64, 64, nl, A, Einv, C, 1.0, 0.0), false, true, "leaf_trsm");
+        int rc = L.gemm(mk(R_eff - j0 - 64, 64, 64, nl, A, Einv, C, 1.0, 0.0), false, true, "leaf_trsm");
         if (rc) return rc;
+      }
+    }
+  }
+  if (split && R > M) {
+    // the P rows: copy them in (after their upload), then L21 = P L^-T
+    if (wait_p) KS_CUDA(cudaStreamWaitEvent(st, wait_p, 0));
+    ks::launch_leaf_copy_p(f->devtree(), lb, st);
+    ++L.count[0];
+    const int S_rows = R - M;
+    for (int j0 = 0; j0 < M; j0 += 64) {
+      const Operand Einv{inv + (int64_t)(j0 / 64) * 64 * 64, 64, (int64_t)M * 64, nullptr};
+      OperandW C{leafA + (int64_t)M * M + j0, M, AS, nullptr};
+      if (j0 == 0) {
+        Operand A{leafA + (int64_t)M * M, M, AS, nullptr};
+        if (int rc = L.gemm(mk(S_rows, 64, 64, nl, A, Einv, C, 1.0, 0.0), false, true, "leaf_p_trsm")) return rc;
+      } else {
+        Operand A{leafA + (int64_t)M * M, M, AS, nullptr};
+        Operand B{leafA + (int64_t)j0 * M, M, AS, nullptr};
+        GemmArgs g = mk(S_rows, 64, j0, nl, A, B, C, -1.0, 1.0);
+        g.E = Einv;
+        ++L.count[0];
+        cudaError_t e = ks::gemm_update_trsm(g, st);
+        if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf P update+trsm gemm: %s", cudaGetErrorString(e));
+        if (int rc = L.check("leaf_p_update_trsm")) return rc;
       }
     }
   }
@@ -177,8 +213,10 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
         wait_p = f->ev_up_leaf[c];
       }
       Launcher Lg{f, gs, &f->launches[0]};
-      if (int rc = enqueue_leaf_assemble(f, Lg, l0, l1, wait_p)) return rc;
-      if (int rc = enqueue_leaf_chol(f, Lg, l0, l1)) return rc;
+      // while the uploads are in flight, factor A before P has arrived
+      const bool split = wait_p != nullptr && (f->d & 1) == 0 && f->n_int > 0 && f->knobs.split_leaf;
+      if (int rc = enqueue_leaf_assemble(f, Lg, l0, l1, wait_p, split)) return rc;
+      if (int rc = enqueue_leaf_chol(f, Lg, l0, l1, split, wait_p)) return rc;
       if (pipe) {  // this subtree's nodes of the deepest npipe levels, on the same stream
         if (f->upload_pending) KS_CUDA(cudaStreamWaitEvent(gs, f->ev_up_sub[g], 0));
         for (int lev = 0; lev < f->npipe; ++lev) {

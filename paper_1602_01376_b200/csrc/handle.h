@@ -56,6 +56,7 @@ struct Knobs {
   int panel_w = 0;             // KS_PANEL_W: 32 / 8 override the register-panel width
   bool fused_merge = false;    // KS_FUSED_MERGE=1: TRSM + update merge in one launch (slower)
   bool unfused_leaf_trsm = false;  // KS_UNFUSED_LEAF_TRSM=1: separate leaf update and TRSM GEMMs
+  bool split_leaf = true;      // KS_SPLIT_LEAF=0: the first factorization waits for the leaves' P up front
   int hager_ctas = 96;         // KS_HAGER_CTAS: CTAs of the deferred wide-level estimates
   int hager_flush = 0;         // KS_HAGER_FLUSH: start the deferred estimates at levels <= n nodes
   bool hager_split = true;     // KS_HAGER_SPLIT=0: narrow-level estimates queue with the wide ones

@@ -49,6 +49,7 @@ Knobs read_knobs() {
   k.panel_w = env_int("KS_PANEL_W", 0);
   k.fused_merge = env_flag("KS_FUSED_MERGE", false);
   k.unfused_leaf_trsm = env_flag("KS_UNFUSED_LEAF_TRSM", false);
+  k.split_leaf = env_flag("KS_SPLIT_LEAF", k.split_leaf);
   k.hager_ctas = std::max(1, env_int("KS_HAGER_CTAS", k.hager_ctas));
   k.hager_flush = env_int("KS_HAGER_FLUSH", k.hager_flush);
   k.hager_split = env_flag("KS_HAGER_SPLIT", k.hager_split);
