@@ -230,7 +230,7 @@ def solve_many(hf: GpuHierFactor, B):
     if B.shape[1] == 0:
         return np.empty_like(B)
     Bc = np.ascontiguousarray(B)
-    X = np.empty_like(Bc)
+    X = _host_result(Bc.shape)
     rc = _lib.load().ks_solve(hf.handle, Bc.ctypes.data_as(C.c_void_p), X.ctypes.data_as(C.c_void_p),
                               Bc.shape[1], None)
     if rc:
@@ -259,7 +259,7 @@ def hss_matvec(hf: GpuHierFactor, w):
     if w.shape[0] != hf.n:
         raise InvalidArgumentError(f"vector length {w.shape[0]} != n = {hf.n}")
     W = np.ascontiguousarray(w[:, None] if w.ndim == 1 else w)
-    Y = np.empty_like(W)
+    Y = _host_result(W.shape)
     rc = _lib.load().ks_matvec(hf.handle, W.ctypes.data_as(C.c_void_p), Y.ctypes.data_as(C.c_void_p), W.shape[1], None)
     if rc:
         _raise(rc)
@@ -274,6 +274,26 @@ def release_cached_memory(device: int | None = None) -> None:
     rc = _lib.load().ks_trim_pool(dev)
     if rc:
         _raise(rc)
+
+
+_PINNED_RESULT_MAX = 1 << 28  # results up to 256 MB come back in page-locked memory
+
+
+def _host_result(shape) -> np.ndarray:
+    """A fresh float64 host array for a result the library copies out of the
+    device. Page-locked (torch's caching pinned allocator, so repeated solves
+    reuse the blocks): the D2H copy is then one DMA into the caller's array
+    instead of a staged copy into fresh pageable pages (config 3, q = 1: 6.3 ->
+    5.2 ms per host solve). Larger results use ordinary memory."""
+    nbytes = 8 * int(np.prod(shape))
+    if 0 < nbytes <= _PINNED_RESULT_MAX:
+        try:
+            import torch
+
+            return torch.empty(tuple(int(x) for x in shape), dtype=torch.float64, pin_memory=True).numpy()
+        except Exception:  # no torch / no pinned memory left: pageable is still correct
+            pass
+    return np.empty(shape, dtype=np.float64)
 
 
 def _is_torch_cuda(x) -> bool:

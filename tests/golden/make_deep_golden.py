@@ -7,6 +7,7 @@ and solve_many (solver.py:200-237). Run in the build container (needs
     python tests/golden/make_deep_golden.py cfg2_full   # config 2 at its BASELINE size, N = 65536
     python tests/golden/make_deep_golden.py cfg3_128k   # config 3's recipe and shape, N = 131072
     python tests/golden/make_deep_golden.py cfg4_64k    # config 4's recipe and shape, N = 65536, q = 16
+    python tests/golden/make_deep_golden.py cfg5_32k    # config 5's recipe and shape (d = 784, m = 2048, s = 512), N = 32768
 
 A fixture (tests/golden/<case>.npz) keeps what the GPU test needs and nothing
 the recipe can regenerate: the integer side of the operator (tree permutation
@@ -43,6 +44,7 @@ DEEP = {
     "cfg2_full": (_cfg("cfg2", name="cfg2_full"), 1),
     "cfg3_128k": (_cfg("cfg3", name="cfg3_128k", n=131072), 2),
     "cfg4_64k": (_cfg("cfg4", name="cfg4_64k", n=65536), 16),
+    "cfg5_32k": (_cfg("cfg5", name="cfg5_32k", n=32768), 1),
 }
 
 
@@ -81,6 +83,8 @@ def make(case: str) -> None:
     out["n_warnings"] = np.int64(len(dg["warnings"]))
     hs, h_off, h_nodes = [], [0], []
     for v in range(1, 7):  # levels 1 and 2: the reduced matrices everything below feeds
+        if v not in hf.node_factors:
+            continue
         H = hf.node_factors[v].H
         h_nodes.append(v)
         hs.append(H.ravel())

@@ -29,7 +29,7 @@ def _sha(a, dt):
     return hashlib.sha256(np.ascontiguousarray(a, dtype=dt).tobytes()).hexdigest()
 
 
-@pytest.mark.parametrize("case", ["cfg2_full", "cfg4_64k", "cfg3_128k"])
+@pytest.mark.parametrize("case", ["cfg2_full", "cfg4_64k", "cfg3_128k", "cfg5_32k"])
 def test_deep_tree_matches_reference(case):
     import json
 
