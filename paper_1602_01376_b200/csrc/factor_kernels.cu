@@ -123,19 +123,18 @@ void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, const double* l
 // blocked by 16 columns so the critical path is ~20 barriers instead of one
 // per column:
 //   for each 16-column block kb: warp 0 factors the 16x16 diagonal block in
-//   registers (shuffles, _cholesky's column order within the block,
-//   linalg.py:185-196) and inverts it; all threads then form the block's rows
-//   below (L21 = A21 L11^-T) and update the trailing lower triangle;
-//   finally the off-diagonal blocks of X = L^-1 by block rows.
+//   registers (lane i owns row i; per column one broadcast of the pivot, a
+//   reciprocal square root and one shuffle per remaining column: _cholesky's
+//   column order within the block, linalg.py:185-196, with l_jj = p * rsqrt(p))
+//   and inverts it with the stored reciprocals; all threads then form the
+//   block's rows below (L21 = A21 L11^-T) and update the trailing lower
+//   triangle; finally the off-diagonal blocks of X = L^-1 by block rows.
 // Failure (pivot <= 0 or non-finite) records the first bad column + 1, as
 // _cholesky raises NotSPDError at linalg.py:190-192 (the block stays finite).
 // X lives transposed in the strict upper triangle of the tile (x[i][j] at
-// a[j][i], i > j) with its diagonal in xd.
+// a[j][i], i > j) with its diagonal in xd; the current block's inverse also
+// densely in xi (zeros above its diagonal).
 // --------------------------------------------------------------------------
-__device__ __forceinline__ double potrf_x(const double (*a)[65], const double* xd, int r, int c) {
-  return r == c ? xd[r] : (r > c ? a[c][r] : 0.0);
-}
-
 __global__ void __launch_bounds__(256, 4) k_potrf64(LeafBatch lb, int j0, double* inv, int* info) {
   pdl_wait();
   const int leaf = blockIdx.x;
@@ -145,6 +144,7 @@ __global__ void __launch_bounds__(256, 4) k_potrf64(LeafBatch lb, int j0, double
   double(*a)[65] = reinterpret_cast<double(*)[65]>(potrf_sm);
   double* xd = potrf_sm + 64 * 65;
   double(*t)[17] = reinterpret_cast<double(*)[17]>(xd + 64);  // 48 x 17 scratch
+  double(*xi)[17] = reinterpret_cast<double(*)[17]>(xd + 64 + 48 * 17);  // 16 x 17: the block's inverse
   __shared__ int bad;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   {  // all 16 loads per thread in flight
@@ -165,30 +165,33 @@ __global__ void __launch_bounds__(256, 4) k_potrf64(LeafBatch lb, int j0, double
 #pragma unroll 1
   for (int kb = 0; kb < 64; kb += 16) {
     if (warp == 0) {
-      // (1) the 16 x 16 diagonal block: lane i < 16 owns row kb + i
+      // (1) the 16 x 16 diagonal block: lane i < 16 owns row kb + i (the upper
+      // part of r and lanes >= 16 carry unused values: no predication)
+      const int row = kb + (lane & 15);
       double r[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) r[k] = (lane < 16 && k <= lane) ? a[kb + lane][kb + k] : 0.0;
+      for (int k = 0; k < 16; ++k) r[k] = a[row][kb + k];
+      double rinv = 0.0;  // lane j: 1 / l_jj
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         double p = __shfl_sync(0xffffffffu, r[j], j);
-        if (!(p > 0.0) || !isfinite(p)) {
+        if (!(p > 0.0) || !isfinite(p)) {  // warp-uniform
           if (lane == 0) atomicMin(&bad, kb + j);
           p = 1.0;
+          if (lane == j) r[j] = 1.0;
         }
-        const double lj = sqrt(p), rl = 1.0 / lj;
-        if (lane == j) r[j] = lj;
-        else if (lane > j) r[j] *= rl;
+        const double rl = rsqrt(p);
+        const double cj = r[j] * rl;  // lane j: l_jj = p / sqrt(p); lanes > j: column j of L
+        r[j] = cj;
+        if (lane == j) rinv = rl;
 #pragma unroll
-        for (int k = j + 1; k < 16; ++k) {
-          const double lkj = __shfl_sync(0xffffffffu, r[j], k);
-          if (lane >= k && lane < 16) r[k] = fma(-r[j], lkj, r[k]);
-        }
+        for (int k = j + 1; k < 16; ++k) r[k] = fma(-cj, __shfl_sync(0xffffffffu, cj, k), r[k]);
       }
       if (lane < 16) {
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          if (k <= lane) a[kb + lane][kb + k] = r[k];
+          if (k <= lane) a[row][kb + k] = r[k];
+        t[0][lane] = rinv;  // scratch row 0: the reciprocal diagonal
       }
       __syncwarp();
       // inverse of the diagonal block: lane c < 16 solves column c of L11 x = e_c
@@ -199,12 +202,12 @@ __global__ void __launch_bounds__(256, 4) k_potrf64(LeafBatch lb, int j0, double
         for (int rr = 0; rr < 16; ++rr) {
           double s = (rr == c) ? 1.0 : 0.0;
 #pragma unroll
-          for (int k = 0; k < rr; ++k)
-            if (k >= c) s = fma(-a[kb + rr][kb + k], x[k], s);
-          x[rr] = (rr >= c) ? s / a[kb + rr][kb + rr] : 0.0;
+          for (int k = 0; k < rr; ++k) s = fma(-a[kb + rr][kb + k], x[k], s);  // x[k] = 0 for k < c
+          x[rr] = s * t[0][rr];
         }
 #pragma unroll
         for (int rr = 0; rr < 16; ++rr) {
+          xi[rr][c] = x[rr];
           if (rr == c) xd[kb + c] = x[rr];
           else if (rr > c) a[kb + c][kb + rr] = x[rr];
         }
@@ -217,8 +220,10 @@ __global__ void __launch_bounds__(256, 4) k_potrf64(LeafBatch lb, int j0, double
       for (int e = threadIdx.x; e < nr * 16; e += 256) {
         const int rr = e >> 4, j = e & 15;
         const double* ar = a[kb + 16 + rr] + kb;
+        const double* xj = xi[j];
         double s = 0.0;
-        for (int k = 0; k <= j; ++k) s = fma(ar[k], potrf_x(a, xd, kb + j, kb + k), s);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) s = fma(ar[k], xj[k], s);  // xj[k] = 0 for k > j
         t[rr][j] = s;
       }
       __syncthreads();
@@ -237,14 +242,17 @@ __global__ void __launch_bounds__(256, 4) k_potrf64(LeafBatch lb, int j0, double
   }
   // (4) off-diagonal blocks of X = L^-1 by block rows:
   //     X[bi][bj] = -X[bi][bi] sum_{k = bj..bi-1} L[bi][k] X[k][bj]
+  //     (X[k][c] for k > c is a[c][k], X[c][c] is xd[c])
 #pragma unroll 1
   for (int bi = 1; bi < 4; ++bi) {
     double(*tt)[16] = reinterpret_cast<double(*)[16]>(&t[0][0]);  // bi x 16 x 16 (<= 768 doubles)
     for (int e = threadIdx.x; e < bi * 256; e += 256) {
       const int bj = e >> 8, rl = (e >> 4) & 15, cl = e & 15;
       const int r = bi * 16 + rl, c = bj * 16 + cl;
-      double s = 0.0;
-      for (int k = c; k < bi * 16; ++k) s = fma(a[r][k], potrf_x(a, xd, k, c), s);
+      const double* lr = a[r];
+      const double* xc = a[c];
+      double s = lr[c] * xd[c];
+      for (int k = c + 1; k < bi * 16; ++k) s = fma(lr[k], xc[k], s);
       tt[bj * 16 + rl][cl] = s;
     }
     __syncthreads();
@@ -255,8 +263,9 @@ __global__ void __launch_bounds__(256, 4) k_potrf64(LeafBatch lb, int j0, double
       xo[u] = 0.0;
       if (e < bi * 256) {
         const int bj = e >> 8, rl = (e >> 4) & 15, cl = e & 15;
-        double s = 0.0;
-        for (int m = 0; m <= rl; ++m) s = fma(potrf_x(a, xd, bi * 16 + rl, bi * 16 + m), tt[bj * 16 + m][cl], s);
+        const int r = bi * 16 + rl;
+        double s = xd[r] * tt[bj * 16 + rl][cl];
+        for (int m = 0; m < rl; ++m) s = fma(a[bi * 16 + m][r], tt[bj * 16 + m][cl], s);
         xo[u] = -s;
       }
     }
@@ -282,7 +291,7 @@ __global__ void __launch_bounds__(256, 4) k_potrf64(LeafBatch lb, int j0, double
 }
 
 void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStream_t st) {
-  constexpr size_t smem = (64 * 65 + 64 + 48 * 17) * sizeof(double);
+  constexpr size_t smem = (64 * 65 + 64 + 48 * 17 + 16 * 17) * sizeof(double);
   ensure_smem(k_potrf64, smem);
   launch_pdl(k_potrf64, dim3(lb.count), dim3(256), smem, st, lb, j0, inv, info);
 }

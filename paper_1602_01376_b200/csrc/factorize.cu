@@ -38,7 +38,7 @@ static int enqueue_leaf_assemble(ks_factor* f, Launcher& L, int l0, int l1, cuda
                     Operand{f->coords.p, f->d, f->d, lb.begin}, OperandW{lb.A, M, lb.a_stride, nullptr}, 1.0, 0.0);
     g.ge = ks::GaussEpi{f->xx.p, lb.begin, lb.size, f->lam_dev.p, f->h};
     ++L.count[0];
-    cudaError_t e = ks::gemm_gauss(g, L.st);
+    cudaError_t e = (f->knobs.ablate & 8) ? cudaSuccess : ks::gemm_gauss(g, L.st);
     if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf gauss gemm: %s", cudaGetErrorString(e));
     if (!defer_p) {
       if (wait_p) KS_CUDA(cudaStreamWaitEvent(L.st, wait_p, 0));
@@ -86,7 +86,7 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1, bool spl
       OperandW C{leafA + (int64_t)j0 * M + j0, M, AS, nullptr};
       if (fused) {
         ++L.count[0];
-        cudaError_t e = ks::gemm_small_tile(mk(64, 64, j0, nl, A, B, C, -1.0, 1.0), st);
+        cudaError_t e = (f->knobs.ablate & 2) ? cudaSuccess : ks::gemm_small_tile(mk(64, 64, j0, nl, A, B, C, -1.0, 1.0), st);
         if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf diagonal update: %s", cudaGetErrorString(e));
         if (int rc = L.check("leaf_update_diag")) return rc;
       } else {
@@ -94,7 +94,7 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1, bool spl
         if (rc) return rc;
       }
     }
-    ks::launch_potrf64(lb, j0, inv, info, st);
+    if (!(f->knobs.ablate & 1)) ks::launch_potrf64(lb, j0, inv, info, st);
     ++L.count[0];
     if (int rc = L.check("potrf64")) return rc;
     if (R_eff - j0 - 64 > 0) {
@@ -106,7 +106,7 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1, bool spl
         GemmArgs g = mk(R_eff - j0 - 64, 64, j0, nl, A, B, C, -1.0, 1.0);
         g.E = Einv;
         ++L.count[0];
-        cudaError_t e = ks::gemm_update_trsm(g, st);
+        cudaError_t e = (f->knobs.ablate & 4) ? cudaSuccess : ks::gemm_update_trsm(g, st);
         if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf update+trsm gemm: %s", cudaGetErrorString(e));
         if (int rc = L.check("leaf_update_trsm")) return rc;
       } else {
@@ -140,7 +140,7 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1, bool spl
       }
     }
   }
-  if (S > 0 && f->n_int > 0) {
+  if (S > 0 && f->n_int > 0 && !(f->knobs.ablate & 16)) {
     Operand A{leafA + (int64_t)M * M, M, AS, nullptr};
     OperandW C{f->hbuf.p, S, (int64_t)S * S, lb.node};
     // SYRK: lower-triangular tiles only, then mirrored (H exactly symmetric, so
@@ -278,10 +278,15 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
   const int64_t TT = (int64_t)T * T, SS = (int64_t)S * S, XS = 2 * SS, PS = (int64_t)S * ZT;
   const int cnt = nb.count;
   cudaStream_t st = L.st;
-  ks::launch_coupling(dt, nb, st);
-  ks::launch_aug2_init(dt, nb, st);  // S = I, E = P_r^T, the padded P copy
-  L.count[0] += 3;
-  int rc = L.check("coupling/aug2_init");
+  const int abl = f->knobs.ablate;
+  if (abl & 1024) return KS_OK;
+  if (!(abl & 32)) ks::launch_coupling(dt, nb, st);
+  ++L.count[0];
+  if (f->need_p_layout) {  // the padded P and P^T copies: once per handle
+    ks::launch_p_layout(dt, nb, st);
+    L.count[0] += 2;
+  }
+  int rc = L.check("coupling/p_layout");
   if (rc) return rc;
   double* Xb = nb.XY;
   double* Yb = nb.XY + SS;
@@ -292,8 +297,9 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
   // stage 1 (independent products, one launch; H is exactly symmetric, so it
   // is read row-major as the right factor):
   //   X = B H_r,  Y = B^T H_l,  P_l H_l,  F = -P_r H_r
-  // stage 2 (one launch):
-  //   S -= Y X,  E -= Y P_l^T,  F += (P_l H_l) X,  C = (P_l H_l) P_l^T
+  // stage 2 (one launch; S and E are written out of place, nothing of Aug is
+  // initialized beforehand):
+  //   S = I - Y X,  E = P_r^T - Y P_l^T,  F += (P_l H_l) X,  C = (P_l H_l) P_l^T
   {
     ks::GemmGroup g1{};
     g1.count = 4;
@@ -306,26 +312,31 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
     g1.p[3] = mk(S, S, S, cnt, Operand{nb.Pn + S, ZT, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
                  OperandW{Fb, T, TT, nullptr}, -1.0, 0.0);
     ++L.count[0];
-    if (cudaError_t e = ks::gemm_group(g1, st)) return fail(KS_ERR_CUDA, "assembly stage 1: %s", cudaGetErrorString(e));
+    if (abl & 64) {
+    } else if (cudaError_t e = ks::gemm_group(g1, st)) return fail(KS_ERR_CUDA, "assembly stage 1: %s", cudaGetErrorString(e));
     if ((rc = L.check("assembly1"))) return rc;
     const int64_t PTS = (int64_t)ZT * S;
     ks::GemmGroup g2{};
     g2.count = 4;
     g2.p[0] = mk(S, S, S, cnt, Operand{Yb, S, XS, nullptr}, Operand{Xb, S, XS, nullptr}, OperandW{Sb, T, TT, nullptr},
-                 -1.0, 1.0);
+                 -1.0, 0.0);
+    g2.p[0].addI = 1;
     g2.p[1] = mk(S, S, S, cnt, Operand{Yb, S, XS, nullptr}, Operand{nb.PT, S, PTS, nullptr},
                  OperandW{Eb, T, TT, nullptr}, -1.0, 1.0);
+    g2.p[1].Cin = Operand{nb.PT + SS, S, PTS, nullptr};  // P_r^T
     g2.p[2] = mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{Xb, S, XS, nullptr},
                  OperandW{Fb, T, TT, nullptr}, 1.0, 1.0);
     g2.p[3] = mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{nb.PT, S, PTS, nullptr},
                  OperandW{Cb, T, TT, nullptr}, 1.0, 0.0);
     ++L.count[0];
-    if (cudaError_t e = ks::gemm_group(g2, st)) return fail(KS_ERR_CUDA, "assembly stage 2: %s", cudaGetErrorString(e));
+    if (abl & 64) {
+    } else if (cudaError_t e = ks::gemm_group(g2, st)) return fail(KS_ERR_CUDA, "assembly stage 2: %s", cudaGetErrorString(e));
     if ((rc = L.check("assembly2"))) return rc;
   }
   ks::launch_znorm1(nb, st);  // ||Z||_1 for the condition estimate (linalg.py:176)
   ++L.count[0];
   if ((rc = L.check("znorm1"))) return rc;
+  if (abl & 128) return KS_OK;
   if (use_slab(f, nb)) {
     // narrow level: the whole LU, U12, Schur block and H in one cooperative launch
     // (its own ||.||_1 of the slabs goes to a scratch word: Z's norm is znorm1's)
@@ -590,6 +601,7 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
   KS_CUDA(cudaMemcpyAsync(f->lam_dev.p, &f->lam, sizeof(double), cudaMemcpyHostToDevice, st));
   // CUDA graph of the ~1000-launch sequence: from the second factorization on
   // (KS_GRAPH=1, default), always (2) or never (0); tracing runs eagerly.
+  f->need_p_layout = !f->p_layout_local;
   const int gm = (trace_on() || debug_sync() || f->profiling) ? 0 : f->knobs.graph;
   const bool use_graph = gm == 2 || (gm == 1 && f->n_factorizations > 0);
   if (use_graph && f->upload_pending) {  // a graph does not capture waits on the upload stream
@@ -621,6 +633,11 @@ int ks_factorize(ks_factor* f, double lam, void* stream) {
     }
   }
   ++f->n_factorizations;
+  f->p_layout_local = true;
+  if (f->knobs.ablate) {  // timing experiment: nothing below is meaningful
+    KS_CUDA(cudaStreamSynchronize(st));
+    return KS_OK;
+  }
   // leaf Cholesky failures (NotSPD) -> LU fallback for those leaves (solver.py:125-131)
   f->leaf_info_h.assign(nl, 0);
   KS_CUDA(cudaMemcpyAsync(f->leaf_info_h.data(), f->leaf_info.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, st));
@@ -711,7 +728,9 @@ int ks_factorize_top(ks_factor* f, void* stream) {
   KS_CUDA(cudaSetDevice(f->device));
   cudaStream_t st = (cudaStream_t)stream;
   Launcher L{f, st, &f->launches[0]};
+  f->need_p_layout = !f->p_layout_top;
   if (int rc = enqueue_levels(f, st, L, f->n_local_levels, (int)f->levels.size())) return rc;
+  f->p_layout_top = true;
   const int k0 = f->n_local_levels < (int)f->levels.size() ? f->level_first[f->n_local_levels] : f->n_int;
   if (f->n_int > k0) {
     KS_CUDA(cudaMemcpyAsync(f->int_info_h.data() + k0, f->int_info.p + k0, sizeof(int) * (f->n_int - k0),

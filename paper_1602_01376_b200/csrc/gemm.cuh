@@ -27,9 +27,10 @@ namespace ks {
 //      kernel exactly 1, solver.py:124), identity on padded rows/columns
 //      (r or c >= size[b]) and 0 above the diagonal.
 //   2  panel TRSM folded into a panel update (N == BN == 64):
-//      C = (alpha*AB + beta*C) * E^T, E[b] a 64 x 64 block (the inverse of the
-//      panel's diagonal Cholesky factor): the updated tile is staged in shared
-//      memory and multiplied on the tensor pipe before it is stored.
+//      C = (alpha*AB + beta*C) * E^T, E[b] a 64 x 64 LOWER TRIANGULAR block (the
+//      inverse of the panel's diagonal Cholesky factor): the updated tile is staged
+//      in shared memory and multiplied on the tensor pipe before it is stored
+//      (only the k <= c terms: E's zeros are skipped).
 struct GaussEpi {
   const double* xx;   // squared norms of the points, tree order
   const int* begin;   // per batch: first point of the leaf
@@ -69,6 +70,12 @@ struct GemmArgs {
   OperandW C;
   double alpha, beta;
   int tri;  // 1: skip CTA tiles strictly above the diagonal of C
+  // EPI == 0: the beta term reads Cin instead of C when Cin.ptr is set (an
+  // out-of-place C = alpha*AB + beta*Cin), and addI adds the identity
+  // (C = alpha*AB + beta*Cin + I): the node assembly forms S = I - Y X and
+  // E = P_r^T - Y P_l^T without initializing Aug first
+  Operand Cin;
+  int addI;
   GaussEpi ge;
   Operand E;  // EPI == 2: right factor of the epilogue product
   KrrEpi ke;  // EPI == 3
@@ -318,17 +325,23 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
       }
     }
     __syncthreads();
+    // E is lower triangular (E[c][k] = 0 for k > c): output columns
+    // [c0, c0 + 8) need only k < c0 + 8 (warp-uniform bounds; the skipped
+    // products are exact zeros)
 #pragma unroll
     for (int kk = 0; kk < BN; kk += 4) {
+      if (kk >= wn0 + Cfg::WTN) break;
       double af[Cfg::MT], bf[Cfg::NT];
 #pragma unroll
       for (int i = 0; i < Cfg::MT; ++i) af[i] = Ts[(wm0 + i * 8 + gq) * TL + kk + tq];
 #pragma unroll
       for (int j = 0; j < Cfg::NT; ++j) bf[j] = Es[(wn0 + j * 8 + gq) * TL + kk + tq];
 #pragma unroll
-      for (int i = 0; i < Cfg::MT; ++i)
+      for (int j = 0; j < Cfg::NT; ++j) {
+        if (kk >= wn0 + j * 8 + 8) continue;
 #pragma unroll
-        for (int j = 0; j < Cfg::NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int i = 0; i < Cfg::MT; ++i) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
     }
 #pragma unroll
     for (int i = 0; i < Cfg::MT; ++i) {
@@ -404,6 +417,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
   }
   double den = 0.0, lam = 0.0;
   int bsz = 0, bbeg = 0;
+  const double* Cin = (EPI == 0 && g.Cin.ptr) ? g.Cin.at(b) : nullptr;
   if (EPI == 1) {
     den = 1.0 / (-2.0 * g.ge.h * g.ge.h);  // multiply by the reciprocal: one rounding in the exponent
     lam = *g.ge.lam;
@@ -469,9 +483,13 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
         v.x = alpha * acc[i][j][0];
         v.y = alpha * acc[i][j][1];
         if (beta != 0.0) {
-          const double2 ov = *p;
+          const double2 ov = Cin ? *reinterpret_cast<const double2*>(Cin + (int64_t)r * g.Cin.ld + c) : *p;
           v.x = fma(beta, ov.x, v.x);
           v.y = fma(beta, ov.y, v.y);
+        }
+        if (g.addI) {
+          if (r == c) v.x += 1.0;
+          if (r == c + 1) v.y += 1.0;
         }
       }
       *p = v;

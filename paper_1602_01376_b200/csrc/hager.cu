@@ -14,6 +14,7 @@
 // next block's coefficients loaded one step ahead and the diagonal blocks
 // applied through their inverses (k_diag_inv); the X / Y products are
 // coalesced GEMVs (warp per row, or thread per column).
+#include <cstdlib>
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -435,6 +436,8 @@ int hager_launches(const NodeBatch& nb) { return (nb.t_pad <= 512 && nb.count < 
 // factors are still in L2 (narrow levels); for wide levels the extra HBM pass
 // costs more than it saves.
 void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, double* lut, int max_ctas, cudaStream_t st) {
+  static const int abl = std::getenv("KS_ABLATE") ? std::atoi(std::getenv("KS_ABLATE")) : 0;  // timing experiment
+  if (abl & 256) return;
   const int S = nb.t_pad;
   const bool cm = lut && nb.count < 64 && S <= 512;
   if (S <= 256) {

@@ -63,6 +63,7 @@ struct Knobs {
   bool hager_early = false;    // KS_HAGER_EARLY=1: a pipelined level's estimates right after each subtree's level
   bool force_leaf_lu = false;  // KS_FORCE_LEAF_LU=1: test hook, every leaf takes the LU path
   int graph = 1;               // KS_GRAPH: 1 graph replay from the 2nd factorization, 2 always, 0 never
+  int ablate = 0;              // KS_ABLATE: timing experiment, skip pieces of the schedule (results are garbage; tools/ablate.py)
 };
 Knobs read_knobs();
 // process-wide debugging switches
@@ -189,6 +190,9 @@ struct ks_factor {
   bool graph_profiling = false;
   int64_t graph_launches = 0;
   int64_t n_factorizations = 0;
+  // the padded P and P^T copies of the internal nodes (pn, pt) depend only on the
+  // operator: laid out by the first factorization of the local / top levels
+  bool p_layout_local = false, p_layout_top = false, need_p_layout = true;
   ksr::DBuf<double> lam_dev;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // narrow levels' condition estimates: their own stream, so they do not queue
@@ -343,6 +347,8 @@ inline GemmArgs mk(int M, int N, int K, int batch, Operand A, Operand B, Operand
   g.A = A; g.B = B; g.C = C;
   g.alpha = alpha; g.beta = beta; g.tri = 0;
   g.E = Operand{nullptr, 0, 0, nullptr};
+  g.Cin = Operand{nullptr, 0, 0, nullptr};
+  g.addI = 0;
   return g;
 }
 

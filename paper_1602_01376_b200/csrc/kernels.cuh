@@ -77,7 +77,7 @@ void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, i
 void launch_mirror_lower(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st);
 void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
 // block formulation (node_kernels.cu): S = I and E = P_r^T blocks of Aug, the padded P copy
-void launch_aug2_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
+void launch_p_layout(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
 // ||Z||_1 from X and Y (linalg.py:176): max column abs sum of [[I, X], [Y, I]]
 void launch_znorm1(const NodeBatch& nb, cudaStream_t st);
 // pend (may be null): {row0, col0, rows, cols} of a U12 block waiting in nb.scratch

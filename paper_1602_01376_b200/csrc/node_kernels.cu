@@ -114,19 +114,14 @@ __device__ __forceinline__ int cand_index(int i, int S, int sl, int sr) {
   return (i < S) ? (i < sl ? i : -1) : (i - S < sr ? sl + (i - S) : -1);
 }
 
-// one CTA per row: rows [0, S) the identity block S = I (columns [0, S) of
-// Aug; the GEMMs then subtract Y X), rows [S, 2S) the padded P copy (Pn,
-// row j: P[j][cand(i)] for the padded candidate index i)
-__global__ void __launch_bounds__(256) k_aug2_init(DevTree t, NodeBatch nb) {
+// The operator's P of every internal node in the two layouts the assembly
+// GEMMs and the solve read (they depend only on the operator, not on lambda:
+// written by the first factorization of a handle, kept afterwards):
+// Pn, one CTA per row j: P[j][cand(i)] for the padded candidate index i
+__global__ void __launch_bounds__(256) k_pn_layout(DevTree t, NodeBatch nb) {
   pdl_wait();
-  const int k = blockIdx.y, row = blockIdx.x;
-  const int S = nb.s_pad, T = nb.T, ZT = nb.zt;
-  if (row < S) {
-    double* out = nb.Aug + (int64_t)k * T * T + (int64_t)row * T;
-    for (int j = threadIdx.x; j < S; j += 256) out[j] = (row == j) ? 1.0 : 0.0;
-    return;
-  }
-  const int j = row - S;
+  const int k = blockIdx.y, j = blockIdx.x;
+  const int S = nb.s_pad, ZT = nb.zt;
   const int v = nb.node[k], sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]], sv = t.rank[v];
   const double* P = t.coeff + t.coeff_off[v] + (int64_t)j * (sl + sr);
   double* out = nb.Pn + (int64_t)k * S * ZT + (int64_t)j * ZT;
@@ -136,14 +131,13 @@ __global__ void __launch_bounds__(256) k_aug2_init(DevTree t, NodeBatch nb) {
   }
 }
 
-// P^T (zt x S: rows [0, S) P_l^T, rows [S, 2S) P_r^T) and E = P_r^T (S x S at
-// (0, S) of Aug; the GEMMs then subtract Y P_l^T) through 32 x 32 shared-memory
-// tiles: reads along P's rows, writes along P^T's and Aug's rows
-__global__ void __launch_bounds__(256) k_aug2_pt(DevTree t, NodeBatch nb) {
+// P^T (zt x S: rows [0, S) P_l^T, rows [S, 2S) P_r^T) through 32 x 32
+// shared-memory tiles: reads along P's rows, writes along P^T's
+__global__ void __launch_bounds__(256) k_pt_layout(DevTree t, NodeBatch nb) {
   pdl_wait();
   __shared__ double tile[32][33];
   const int k = blockIdx.z;
-  const int S = nb.s_pad, T = nb.T;
+  const int S = nb.s_pad;
   const int v = nb.node[k], sl = t.rank[nb.left[k]], sr = t.rank[nb.right[k]], sv = t.rank[v];
   const double* P = t.coeff + t.coeff_off[v];
   const int cand = sl + sr;
@@ -159,15 +153,11 @@ __global__ void __launch_bounds__(256) k_aug2_pt(DevTree t, NodeBatch nb) {
   __syncthreads();
   double* PT = nb.PT + (int64_t)k * nb.zt * S;
   for (int ii = ty; ii < 32; ii += 8) PT[(int64_t)(i0 + ii) * S + j0 + tx] = tile[tx][ii];
-  if (i0 >= S) {
-    double* A = nb.Aug + (int64_t)k * T * T;
-    for (int ii = ty; ii < 32; ii += 8) A[(int64_t)(i0 - S + ii) * T + S + j0 + tx] = tile[tx][ii];
-  }
 }
 
-void launch_aug2_init(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
-  launch_pdl(k_aug2_init, dim3(2 * nb.s_pad, nb.count), dim3(256), 0, st, t, nb);
-  launch_pdl(k_aug2_pt, dim3(nb.s_pad / 32, nb.zt / 32, nb.count), dim3(256), 0, st, t, nb);
+void launch_p_layout(const DevTree& t, const NodeBatch& nb, cudaStream_t st) {
+  launch_pdl(k_pn_layout, dim3(nb.s_pad, nb.count), dim3(256), 0, st, t, nb);
+  launch_pdl(k_pt_layout, dim3(nb.s_pad / 32, nb.zt / 32, nb.count), dim3(256), 0, st, t, nb);
 }
 
 // ||Z||_1 = max column abs sum of [[I, X], [Y, I]] (linalg.py:176): the columns

@@ -56,6 +56,7 @@ Knobs read_knobs() {
   k.hager_early = env_flag("KS_HAGER_EARLY", k.hager_early);
   k.force_leaf_lu = env_flag("KS_FORCE_LEAF_LU", false);
   k.graph = env_int("KS_GRAPH", k.graph);
+  k.ablate = env_int("KS_ABLATE", 0);
   return k;
 }
 
