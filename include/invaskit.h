@@ -158,6 +158,10 @@ int ks_set_profiling(ks_factor* f, int on);
 int ks_get_phase_ms(const ks_factor* f, double* ms, int cap);
 /* Per internal level (deepest first) main-stream time of the last factorization. */
 int ks_get_level_ms(const ks_factor* f, double* ms, int cap);
+/* Levels the schedule runs per subtree on the subtree's own stream (subtree
+ * pipelining): out2[0] in a replayed factorization, out2[1] in the last first
+ * factorization that ran behind its uploads (0 if it did not pipeline). */
+int ks_pipelined_levels(const ks_factor* f, int* out2);
 /* With KS_TRACE=1 in the environment: per-kernel device time table of the last
  * factorization (events after every launch on the launching stream). */
 int ks_trace_report(const ks_factor* f, char* buf, int64_t len);

@@ -82,6 +82,7 @@ SIGNATURES = {
     "ks_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "ks_get_phase_ms": (C.c_int, [C.c_void_p, _f64p, C.c_int]),
     "ks_get_level_ms": (C.c_int, [C.c_void_p, _f64p, C.c_int]),
+    "ks_pipelined_levels": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
     "ks_trace_report": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
     "ks_last_launches": (C.c_int64, [C.c_void_p, C.c_int]),
     "ks_debug_copy": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, _f64p, C.c_int64]),

@@ -125,7 +125,7 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     for (int lev = 0; lev < f->n_local_levels && nlv % G == 0; ++lev) {
       const auto& lv = f->levels[lev];
       const int c = (int)lv.size();
-      if (c % G || c / G < f->knobs.pipe_min) break;
+      if (c % G || c / G < 1) break;
       bool ok = true;
       for (int i = 0; i < c; ++i) {
         const int g = i / (c / G), v = lv[i];
@@ -133,8 +133,12 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
       }
       if (!ok) break;
       for (int i = 0; i < c; ++i) grp[lv[i]] = i / (c / G);
-      f->npipe = lev + 1;
+      if (f->npipe == lev && c / G >= f->knobs.pipe_min) f->npipe = lev + 1;
+      // the first factorization (uploads in flight) pipelines every
+      // subtree-local level: the subtrees finish staggered behind their uploads
+      f->npipe_first = lev + 1;
     }
+    if (f->npipe == 0 || !f->knobs.pipe_first) f->npipe_first = f->npipe;
   }
   f->m_pad = (int)roundup(m_max, 64);
   f->s_pad = (int)roundup(s_max, 64);
@@ -287,6 +291,8 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_up_all, cudaEventDisableTiming));
     for (auto& e : f->ev_up_leaf) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : f->ev_up_sub) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    f->ev_up_sublev.resize((size_t)ks_factor::kLeafChunks * f->npipe_first);
+    for (auto& e : f->ev_up_sublev) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     f->ev_up_level.resize(f->levels.size());
     for (auto& e : f->ev_up_level) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     cudaStream_t u = f->upl;
@@ -355,11 +361,13 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     }
     for (int c = 0; c < ks_factor::kLeafChunks; ++c) {
       // with subtree pipelining: this subtree's nodes of the pipelined levels
-      for (int lev = 0; lev < f->npipe; ++lev) {
+      for (int lev = 0; lev < f->npipe_first; ++lev) {
         const auto& lv = f->levels[lev];
         const size_t c0 = lv.size() * c / ks_factor::kLeafChunks, c1 = lv.size() * (c + 1) / ks_factor::kLeafChunks;
         for (size_t i = c0; i < c1; ++i)
           if (int rc = add(lv[i])) return rc;
+        if (int rc = flush()) return rc;  // a milestone per subtree and level
+        KS_CUDA(cudaEventRecord(f->ev_up_sublev[(size_t)c * f->npipe_first + lev], u));
       }
       if (int rc = flush()) return rc;
       KS_CUDA(cudaEventRecord(f->ev_up_sub[c], u));

@@ -208,6 +208,13 @@ int ks_get_phase_ms(const ks_factor* f, double* ms, int cap) {
   return n;
 }
 
+int ks_pipelined_levels(const ks_factor* f, int* out2) {
+  if (!f || !out2) return fail(KS_ERR_INVALID, "null argument");
+  out2[0] = f->npipe;
+  out2[1] = f->first_pipelined;
+  return KS_OK;
+}
+
 int ks_get_level_ms(const ks_factor* f, double* ms, int cap) {
   if (!f) return 0;
   const int n = std::min<int>(cap, (int)f->level_ms.size());

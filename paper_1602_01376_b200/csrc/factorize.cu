@@ -158,8 +158,9 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1, bool spl
 }
 
 static int enqueue_levels(ks_factor* f, cudaStream_t st, Launcher& L, int lev0, int lev1, int deferred_before = 0);
-static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool is_root_level);
+static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool is_root_level, int plan_count = -1);
 static ks::NodeBatch sub_batch(const ks::NodeBatch& nb, int off, int cnt);
+static int plan_batch(const ks_factor* f, int level_count);
 // subtree pipelining (ks_factor::npipe) in this factorization: the default 4
 // node groups, not under the per-level profiler or the tracer (their level
 // boundaries would blur); KS_PIPE=0 disables it
@@ -192,13 +193,21 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   if (f->upload_pending) KS_CUDA(cudaStreamWaitEvent(st, f->ev_up_coords, 0));
   if (int rc = L.check("start")) return rc;
   bool pipe = false, early = false;
-  int n_early = 0;
+  int n_early = 0, np = 0;  // np: levels pipelined per subtree in this factorization
+  bool first_side = false;  // the per-subtree estimates went to `side`
   if (int rc = mark(f->ev_phase[1])) return rc;
   {
     const int G = (nl >= 2 * 64) ? n_groups(f) : 1;
     pipe = pipelined(f, G);
-    early = pipe && f->knobs.hager_early && !trace_on();
-    n_early = early ? G : 0;
+    // uploads in flight: every subtree-local level right behind its subtree's
+    // uploads, each level's estimates at once beside the next level (the GPU
+    // has slack while PCIe gates the work; only the tail after the last byte counts)
+    const bool first = pipe && f->upload_pending && f->knobs.pipe_first;
+    if (first) np = f->first_pipelined = f->npipe_first;
+    else if (pipe) np = f->npipe;
+    early = pipe && (f->knobs.hager_early || first) && !trace_on();
+    first_side = early && first && f->knobs.first_hager_side;
+    n_early = (early && !first_side) ? G : 0;
     if (G > 1) {
       KS_CUDA(cudaEventRecord(f->gfork, st));
       for (int g = 0; g < G; ++g) KS_CUDA(cudaStreamWaitEvent(f->gst[g], f->gfork, 0));
@@ -217,18 +226,22 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
       const bool split = wait_p != nullptr && (f->d & 1) == 0 && f->n_int > 0 && f->knobs.split_leaf;
       if (int rc = enqueue_leaf_assemble(f, Lg, l0, l1, wait_p, split)) return rc;
       if (int rc = enqueue_leaf_chol(f, Lg, l0, l1, split, wait_p)) return rc;
-      if (pipe) {  // this subtree's nodes of the deepest npipe levels, on the same stream
-        if (f->upload_pending) KS_CUDA(cudaStreamWaitEvent(gs, f->ev_up_sub[g], 0));
-        for (int lev = 0; lev < f->npipe; ++lev) {
+      if (pipe) {  // this subtree's nodes of the deepest np levels, on the same stream
+        for (int lev = 0; lev < np; ++lev) {
+          if (f->upload_pending)
+            KS_CUDA(cudaStreamWaitEvent(gs, f->ev_up_sublev[(size_t)g * f->npipe_first + lev], 0));
           f->cur_tag = lev;
           const ks::NodeBatch nb = f->nodebatch(lev);
           const int c = nb.count / G;
           const ks::NodeBatch sb = sub_batch(nb, g * c, c);
-          if (int rc = enqueue_level_body(f, Lg, sb, false)) return rc;
+          if (int rc = enqueue_level_body(f, Lg, sb, false, plan_batch(f, nb.count))) return rc;
           if (early) {  // this subtree's estimates at once, beside its next level
+            // (behind uploads: all on `side` -- the subtrees finish in upload order, and
+            // more concurrently waiting streams than hardware queues serialize each other)
+            cudaStream_t hs = (first && f->knobs.first_hager_side) ? f->side : f->hst[g];
             KS_CUDA(cudaEventRecord(f->hfork[g], gs));
-            KS_CUDA(cudaStreamWaitEvent(f->hst[g], f->hfork[g], 0));
-            ks::launch_hager(dt, sb, f->dinv.p, f->lut.p, std::max(1, f->knobs.hager_ctas / G), f->hst[g]);
+            KS_CUDA(cudaStreamWaitEvent(hs, f->hfork[g], 0));
+            ks::launch_hager(dt, sb, f->dinv.p, f->lut.p, first ? 32 : std::max(1, f->knobs.hager_ctas / G), hs);
             L.count[0] += ks::hager_launches(sb);
           }
         }
@@ -246,11 +259,15 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   if (int rc = mark(f->ev_phase[3])) return rc;
   // ---- the shard's internal levels, deepest first (the pipelined ones are
   // done; their condition estimates are still to be launched) ----
-  if (int rc = enqueue_levels(f, st, L, pipe ? f->npipe : 0, f->n_local_levels, (pipe && !early) ? f->npipe : 0))
+  if (int rc = enqueue_levels(f, st, L, np, f->n_local_levels, (pipe && !early) ? np : 0))
     return rc;
   for (int g = 0; g < n_early; ++g) {
     KS_CUDA(cudaEventRecord(f->hjoin[g], f->hst[g]));
     KS_CUDA(cudaStreamWaitEvent(st, f->hjoin[g], 0));
+  }
+  if (first_side) {
+    KS_CUDA(cudaEventRecord(f->hjoin[0], f->side));
+    KS_CUDA(cudaStreamWaitEvent(st, f->hjoin[0], 0));
   }
   if (int rc = mark(f->ev_phase[4])) return rc;
   return KS_OK;
@@ -258,8 +275,17 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
 
 // Levels with at most KS_SLAB_MAX (default 4) nodes run the persistent
 // per-node LU (lu_slab.cu); KS_SLAB_MAX=0 keeps the launch sequence everywhere.
-static bool use_slab(const ks_factor* f, const ks::NodeBatch& nb) {
-  return nb.count <= f->knobs.slab_max && f->lu_sync.p && ks::slab_width(nb) > 0;
+static bool use_slab(const ks_factor* f, const ks::NodeBatch& nb, int plan_count) {
+  return plan_count <= f->knobs.slab_max && f->lu_sync.p && ks::slab_width(nb) > 0;
+}
+
+// The LU variant of a node (persistent LU / spine / plain recursion) follows
+// the batch size the REPLAYED schedule gives the node's level (a wide level's
+// node group, a narrow level whole), not the size of the sub-batch at hand:
+// the first factorization pipelines deeper (smaller sub-batches) and must give
+// the same bits as every later one.
+static int plan_batch(const ks_factor* f, int level_count) {
+  return level_count >= 64 ? std::max(1, level_count / n_groups(f)) : level_count;
 }
 
 // batches of at most KS_SPINE_MAX (default 16) nodes carry the P^T columns
@@ -272,7 +298,8 @@ static bool use_slab(const ks_factor* f, const ks::NodeBatch& nb) {
 // as DMMA GEMMs, ||Z||_1, then the LU of Aug's first s_pad columns with pivots
 // among S's rows (linalg.py:199-213 on the Schur complement of Z's identity
 // block) whose trailing block is H = P G Z^-1 P^T (solver.py:154-164).
-static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool is_root_level) {
+static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb, bool is_root_level, int plan_count) {
+  if (plan_count < 0) plan_count = nb.count;
   const ks::DevTree dt = f->devtree();
   const int S = nb.s_pad, T = nb.T, ZT = nb.zt;
   const int64_t TT = (int64_t)T * T, SS = (int64_t)S * S, XS = 2 * SS, PS = (int64_t)S * ZT;
@@ -337,7 +364,7 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
   ++L.count[0];
   if ((rc = L.check("znorm1"))) return rc;
   if (abl & 128) return KS_OK;
-  if (use_slab(f, nb)) {
+  if (use_slab(f, nb, plan_count)) {
     // narrow level: the whole LU, U12, Schur block and H in one cooperative launch
     // (its own ||.||_1 of the slabs goes to a scratch word: Z's norm is znorm1's)
     ks::NodeBatch sb = nb;
@@ -360,7 +387,7 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
   // batches keep the separate U12 TRSM and Schur GEMM (higher tensor-pipe rate).
   int pend[4] = {0, 0, 0, 0};
   const int TP = nb.t_pad;
-  const bool spine = nb.count <= f->knobs.spine_max;
+  const bool spine = plan_count <= f->knobs.spine_max;
   if ((rc = rlu(L, nb, 0, TP, f->pw, pend, spine ? S : 0))) return rc;
   if (!spine) {
     if ((rc = trsm_ul(L, nb, 0, TP, TP, S))) return rc;

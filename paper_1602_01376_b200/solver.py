@@ -148,6 +148,13 @@ class GpuHierFactor:
         n = _lib.load().ks_get_level_ms(self.handle, ms, 64)
         return [float(ms[i]) for i in range(n)]
 
+    def pipelined_levels(self) -> tuple[int, int]:
+        """(levels pipelined per subtree in a replayed factorization, levels the
+        first factorization pipelined behind its uploads)."""
+        out = (C.c_int * 2)()
+        _lib.load().ks_pipelined_levels(self.handle, out)
+        return int(out[0]), int(out[1])
+
     def trace_report(self) -> str:
         buf = C.create_string_buffer(1 << 16)
         _lib.load().ks_trace_report(self.handle, buf, len(buf))
