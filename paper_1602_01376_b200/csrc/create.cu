@@ -162,9 +162,37 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
   if (f->s_pad > 1024) { delete f; return fail(KS_ERR_UNSUPPORTED, "skeleton rank %lld too large (max 1024)", (long long)s_max); }
 
   const double t_plan = host_ms();
-  // the permutation first: the device gather of the points trusts it. Host
-  // worker threads (the inverse is N random writes): pass 1 range-checks and
-  // inverts, pass 2 confirms pos[perm[i]] == i (any duplicate fails it).
+  // The points and the permutation start their DMA at once (the largest fixed
+  // piece before any P block; it needs no validation result): the host checks
+  // below run while it is in flight, and the device gather that trusts the
+  // permutation is only queued after the permutation has been verified.
+  double* orig = nullptr;
+  int64_t* pmd = nullptr;
+  auto early_upload = [&]() -> int {
+    KS_CUDA(cudaStreamCreateWithFlags(&f->upl, cudaStreamNonBlocking));
+    cudaStream_t u = f->upl;
+    KS_CUDA(f->coords.alloc((size_t)(p->n + f->m_pad) * p->d));
+    KS_CUDA(f->xx.alloc((size_t)p->n + f->m_pad));
+    KS_CUDA(pool_alloc_async(reinterpret_cast<void**>(&orig), sizeof(double) * p->n * p->d, u));
+    KS_CUDA(pool_alloc_async(reinterpret_cast<void**>(&pmd), sizeof(int64_t) * p->n, u));
+    KS_CUDA(cudaMemsetAsync(f->coords.p + (size_t)p->n * p->d, 0, sizeof(double) * f->m_pad * p->d, u));
+    KS_CUDA(cudaMemcpyAsync(orig, p->coords, sizeof(double) * p->n * p->d, cudaMemcpyHostToDevice, u));
+    KS_CUDA(cudaMemcpyAsync(pmd, p->perm, sizeof(int64_t) * p->n, cudaMemcpyHostToDevice, u));
+    f->h2d_bytes += (int64_t)(sizeof(double) * p->n * p->d + sizeof(int64_t) * p->n);
+    return KS_OK;
+  };
+  // From here on the handle owns device memory and streams: errors go through ks_destroy.
+  auto abort_create = [&](int rc) {
+    if (f->upl) cudaStreamSynchronize(f->upl);
+    if (orig) pool_free(orig);
+    if (pmd) pool_free(pmd);
+    ks_destroy(f);
+    return rc;
+  };
+  auto bad2 = [&](const char* msg) { return abort_create(fail(KS_ERR_INVALID, "%s", msg)); };
+  if (int rc = early_upload()) return abort_create(rc);
+  // the permutation: host worker threads (the inverse is N random writes): pass 1
+  // range-checks and inverts, pass 2 confirms pos[perm[i]] == i (any duplicate fails it).
   auto parallel_for = [](int64_t n, auto&& body) {
     const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(16, n / (1 << 16)));
     std::vector<std::thread> th;
@@ -186,7 +214,7 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
       for (int64_t i = a; i < b; ++i)
         if (pos[p->perm[i]] != i) { perm_bad = 1; return; }
     });
-  if (perm_bad) return bad("perm is not a permutation");
+  if (perm_bad) return bad2("perm is not a permutation");
   const size_t nl = f->leaf_nodes.size();
   const int64_t nsk = p->skel_off[nn];
   std::vector<int> sp((size_t)nsk);
@@ -198,7 +226,7 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
       sp[i] = (int)pos[id];
     }
   });
-  if (skel_bad) return bad("skeleton id out of range");
+  if (skel_bad) return bad2("skeleton id out of range");
   std::vector<int64_t> so(p->skel_off, p->skel_off + nn + 1), co(p->coeff_off, p->coeff_off + nn + 1);
   std::vector<int> rk(nn);
   for (int64_t v = 0; v < nn; ++v) rk[v] = (int)f->rank[v];
@@ -214,11 +242,6 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     ileft.push_back((int)f->left[v]);
     iright.push_back((int)f->right[v]);
   }
-  // From here on the handle owns device memory and streams: errors go through ks_destroy.
-  auto abort_create = [&](int rc) {
-    ks_destroy(f);
-    return rc;
-  };
   auto alloc_all = [&]() -> int {
     KS_CUDA(f->rank_d.alloc(rk.size()));
     KS_CUDA(f->skel_pos.alloc(sp.size()));
@@ -258,8 +281,6 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(f->norm1_slab.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->norm1.alloc(std::max(f->n_int, 1)));
     KS_CUDA(f->cond.alloc(std::max(f->n_int, 1)));
-    KS_CUDA(f->coords.alloc((size_t)(p->n + f->m_pad) * p->d));
-    KS_CUDA(f->xx.alloc((size_t)p->n + f->m_pad));
     KS_CUDA(f->coeff.alloc((size_t)p->coeff_off[nn]));
     KS_CUDA(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
     KS_CUDA(cudaStreamCreateWithFlags(&f->side2, cudaStreamNonBlocking));
@@ -286,7 +307,6 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
   // factorization consumes them; the point-coordinate check overlaps the DMA.
   // Points: tree order on the device (coords_tree[i] = coords[perm[i]]) + norms.
   auto start_uploads = [&]() -> int {
-    KS_CUDA(cudaStreamCreateWithFlags(&f->upl, cudaStreamNonBlocking));
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_up_coords, cudaEventDisableTiming));
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_up_all, cudaEventDisableTiming));
     for (auto& e : f->ev_up_leaf) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -312,18 +332,13 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     if (int rc = put(f->int_node, inode)) return rc;
     if (int rc = put(f->int_left, ileft)) return rc;
     if (int rc = put(f->int_right, iright)) return rc;
-    double* orig = nullptr;
-    int64_t* pmd = nullptr;
-    KS_CUDA(pool_alloc_async(reinterpret_cast<void**>(&orig), sizeof(double) * p->n * p->d, u));
-    KS_CUDA(pool_alloc_async(reinterpret_cast<void**>(&pmd), sizeof(int64_t) * p->n, u));
-    KS_CUDA(cudaMemsetAsync(f->coords.p + (size_t)p->n * p->d, 0, sizeof(double) * f->m_pad * p->d, u));
-    KS_CUDA(cudaMemcpyAsync(orig, p->coords, sizeof(double) * p->n * p->d, cudaMemcpyHostToDevice, u));
-    KS_CUDA(cudaMemcpyAsync(pmd, p->perm, sizeof(int64_t) * p->n, cudaMemcpyHostToDevice, u));
-    f->h2d_bytes += (int64_t)(sizeof(double) * p->n * p->d + sizeof(int64_t) * p->n);
+    // the points (in flight since early_upload) to tree order, and their norms
     ks::launch_gather_rows(orig, pmd, p->n, p->d, f->coords.p, u);
     ks::launch_row_sqnorms(f->coords.p, p->n + f->m_pad, p->d, f->xx.p, u);
     KS_CUDA(cudaFreeAsync(orig, u));
+    orig = nullptr;
     KS_CUDA(cudaFreeAsync(pmd, u));
+    pmd = nullptr;
     KS_CUDA(cudaEventRecord(f->ev_up_coords, u));
     // P blocks: leaves in leaf order (a milestone event per leaf quarter), then
     // internal nodes level by level, deepest first (an event per level), then
