@@ -201,32 +201,33 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     for (auto& x : th) x.join();
   };
   std::vector<int64_t> pos(p->n);
-  std::atomic<int> perm_bad{0};
-  parallel_for(p->n, [&](int64_t a, int64_t b) {
-    for (int64_t i = a; i < b; ++i) {
-      const int64_t id = p->perm[i];
-      if (id < 0 || id >= p->n) { perm_bad = 1; return; }
-      pos[id] = i;
-    }
-  });
-  if (!perm_bad)
-    parallel_for(p->n, [&](int64_t a, int64_t b) {
-      for (int64_t i = a; i < b; ++i)
-        if (pos[p->perm[i]] != i) { perm_bad = 1; return; }
-    });
-  if (perm_bad) return bad2("perm is not a permutation");
+  std::atomic<int> perm_bad{0}, skel_bad{0};
   const size_t nl = f->leaf_nodes.size();
   const int64_t nsk = p->skel_off[nn];
   std::vector<int> sp((size_t)nsk);
-  std::atomic<int> skel_bad{0};
-  parallel_for(nsk, [&](int64_t a, int64_t b) {
-    for (int64_t i = a; i < b; ++i) {
-      const int64_t id = p->skel[i];
-      if (id < 0 || id >= p->n) { skel_bad = 1; return; }
-      sp[i] = (int)pos[id];
-    }
+  // (on a thread of its own, beside the allocations below)
+  std::thread host_checks([&]() {
+    parallel_for(p->n, [&](int64_t a, int64_t b) {
+      for (int64_t i = a; i < b; ++i) {
+        const int64_t id = p->perm[i];
+        if (id < 0 || id >= p->n) { perm_bad = 1; return; }
+        pos[id] = i;
+      }
+    });
+    if (!perm_bad)
+      parallel_for(p->n, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i)
+          if (pos[p->perm[i]] != i) { perm_bad = 1; return; }
+      });
+    if (perm_bad) return;
+    parallel_for(nsk, [&](int64_t a, int64_t b) {
+      for (int64_t i = a; i < b; ++i) {
+        const int64_t id = p->skel[i];
+        if (id < 0 || id >= p->n) { skel_bad = 1; return; }
+        sp[i] = (int)pos[id];
+      }
+    });
   });
-  if (skel_bad) return bad2("skeleton id out of range");
   std::vector<int64_t> so(p->skel_off, p->skel_off + nn + 1), co(p->coeff_off, p->coeff_off + nn + 1);
   std::vector<int> rk(nn);
   for (int64_t v = 0; v < nn; ++v) rk[v] = (int)f->rank[v];
@@ -301,7 +302,11 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_join, cudaEventDisableTiming));
     return KS_OK;
   };
-  if (int rc = alloc_all()) return abort_create(rc);
+  const int alloc_rc = alloc_all();
+  host_checks.join();
+  if (alloc_rc) return abort_create(alloc_rc);
+  if (perm_bad) return bad2("perm is not a permutation");
+  if (skel_bad) return bad2("skeleton id out of range");
   const double t_alloc = host_ms();
   // ---- asynchronous uploads on the upload stream, in the order the first
   // factorization consumes them; the point-coordinate check overlaps the DMA.
