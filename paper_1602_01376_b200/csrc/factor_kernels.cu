@@ -310,23 +310,6 @@ __global__ void k_sym_h(double* H, int64_t stride, const int* idx, int s) {
   }
 }
 
-// Upper triangle := lower triangle (SYRK computed on lower tiles only).
-__global__ void k_mirror_lower(double* H, int64_t stride, const int* idx, int s) {
-  pdl_wait();
-  double* h = H + (int64_t)idx[blockIdx.y] * stride;
-  const int64_t total = (int64_t)s * s;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / s), j = (int)(e % s);
-    if (j > i) h[e] = h[(int64_t)j * s + i];
-  }
-}
-
-void launch_mirror_lower(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st) {
-  if (count <= 0 || s_pad <= 0) return;
-  dim3 g(32, count);
-  launch_pdl(k_mirror_lower, g, dim3(256), 0, st, H, h_stride, node_idx, s_pad);
-}
-
 void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st) {
   if (count <= 0 || s_pad <= 0) return;
   dim3 g(32, count);

@@ -143,15 +143,12 @@ static int enqueue_leaf_chol(ks_factor* f, Launcher& L, int l0, int l1, bool spl
   if (S > 0 && f->n_int > 0 && !(f->knobs.ablate & 16)) {
     Operand A{leafA + (int64_t)M * M, M, AS, nullptr};
     OperandW C{f->hbuf.p, S, (int64_t)S * S, lb.node};
-    // SYRK: lower-triangular tiles only, then mirrored (H exactly symmetric, so
-    // the reference's 0.5 (H + H^T) is the identity on it)
-    GemmArgs g = mk(S, S, M, nl, A, A, C, 1.0, 0.0);
-    g.tri = 1;
-    int rc = L.gemm(g, false, true, "leaf_syrk");
-    if (rc) return rc;
-    ks::launch_mirror_lower(f->hbuf.p, (int64_t)S * S, lb.node, nl, S, st);
+    // SYRK: tiles on and below the diagonal, mirrored by the epilogue (H exactly
+    // symmetric, so the reference's 0.5 (H + H^T) is the identity on it)
     ++L.count[0];
-    if (int rc = L.check("sym_h")) return rc;
+    cudaError_t e = ks::gemm_syrk(mk(S, S, M, nl, A, A, C, 1.0, 0.0), st);
+    if (e != cudaSuccess) return fail(KS_ERR_CUDA, "leaf syrk: %s", cudaGetErrorString(e));
+    if (int rc = L.check("leaf_syrk")) return rc;
   }
   KS_CUDA(cudaGetLastError());
   return KS_OK;

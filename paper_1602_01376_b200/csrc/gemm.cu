@@ -170,6 +170,16 @@ cudaError_t gemm_small_tile(const GemmArgs& g, cudaStream_t st) {
   return launch<64, 64, 2, 4, false, true, 4>(g, st);
 }
 
+cudaError_t gemm_syrk(const GemmArgs& g, cudaStream_t st) {
+  if (g.M <= 0 || g.batch <= 0) return cudaSuccess;
+  if (g.M != g.N || ((g.M | g.K) & 1) || g.K <= 0 || ((g.A.ld | g.B.ld | g.C.ld) & 1) || g.beta != 0.0)
+    return cudaErrorInvalidValue;
+  GemmArgs t = g;
+  t.tri = 1;
+  // 64 x 64 tiles: 10 of the 16 tiles of a 256 x 256 block are computed (6 of 8 with 128 x 64)
+  return launch<64, 64, 2, 2, false, true, 4, 5>(t, st);
+}
+
 cudaError_t gemm_update_trsm(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.batch <= 0) return cudaSuccess;
   if (g.N != 64 || (g.K & 1) || g.K <= 0 || ((g.A.ld | g.B.ld | g.C.ld | g.E.ld) & 1)) return cudaErrorInvalidValue;

@@ -50,6 +50,11 @@ struct KrrEpi {
   double den;        // 1 / (-2 h h)
 };
 
+//   5  SYRK C = alpha * A A^T (BM == BN, tri = 1): tiles strictly above the diagonal
+//      are skipped, tiles below it also store their transpose, diagonal tiles
+//      compute both halves (the two sums have the same terms in the same order, so
+//      C is symmetric bit for bit: the reference's 0.5 (H + H^T), solver.py:135, is
+//      the identity on it).
 //   4  coupling block B = K(S_l, S_r) from the Gram product of gathered skeleton
 //      coordinates (kernels.py:107-111 in GEMM form, compress.py:281-283):
 //      C[r][c] = exp(max(xa_r + xb_c - 2G, 0) / (-2 h h)) for r < rank(na[b]),
@@ -418,6 +423,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
   double den = 0.0, lam = 0.0;
   int bsz = 0, bbeg = 0;
   const double* Cin = (EPI == 0 && g.Cin.ptr) ? g.Cin.at(b) : nullptr;
+  (void)Cin;
   if (EPI == 1) {
     den = 1.0 / (-2.0 * g.ge.h * g.ge.h);  // multiply by the reciprocal: one rounding in the exponent
     lam = *g.ge.lam;
@@ -493,6 +499,12 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
         }
       }
       *p = v;
+      if constexpr (EPI == 5) {  // SYRK: tiles below the diagonal also write their mirror image
+        if (n0 < m0) {
+          C[(int64_t)c * g.C.ld + r] = v.x;
+          C[(int64_t)(c + 1) * g.C.ld + r] = v.y;
+        }
+      }
     }
   }
 }
@@ -531,6 +543,8 @@ cudaError_t gemm(const GemmArgs& g, bool ta, bool tb, cudaStream_t st);
 cudaError_t gemm_gauss(const GemmArgs& g, cudaStream_t st);
 // 64 x 64 outputs with long K (op(B) = B^T), 8 warps per tile.
 cudaError_t gemm_small_tile(const GemmArgs& g, cudaStream_t st);
+// C = alpha * A A^T, symmetric output written in full (EPI == 5): M == N, op(B) = B^T with B = A.
+cudaError_t gemm_syrk(const GemmArgs& g, cudaStream_t st);
 // Panel update with the panel TRSM folded in (EPI == 2): N must be 64, op(B) = B^T.
 cudaError_t gemm_update_trsm(const GemmArgs& g, cudaStream_t st);
 // gg.count problems of one shape (M, N, K, batch, alpha/beta per problem), no

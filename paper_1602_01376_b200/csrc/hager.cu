@@ -436,7 +436,7 @@ int hager_launches(const NodeBatch& nb) { return (nb.t_pad <= 512 && nb.count < 
 // factors are still in L2 (narrow levels); for wide levels the extra HBM pass
 // costs more than it saves.
 void launch_hager(const DevTree& t, const NodeBatch& nb, double* dinv, double* lut, int max_ctas, cudaStream_t st) {
-  static const int abl = std::getenv("KS_ABLATE") ? std::atoi(std::getenv("KS_ABLATE")) : 0;  // timing experiment
+  const int abl = std::getenv("KS_ABLATE") ? std::atoi(std::getenv("KS_ABLATE")) : 0;  // timing experiment (tools/ablate.py)
   if (abl & 256) return;
   const int S = nb.t_pad;
   const bool cm = lut && nb.count < 64 && S <= 512;

@@ -74,7 +74,6 @@ void launch_leaf_copy_p(const DevTree& t, const LeafBatch& lb, cudaStream_t st);
 void launch_leaf_assemble(const DevTree& t, const LeafBatch& lb, const double* lam, cudaStream_t st);
 void launch_potrf64(const LeafBatch& lb, int j0, double* inv, int* info, cudaStream_t st);
 void launch_sym_h(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st);
-void launch_mirror_lower(double* H, int64_t h_stride, const int* node_idx, int count, int s_pad, cudaStream_t st);
 void launch_coupling(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
 // block formulation (node_kernels.cu): S = I and E = P_r^T blocks of Aug, the padded P copy
 void launch_p_layout(const DevTree& t, const NodeBatch& nb, cudaStream_t st);
