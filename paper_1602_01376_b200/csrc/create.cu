@@ -288,7 +288,18 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_fork2, cudaEventDisableTiming));
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_join2, cudaEventDisableTiming));
     KS_CUDA(cudaStreamCreateWithFlags(&f->cap, cudaStreamNonBlocking));
-    for (auto& g : f->gst) KS_CUDA(cudaStreamCreateWithFlags(&g, cudaStreamNonBlocking));
+    {
+      // KS_GROUP_PRIO=1: descending priorities over the group streams, so the groups
+      // leave the leaf phase one after another and a finished group's latency-bound
+      // internal levels run under the later groups' leaf GEMMs (instead of all eight
+      // subtrees reaching their levels in lockstep)
+      int lo = 0, hi = 0;  // least, greatest (numerically lower = higher priority)
+      KS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      for (int g = 0; g < ks_factor::kGroups; ++g) {
+        const int pr = f->knobs.group_prio ? std::min(lo, std::max(hi, hi + g)) : lo;
+        KS_CUDA(cudaStreamCreateWithPriority(&f->gst[g], cudaStreamNonBlocking, pr));
+      }
+    }
     for (auto& g : f->hst) KS_CUDA(cudaStreamCreateWithFlags(&g, cudaStreamNonBlocking));
     for (auto& e : f->hfork) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : f->hjoin) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

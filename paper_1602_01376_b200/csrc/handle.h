@@ -58,6 +58,7 @@ struct Knobs {
   bool unfused_leaf_trsm = false;  // KS_UNFUSED_LEAF_TRSM=1: separate leaf update and TRSM GEMMs
   bool pipe_first = false;     // KS_PIPE_FIRST=1: the first factorization (behind its uploads) pipelines every subtree-local level (measured: no gain)
   bool first_hager_side = false;  // KS_FIRST_HAGER_SIDE=1: the first factorization's per-subtree estimates on one stream
+  bool group_prio = false;     // KS_GROUP_PRIO=1: descending stream priorities over the leaf groups / subtrees
   bool split_leaf = true;      // KS_SPLIT_LEAF=0: the first factorization waits for the leaves' P up front
   int hager_ctas = 96;         // KS_HAGER_CTAS: CTAs of the deferred wide-level estimates
   int hager_flush = 0;         // KS_HAGER_FLUSH: start the deferred estimates at levels <= n nodes
