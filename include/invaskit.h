@@ -159,8 +159,8 @@ int ks_get_phase_ms(const ks_factor* f, double* ms, int cap);
 /* Per internal level (deepest first) main-stream time of the last factorization. */
 int ks_get_level_ms(const ks_factor* f, double* ms, int cap);
 /* Levels the schedule runs per subtree on the subtree's own stream (subtree
- * pipelining): out2[0] in a replayed factorization, out2[1] in the last first
- * factorization that ran behind its uploads (0 if it did not pipeline). */
+ * pipelining): out2[0] as planned, out2[1] as enabled for this handle (0 when
+ * KS_PIPE=0 or the group count disables it). */
 int ks_pipelined_levels(const ks_factor* f, int* out2);
 /* With KS_TRACE=1 in the environment: per-kernel device time table of the last
  * factorization (events after every launch on the launching stream). */

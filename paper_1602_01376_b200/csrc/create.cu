@@ -125,7 +125,7 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     for (int lev = 0; lev < f->n_local_levels && nlv % G == 0; ++lev) {
       const auto& lv = f->levels[lev];
       const int c = (int)lv.size();
-      if (c % G || c / G < 1) break;
+      if (c % G || c / G < f->knobs.pipe_min) break;
       bool ok = true;
       for (int i = 0; i < c; ++i) {
         const int g = i / (c / G), v = lv[i];
@@ -133,12 +133,8 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
       }
       if (!ok) break;
       for (int i = 0; i < c; ++i) grp[lv[i]] = i / (c / G);
-      if (f->npipe == lev && c / G >= f->knobs.pipe_min) f->npipe = lev + 1;
-      // the first factorization (uploads in flight) pipelines every
-      // subtree-local level: the subtrees finish staggered behind their uploads
-      f->npipe_first = lev + 1;
+      f->npipe = lev + 1;
     }
-    if (f->npipe == 0 || !f->knobs.pipe_first) f->npipe_first = f->npipe;
   }
   f->m_pad = (int)roundup(m_max, 64);
   f->s_pad = (int)roundup(s_max, 64);
@@ -288,18 +284,7 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_fork2, cudaEventDisableTiming));
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_join2, cudaEventDisableTiming));
     KS_CUDA(cudaStreamCreateWithFlags(&f->cap, cudaStreamNonBlocking));
-    {
-      // KS_GROUP_PRIO=1: descending priorities over the group streams, so the groups
-      // leave the leaf phase one after another and a finished group's latency-bound
-      // internal levels run under the later groups' leaf GEMMs (instead of all eight
-      // subtrees reaching their levels in lockstep)
-      int lo = 0, hi = 0;  // least, greatest (numerically lower = higher priority)
-      KS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      for (int g = 0; g < ks_factor::kGroups; ++g) {
-        const int pr = f->knobs.group_prio ? std::min(lo, std::max(hi, hi + g)) : lo;
-        KS_CUDA(cudaStreamCreateWithPriority(&f->gst[g], cudaStreamNonBlocking, pr));
-      }
-    }
+    for (auto& g : f->gst) KS_CUDA(cudaStreamCreateWithFlags(&g, cudaStreamNonBlocking));
     for (auto& g : f->hst) KS_CUDA(cudaStreamCreateWithFlags(&g, cudaStreamNonBlocking));
     for (auto& e : f->hfork) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : f->hjoin) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -327,7 +312,7 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_up_all, cudaEventDisableTiming));
     for (auto& e : f->ev_up_leaf) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : f->ev_up_sub) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    f->ev_up_sublev.resize((size_t)ks_factor::kLeafChunks * f->npipe_first);
+    f->ev_up_sublev.resize((size_t)ks_factor::kLeafChunks * f->npipe);
     for (auto& e : f->ev_up_sublev) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     f->ev_up_level.resize(f->levels.size());
     for (auto& e : f->ev_up_level) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -392,13 +377,13 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     }
     for (int c = 0; c < ks_factor::kLeafChunks; ++c) {
       // with subtree pipelining: this subtree's nodes of the pipelined levels
-      for (int lev = 0; lev < f->npipe_first; ++lev) {
+      for (int lev = 0; lev < f->npipe; ++lev) {
         const auto& lv = f->levels[lev];
         const size_t c0 = lv.size() * c / ks_factor::kLeafChunks, c1 = lv.size() * (c + 1) / ks_factor::kLeafChunks;
         for (size_t i = c0; i < c1; ++i)
           if (int rc = add(lv[i])) return rc;
         if (int rc = flush()) return rc;  // a milestone per subtree and level
-        KS_CUDA(cudaEventRecord(f->ev_up_sublev[(size_t)c * f->npipe_first + lev], u));
+        KS_CUDA(cudaEventRecord(f->ev_up_sublev[(size_t)c * f->npipe + lev], u));
       }
       if (int rc = flush()) return rc;
       KS_CUDA(cudaEventRecord(f->ev_up_sub[c], u));

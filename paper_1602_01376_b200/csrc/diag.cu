@@ -211,7 +211,7 @@ int ks_get_phase_ms(const ks_factor* f, double* ms, int cap) {
 int ks_pipelined_levels(const ks_factor* f, int* out2) {
   if (!f || !out2) return fail(KS_ERR_INVALID, "null argument");
   out2[0] = f->npipe;
-  out2[1] = f->first_pipelined;
+  out2[1] = (f->npipe > 0 && f->knobs.pipe && f->knobs.groups == ks_factor::kLeafChunks) ? f->npipe : 0;
   return KS_OK;
 }
 

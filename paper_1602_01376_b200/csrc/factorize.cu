@@ -191,20 +191,13 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   if (int rc = L.check("start")) return rc;
   bool pipe = false, early = false;
   int n_early = 0, np = 0;  // np: levels pipelined per subtree in this factorization
-  bool first_side = false;  // the per-subtree estimates went to `side`
   if (int rc = mark(f->ev_phase[1])) return rc;
   {
     const int G = (nl >= 2 * 64) ? n_groups(f) : 1;
     pipe = pipelined(f, G);
-    // uploads in flight: every subtree-local level right behind its subtree's
-    // uploads, each level's estimates at once beside the next level (the GPU
-    // has slack while PCIe gates the work; only the tail after the last byte counts)
-    const bool first = pipe && f->upload_pending && f->knobs.pipe_first;
-    if (first) np = f->first_pipelined = f->npipe_first;
-    else if (pipe) np = f->npipe;
-    early = pipe && (f->knobs.hager_early || first) && !trace_on();
-    first_side = early && first && f->knobs.first_hager_side;
-    n_early = (early && !first_side) ? G : 0;
+    if (pipe) np = f->npipe;
+    early = pipe && f->knobs.hager_early && !trace_on();
+    n_early = early ? G : 0;
     if (G > 1) {
       KS_CUDA(cudaEventRecord(f->gfork, st));
       for (int g = 0; g < G; ++g) KS_CUDA(cudaStreamWaitEvent(f->gst[g], f->gfork, 0));
@@ -226,19 +219,16 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
       if (pipe) {  // this subtree's nodes of the deepest np levels, on the same stream
         for (int lev = 0; lev < np; ++lev) {
           if (f->upload_pending)
-            KS_CUDA(cudaStreamWaitEvent(gs, f->ev_up_sublev[(size_t)g * f->npipe_first + lev], 0));
+            KS_CUDA(cudaStreamWaitEvent(gs, f->ev_up_sublev[(size_t)g * f->npipe + lev], 0));
           f->cur_tag = lev;
           const ks::NodeBatch nb = f->nodebatch(lev);
           const int c = nb.count / G;
           const ks::NodeBatch sb = sub_batch(nb, g * c, c);
           if (int rc = enqueue_level_body(f, Lg, sb, false, plan_batch(f, nb.count))) return rc;
           if (early) {  // this subtree's estimates at once, beside its next level
-            // (behind uploads: all on `side` -- the subtrees finish in upload order, and
-            // more concurrently waiting streams than hardware queues serialize each other)
-            cudaStream_t hs = (first && f->knobs.first_hager_side) ? f->side : f->hst[g];
             KS_CUDA(cudaEventRecord(f->hfork[g], gs));
-            KS_CUDA(cudaStreamWaitEvent(hs, f->hfork[g], 0));
-            ks::launch_hager(dt, sb, f->dinv.p, f->lut.p, first ? 32 : std::max(1, f->knobs.hager_ctas / G), hs);
+            KS_CUDA(cudaStreamWaitEvent(f->hst[g], f->hfork[g], 0));
+            ks::launch_hager(dt, sb, f->dinv.p, f->lut.p, std::max(1, f->knobs.hager_ctas / G), f->hst[g]);
             L.count[0] += ks::hager_launches(sb);
           }
         }
@@ -261,10 +251,6 @@ static int enqueue_factorization(ks_factor* f, cudaStream_t st) {
   for (int g = 0; g < n_early; ++g) {
     KS_CUDA(cudaEventRecord(f->hjoin[g], f->hst[g]));
     KS_CUDA(cudaStreamWaitEvent(st, f->hjoin[g], 0));
-  }
-  if (first_side) {
-    KS_CUDA(cudaEventRecord(f->hjoin[0], f->side));
-    KS_CUDA(cudaStreamWaitEvent(st, f->hjoin[0], 0));
   }
   if (int rc = mark(f->ev_phase[4])) return rc;
   return KS_OK;

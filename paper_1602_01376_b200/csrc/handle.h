@@ -56,9 +56,6 @@ struct Knobs {
   int panel_w = 0;             // KS_PANEL_W: 32 / 8 override the register-panel width
   bool fused_merge = false;    // KS_FUSED_MERGE=1: TRSM + update merge in one launch (slower)
   bool unfused_leaf_trsm = false;  // KS_UNFUSED_LEAF_TRSM=1: separate leaf update and TRSM GEMMs
-  bool pipe_first = false;     // KS_PIPE_FIRST=1: the first factorization (behind its uploads) pipelines every subtree-local level (measured: no gain)
-  bool first_hager_side = false;  // KS_FIRST_HAGER_SIDE=1: the first factorization's per-subtree estimates on one stream
-  bool group_prio = false;     // KS_GROUP_PRIO=1: descending stream priorities over the leaf groups / subtrees
   bool split_leaf = true;      // KS_SPLIT_LEAF=0: the first factorization waits for the leaves' P up front
   int hager_ctas = 96;         // KS_HAGER_CTAS: CTAs of the deferred wide-level estimates
   int hager_flush = 0;         // KS_HAGER_FLUSH: start the deferred estimates at levels <= n nodes
@@ -146,8 +143,6 @@ struct ks_factor {
   // subtrees, each factored on its own stream right after its own leaves
   // (children of a subtree's nodes lie in the same subtree one level down)
   int npipe = 0;
-  int npipe_first = 0;  // the same for the first factorization (every subtree-local level)
-  int first_pipelined = 0;  // levels the first factorization actually pipelined (diagnostic)
   int64_t loc_begin = 0, loc_end = 0;   // tree-order rows owned by the shard
   std::vector<int64_t> peers;           // nodes at the shard level (all shards' roots)
   bool local_factored = false;
@@ -209,7 +204,7 @@ struct ks_factor {
   cudaStream_t upl = nullptr;
   cudaEvent_t ev_up_coords = nullptr, ev_up_all = nullptr, ev_up_leaf[kLeafChunks] = {}, ev_up_sub[kLeafChunks] = {};
   std::vector<cudaEvent_t> ev_up_level;
-  std::vector<cudaEvent_t> ev_up_sublev;  // [subtree][level < npipe_first]
+  std::vector<cudaEvent_t> ev_up_sublev;  // [subtree][level < npipe]
   bool upload_pending = false;
   int64_t h2d_bytes = 0;  // host -> device bytes ks_create copied (operator inputs this handle reads)
   // diagnostics

@@ -50,9 +50,6 @@ Knobs read_knobs() {
   k.fused_merge = env_flag("KS_FUSED_MERGE", false);
   k.unfused_leaf_trsm = env_flag("KS_UNFUSED_LEAF_TRSM", false);
   k.split_leaf = env_flag("KS_SPLIT_LEAF", k.split_leaf);
-  k.pipe_first = env_flag("KS_PIPE_FIRST", k.pipe_first);
-  k.group_prio = env_flag("KS_GROUP_PRIO", k.group_prio);
-  k.first_hager_side = env_flag("KS_FIRST_HAGER_SIDE", k.first_hager_side);
   k.hager_ctas = std::max(1, env_int("KS_HAGER_CTAS", k.hager_ctas));
   k.hager_flush = env_int("KS_HAGER_FLUSH", k.hager_flush);
   k.hager_split = env_flag("KS_HAGER_SPLIT", k.hager_split);

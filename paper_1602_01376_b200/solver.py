@@ -149,8 +149,8 @@ class GpuHierFactor:
         return [float(ms[i]) for i in range(n)]
 
     def pipelined_levels(self) -> tuple[int, int]:
-        """(levels pipelined per subtree in a replayed factorization, levels the
-        first factorization pipelined behind its uploads)."""
+        """(levels planned to run per subtree on the subtree's own stream, the same
+        if subtree pipelining is enabled for this handle, else 0)."""
         out = (C.c_int * 2)()
         _lib.load().ks_pipelined_levels(self.handle, out)
         return int(out[0]), int(out[1])

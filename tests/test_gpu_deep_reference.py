@@ -32,7 +32,7 @@ def _sha(a, dt):
 @pytest.mark.parametrize("case,pipe_min", [("cfg2_full", None), ("cfg4_64k", None), ("cfg3_128k", None),
                                            ("cfg5_32k", None), ("cfg4_64k", "1"), ("cfg3_128k", "1")])
 def test_deep_tree_matches_reference(case, pipe_min, monkeypatch):
-    """pipe_min = "1" (KS_PIPE_MIN=1, KS_PIPE_FIRST=1): every subtree-local level is
+    """pipe_min = "1" (KS_PIPE_MIN=1): every subtree-local level is
     pipelined per subtree on its own stream (8-, 4-, 2- and 1-node sub-batches,
     per-level condition estimates beside the next level) in the first
     factorization and in the replayed graph of the second; each node's LU variant
@@ -66,11 +66,9 @@ def test_deep_tree_matches_reference(case, pipe_min, monkeypatch):
 
     if pipe_min:
         monkeypatch.setenv("KS_PIPE_MIN", pipe_min)
-        monkeypatch.setenv("KS_PIPE_FIRST", "1")
     hf = ks.factorize(op, cfg.lam)
     if pipe_min:
         monkeypatch.delenv("KS_PIPE_MIN")
-        monkeypatch.delenv("KS_PIPE_FIRST")
     u = ks.solve_many(hf, b)
     if pipe_min:
         assert hf.pipelined_levels()[1] >= 3  # the deep per-subtree pipeline really ran
