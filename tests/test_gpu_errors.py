@@ -81,3 +81,37 @@ def test_error_leaves_the_library_usable(golden):
         assert rel(ks.solve_many(hf, g["b"]), g["u"]) <= 1e-10
     finally:
         hf.close()
+
+
+@pytest.mark.parametrize("what,msg", [("perm_dup", "perm is not a permutation"),
+                                      ("perm_range", "perm is not a permutation"),
+                                      ("skel_range", "skeleton id out of range"),
+                                      ("coords_nan", "non-finite"),
+                                      ("tree", "children do not split the parent range")])
+def test_create_rejects_bad_operator_inputs(golden, what, msg):
+    """ks_create starts the points' DMA before its host-side validation has finished
+    (DESIGN §1.1): a rejected problem must abort cleanly with those copies in
+    flight -- InvalidArgumentError with the reason (the reference validates its
+    tree and point arrays the same way: tree.py:98-127, points.py:38-63), no
+    leaked handle, and the next, valid factorization is unaffected."""
+    import paper_1602_01376_b200 as ks
+    g = dict(golden("cfg1"))
+    bad = {k: np.array(v, copy=True) if isinstance(v, np.ndarray) else v for k, v in g.items()}
+    if what == "perm_dup":
+        bad["perm"][1] = bad["perm"][0]
+    elif what == "perm_range":
+        bad["perm"][3] = bad["perm"].size
+    elif what == "skel_range":
+        bad["skel"][5] = bad["coords"].shape[0] + 7
+    elif what == "coords_nan":
+        bad["coords"][17, 0] = np.nan
+    else:
+        bad["node_end"][1] -= 1
+    with pytest.raises(ks.InvalidArgumentError, match=msg):
+        ks.factorize(bad, float(g["lam"]))
+    hf = ks.factorize(g, float(g["lam"]))
+    try:
+        u = ks.solve_many(hf, g["b"])
+        assert rel(u, g["u"]) <= 1e-10
+    finally:
+        hf.close()
