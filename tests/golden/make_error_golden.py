@@ -3,8 +3,9 @@
 Run in the build container (needs /root/reference):
     python tests/golden/make_error_golden.py
 
-Two tiny operators whose reduced systems Z (solver.py:138-149) fail the way the
-reference reports it, each with the failing node NOT the root:
+Tiny operators that fail the way the reference reports it (the first two in a
+reduced system Z, solver.py:138-149, with the failing node NOT the root; the third
+in a leaf):
 
 * singular.npz  -- two coincident points (exactly representable coordinates)
   are the skeletons of two sibling leaves, lambda = 0: the leaf blocks are
@@ -15,6 +16,10 @@ reference reports it, each with the failing node NOT the root:
   det Z = 1 - B^2 H_l H_r = 1e-15 at their parent (node 2): the Hager estimate
   (linalg.py:282-304) is ~4e15 > 1e14 and the reference raises
   IllConditionedError(2, cond) (solver.py:150-152).
+
+* leaf_not_spd.npz -- a leaf with two coincident points at lambda = 0: the Cholesky
+  fails (NotSPDError), the LU fallback (solver.py:125-131) meets an exactly zero pivot
+  column: SingularMatrixError raised from the leaf.
 
 The tree and leaf blocks are the reference's own (build_tree, compress); the
 rank-1 skeletons and P are set by hand and the couplings recomputed with the
@@ -133,6 +138,29 @@ def make_illcond_hard() -> None:
     raise AssertionError("reference did not raise IllConditionedError")
 
 
+def make_leaf_not_spd() -> None:
+    # sorted x: leaves {0, 0} {100, 101} {200, 201} {300, 301}: the first leaf holds
+    # two coincident points, so at lambda = 0 its block is exactly [[1, 1], [1, 1]]:
+    # _cholesky meets the pivot 1 - 1*1 = 0 (NotSPDError, linalg.py:190-192), factorize
+    # falls back to the pivoted LU (solver.py:125-131), whose second column is exactly
+    # zero: SingularMatrixError (linalg.py:205-206) from the LEAF. No rounding is
+    # involved, so the GPU must detect the same pivot in its blocked Cholesky.
+    x = np.array([0.0, 0.0, 100.0, 101.0, 200.0, 201.0, 300.0, 301.0])
+    ck = _ck(x, 1.0)
+    lv = _leaves(ck)
+    assert [nd.id for nd in lv] == [3, 4, 5, 6]
+    assert set(ck.tree.node_points(3)) == {0, 1}
+    _set_skeletons(ck, {3: 0, 4: 2, 5: 4, 6: 6}, {})
+    try:
+        ks.factorize(ck, 0.0)
+    except ks.SingularMatrixError as exc:
+        assert "elimination step 1" in str(exc)
+        _save("leaf_not_spd", ck, 0.0, exc)
+        return
+    raise AssertionError("reference did not raise SingularMatrixError")
+
+
 if __name__ == "__main__":
     make_singular()
     make_illcond_hard()
+    make_leaf_not_spd()

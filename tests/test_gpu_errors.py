@@ -8,6 +8,9 @@ public API over the C-ABI, against fixtures made by running the reference:
                    IllConditionedError(node_id, cond) (solver.py:150-152)
 * singular.npz     an exactly singular Z at node 1: SingularMatrixError
                    (linalg.py:205-206)
+* leaf_not_spd.npz a leaf block that is exactly [[1, 1], [1, 1]]: Cholesky failure
+                   detected, LU fallback (solver.py:125-131), SingularMatrixError
+                   from the leaf
 """
 import numpy as np
 import pytest
@@ -66,6 +69,19 @@ def test_singular_matrix_error(golden):
     g = golden("singular")
     assert str(g["expect_error"]) == "SingularMatrixError"
     with pytest.raises(ks.SingularMatrixError, match="node 1"):
+        ks.factorize(g, float(g["lam"]))
+
+
+def test_leaf_not_spd_goes_through_the_lu_fallback(golden):
+    """A leaf with two coincident points at lambda = 0: its block is exactly
+    [[1, 1], [1, 1]], so the blocked Cholesky (k_potrf64) must flag the zero pivot
+    (NotSPDError in the reference, linalg.py:190-192), the leaf is re-factored by
+    the pivoted LU (solver.py:125-131), and that LU meets the exactly zero column the
+    reference's does: SingularMatrixError at elimination step 1, from the leaf."""
+    import paper_1602_01376_b200 as ks
+    g = golden("leaf_not_spd")
+    assert str(g["expect_error"]) == "SingularMatrixError"
+    with pytest.raises(ks.SingularMatrixError, match="leaf 3: zero pivot column at elimination step 1"):
         ks.factorize(g, float(g["lam"]))
 
 

@@ -66,7 +66,8 @@ def test_oracle_diagnostics(factored, case):
     assert len(of.diagnostics["warnings"]) == int(g["n_warnings"])
 
 
-@pytest.mark.parametrize("case,exc", [("singular", O.Singular), ("illcond_hard", O.IllConditioned)])
+@pytest.mark.parametrize("case,exc", [("singular", O.Singular), ("illcond_hard", O.IllConditioned),
+                                      ("leaf_not_spd", O.Singular)])
 def test_oracle_error_paths(golden, case, exc):
     """The oracle raises where the reference raised (tests/golden/make_error_golden.py)."""
     g = golden(case)
