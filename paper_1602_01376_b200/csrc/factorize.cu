@@ -338,6 +338,7 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
                  OperandW{Fb, T, TT, nullptr}, 1.0, 1.0);
     g2.p[3] = mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{nb.PT, S, PTS, nullptr},
                  OperandW{Cb, T, TT, nullptr}, 1.0, 0.0);
+    g2.p[3].tri = 2;  // C = P_l H_l P_l^T is symmetric: tiles on and below the diagonal, mirrored
     ++L.count[0];
     if (abl & 64) {
     } else if (cudaError_t e = ks::gemm_group(g2, st)) return fail(KS_ERR_CUDA, "assembly stage 2: %s", cudaGetErrorString(e));
@@ -374,9 +375,11 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
   if ((rc = rlu(L, nb, 0, TP, f->pw, pend, spine ? S : 0))) return rc;
   if (!spine) {
     if ((rc = trsm_ul(L, nb, 0, TP, TP, S))) return rc;
-    if ((rc = L.gemm(mk(S, S, TP, cnt, Operand{Fb, T, TT, nullptr}, Operand{Eb, T, TT, nullptr},
-                        OperandW{Cb, T, TT, nullptr}, -1.0, 1.0), false, false, "schur")))
-      return rc;
+    // H = C - F S^-1 E is symmetric like C: the same 10 of 16 tiles, mirrored
+    GemmArgs gs = mk(S, S, TP, cnt, Operand{Fb, T, TT, nullptr}, Operand{Eb, T, TT, nullptr},
+                     OperandW{Cb, T, TT, nullptr}, -1.0, 1.0);
+    gs.tri = 2;
+    if ((rc = L.gemm(gs, false, false, "schur"))) return rc;
   }
   ks::launch_compose_perm(nb, st);
   ++L.count[0];

@@ -94,6 +94,11 @@ cudaError_t dispatch(const GemmArgs& g, cudaStream_t st) {
   // measured on B200 with tools/gemm_variants.py: N <= 64 panels keep 128x64
   // tiles (8 warps, 32x32 warp tiles); wider outputs use 64x32 warp tiles
   // (128x64 CTA tiles) when K is long and 64x64 tiles with 4 stages otherwise
+  if (g.tri == 2 && (g.N <= 64 || g.M != g.N)) {
+    GemmArgs t = g;
+    t.tri = 0;
+    return dispatch<TA, TB>(t, st);
+  }
   if (g.N <= 16) return launch<128, 16, 4, 1, TA, TB, 3>(g, st);
   if (g.N <= 32) return launch<128, 32, 4, 1, TA, TB, 3>(g, st);
   if (g.N <= 64) {
@@ -102,7 +107,12 @@ cudaError_t dispatch(const GemmArgs& g, cudaStream_t st) {
     return launch<64, 64, 2, 2, TA, TB, 4>(g, st);
   }
   const long tiles = (long)((g.M + 127) / 128) * ((g.N + 63) / 64) * g.batch;
-  if (g.K >= 512 && tiles >= 2 * 148) return launch<128, 64, 2, 2, TA, TB, 3>(g, st);
+  if (g.K >= 512 && tiles >= 2 * 148) {
+    if (g.tri != 2) return launch<128, 64, 2, 2, TA, TB, 3>(g, st);
+    GemmArgs t = g;  // the mirrored form needs square tiles: compute the full result here
+    t.tri = 0;
+    return launch<128, 64, 2, 2, TA, TB, 3>(t, st);
+  }
   return launch<64, 64, 2, 2, TA, TB, 4>(g, st);
 }
 
@@ -132,12 +142,17 @@ cudaError_t gemm_group(const GemmGroup& gg, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
   for (int i = 0; i < gg.count; ++i) {
     const GemmArgs& q = gg.p[i];
-    if (q.M != g.M || q.N != g.N || q.K != g.K || q.batch != g.batch || q.tri) return cudaErrorInvalidValue;
+    if (q.M != g.M || q.N != g.N || q.K != g.K || q.batch != g.batch || q.tri == 1) return cudaErrorInvalidValue;
+    if (q.tri == 2 && q.M != q.N) return cudaErrorInvalidValue;
     if (((q.M | q.N | q.K) & 1) || q.K <= 0 || ((q.A.ld | q.B.ld | q.C.ld) & 1)) return cudaErrorInvalidValue;
   }
   // the same shape choice as gemm() for these products (K = s_pad < 512)
   const long tiles = (long)((g.M + 127) / 128) * ((g.N + 63) / 64) * g.batch * gg.count;
-  if (g.K >= 512 && tiles >= 2 * 148) return launch_group<128, 64, 2, 2, 3>(gg, st);
+  if (g.K >= 512 && tiles >= 2 * 148) {
+    GemmGroup t = gg;  // 128 x 64 tiles: symmetric problems are computed in full
+    for (int i = 0; i < t.count; ++i) t.p[i].tri = 0;
+    return launch_group<128, 64, 2, 2, 3>(t, st);
+  }
   return launch_group<64, 64, 2, 2, 4>(gg, st);
 }
 

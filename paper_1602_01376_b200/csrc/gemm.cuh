@@ -74,7 +74,9 @@ struct GemmArgs {
   Operand A, B;
   OperandW C;
   double alpha, beta;
-  int tri;  // 1: skip CTA tiles strictly above the diagonal of C
+  int tri;  // 1: skip CTA tiles strictly above the diagonal of C; 2 (EPI 0, square tiles): also
+            // store the transpose of every tile below the diagonal (a symmetric result
+            // computed on 10 of 16 tiles; the launchers clear it where tiles are not square)
   // EPI == 0: the beta term reads Cin instead of C when Cin.ptr is set (an
   // out-of-place C = alpha*AB + beta*Cin), and addI adds the identity
   // (C = alpha*AB + beta*Cin + I): the node assembly forms S = I - Y X and
@@ -499,6 +501,12 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
         }
       }
       *p = v;
+      if constexpr (EPI == 0 && BM == BN) {
+        if (g.tri == 2 && n0 < m0) {
+          C[(int64_t)c * g.C.ld + r] = v.x;
+          C[(int64_t)(c + 1) * g.C.ld + r] = v.y;
+        }
+      }
       if constexpr (EPI == 5) {  // SYRK: tiles below the diagonal also write their mirror image
         if (n0 < m0) {
           C[(int64_t)c * g.C.ld + r] = v.x;
