@@ -311,7 +311,6 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_up_coords, cudaEventDisableTiming));
     KS_CUDA(cudaEventCreateWithFlags(&f->ev_up_all, cudaEventDisableTiming));
     for (auto& e : f->ev_up_leaf) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto& e : f->ev_up_sub) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     f->ev_up_sublev.resize((size_t)ks_factor::kLeafChunks * f->npipe);
     for (auto& e : f->ev_up_sublev) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     f->ev_up_level.resize(f->levels.size());
@@ -385,8 +384,6 @@ int create_impl(const ks_problem* p, int device, int64_t shard_root, ks_factor**
         if (int rc = flush()) return rc;  // a milestone per subtree and level
         KS_CUDA(cudaEventRecord(f->ev_up_sublev[(size_t)c * f->npipe + lev], u));
       }
-      if (int rc = flush()) return rc;
-      KS_CUDA(cudaEventRecord(f->ev_up_sub[c], u));
     }
     for (size_t lev = 0; lev < f->levels.size(); ++lev) {
       for (int v : f->levels[lev])

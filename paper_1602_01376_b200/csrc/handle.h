@@ -202,7 +202,7 @@ struct ks_factor {
   // uploads started by ks_create, consumed by the first factorization
   static constexpr int kLeafChunks = 8;
   cudaStream_t upl = nullptr;
-  cudaEvent_t ev_up_coords = nullptr, ev_up_all = nullptr, ev_up_leaf[kLeafChunks] = {}, ev_up_sub[kLeafChunks] = {};
+  cudaEvent_t ev_up_coords = nullptr, ev_up_all = nullptr, ev_up_leaf[kLeafChunks] = {};
   std::vector<cudaEvent_t> ev_up_level;
   std::vector<cudaEvent_t> ev_up_sublev;  // [subtree][level < npipe]
   bool upload_pending = false;

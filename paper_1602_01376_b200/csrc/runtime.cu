@@ -310,8 +310,6 @@ void ks_destroy(ks_factor* f) {
   if (f->ev_up_all) cudaEventDestroy(f->ev_up_all);
   for (auto e : f->ev_up_leaf)
     if (e) cudaEventDestroy(e);
-  for (auto e : f->ev_up_sub)
-    if (e) cudaEventDestroy(e);
   for (auto e : f->ev_up_level)
     if (e) cudaEventDestroy(e);
   for (auto e : f->ev_up_sublev)
