@@ -107,12 +107,7 @@ cudaError_t dispatch(const GemmArgs& g, cudaStream_t st) {
     return launch<64, 64, 2, 2, TA, TB, 4>(g, st);
   }
   const long tiles = (long)((g.M + 127) / 128) * ((g.N + 63) / 64) * g.batch;
-  if (g.K >= 512 && tiles >= 2 * 148) {
-    if (g.tri != 2) return launch<128, 64, 2, 2, TA, TB, 3>(g, st);
-    GemmArgs t = g;  // the mirrored form needs square tiles: compute the full result here
-    t.tri = 0;
-    return launch<128, 64, 2, 2, TA, TB, 3>(t, st);
-  }
+  if (g.K >= 512 && tiles >= 2 * 148) return launch<128, 64, 2, 2, TA, TB, 3>(g, st);
   return launch<64, 64, 2, 2, TA, TB, 4>(g, st);
 }
 
@@ -148,11 +143,7 @@ cudaError_t gemm_group(const GemmGroup& gg, cudaStream_t st) {
   }
   // the same shape choice as gemm() for these products (K = s_pad < 512)
   const long tiles = (long)((g.M + 127) / 128) * ((g.N + 63) / 64) * g.batch * gg.count;
-  if (g.K >= 512 && tiles >= 2 * 148) {
-    GemmGroup t = gg;  // 128 x 64 tiles: symmetric problems are computed in full
-    for (int i = 0; i < t.count; ++i) t.p[i].tri = 0;
-    return launch_group<128, 64, 2, 2, 3>(t, st);
-  }
+  if (g.K >= 512 && tiles >= 2 * 148) return launch_group<128, 64, 2, 2, 3>(gg, st);
   return launch_group<64, 64, 2, 2, 4>(gg, st);
 }
 

@@ -74,9 +74,10 @@ struct GemmArgs {
   Operand A, B;
   OperandW C;
   double alpha, beta;
-  int tri;  // 1: skip CTA tiles strictly above the diagonal of C; 2 (EPI 0, square tiles): also
-            // store the transpose of every tile below the diagonal (a symmetric result
-            // computed on 10 of 16 tiles; the launchers clear it where tiles are not square)
+  int tri;  // 1: skip CTA tiles strictly above the diagonal of C (n0 >= m0 + BM); 2 (EPI 0,
+            // M == N, BM a multiple of BN): also store the transpose of every tile strictly
+            // below the diagonal (n0 + BN <= m0) -- a symmetric result from the tiles on
+            // and below the diagonal (10 of 16 with 64 x 64 tiles)
   // EPI == 0: the beta term reads Cin instead of C when Cin.ptr is set (an
   // out-of-place C = alpha*AB + beta*Cin), and addI adds the identity
   // (C = alpha*AB + beta*Cin + I): the node assembly forms S = I - Y X and
@@ -501,8 +502,8 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int b, int m0, int 
         }
       }
       *p = v;
-      if constexpr (EPI == 0 && BM == BN) {
-        if (g.tri == 2 && n0 < m0) {
+      if constexpr (EPI == 0) {
+        if (g.tri == 2 && n0 + BN <= m0) {  // a tile strictly below the diagonal: its transpose lies in skipped tiles
           C[(int64_t)c * g.C.ld + r] = v.x;
           C[(int64_t)(c + 1) * g.C.ld + r] = v.y;
         }
