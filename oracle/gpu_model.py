@@ -10,7 +10,7 @@ the same quantities through augmented factorizations:
            with its identity (1,1) block as pivot: only S = I - Y X is LU-
            factored with partial pivoting, as the first s_r columns of
               [[S, E],     E = P_r^T - Y P_l^T
-               [F, C]]     F = P_l H_l X - P_r H_r,  C = P_l H_l P_l^T
+               [F, C]]     F = P_l H_l X - P_r H_r = -E^T H_r,  C = P_l H_l P_l^T
            (pivots among S's rows); the trailing block is C - F S^-1 E =
            P G Z^-1 P^T = H (solver.py:154-164).
   solve  : up   leaf z = L^-1 b, c = L21 z;
@@ -73,7 +73,7 @@ def factorize_model(prob: Problem, lam: float):
             Aug = np.zeros((s_r + s, s_r + s))
             Aug[:s_r, :s_r] = np.eye(s_r) - Y @ X
             Aug[:s_r, s_r:] = Pr.T - Y @ Pl.T
-            Aug[s_r:, :s_r] = PHl @ X - Pr @ Hr
+            Aug[s_r:, :s_r] = -Aug[:s_r, s_r:].T @ Hr  # = P_l H_l X - P_r H_r (H symmetric): one product
             Aug[s_r:, s_r:] = PHl @ Pl.T
             LU, piv = _lu_restricted(Aug, s_r)
             F["node"][v] = (LU, piv, B, X, Y, PHl, s_l, s_r)

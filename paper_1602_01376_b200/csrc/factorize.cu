@@ -306,43 +306,47 @@ static int enqueue_level_body(ks_factor* f, Launcher& L, const ks::NodeBatch& nb
   double* Cb = nb.Aug + (int64_t)S * T + S;
   // stage 1 (independent products, one launch; H is exactly symmetric, so it
   // is read row-major as the right factor):
-  //   X = B H_r,  Y = B^T H_l,  P_l H_l,  F = -P_r H_r
+  //   X = B H_r,  Y = B^T H_l,  P_l H_l
   // stage 2 (one launch; S and E are written out of place, nothing of Aug is
   // initialized beforehand):
-  //   S = I - Y X,  E = P_r^T - Y P_l^T,  F += (P_l H_l) X,  C = (P_l H_l) P_l^T
+  //   S = I - Y X,  E = P_r^T - Y P_l^T,  C = (P_l H_l) P_l^T
+  // stage 3:
+  //   F = P_l H_l X - P_r H_r = -E^T H_r   (F^T = X^T H_l P_l^T - H_r P_r^T = H_r (Y P_l^T - P_r^T):
+  //   one product instead of two)
   {
     ks::GemmGroup g1{};
-    g1.count = 4;
+    g1.count = 3;
     g1.p[0] = mk(S, S, S, cnt, Operand{nb.Bc, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
                  OperandW{Xb, S, XS, nullptr}, 1.0, 0.0);
     g1.p[1] = mk(S, S, S, cnt, Operand{nb.BcT, S, SS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
                  OperandW{Yb, S, XS, nullptr}, 1.0, 0.0);
     g1.p[2] = mk(S, S, S, cnt, Operand{nb.Pn, ZT, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.left},
                  OperandW{nb.PHl, S, SS, nullptr}, 1.0, 0.0);
-    g1.p[3] = mk(S, S, S, cnt, Operand{nb.Pn + S, ZT, PS, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
-                 OperandW{Fb, T, TT, nullptr}, -1.0, 0.0);
     ++L.count[0];
     if (abl & 64) {
     } else if (cudaError_t e = ks::gemm_group(g1, st)) return fail(KS_ERR_CUDA, "assembly stage 1: %s", cudaGetErrorString(e));
     if ((rc = L.check("assembly1"))) return rc;
     const int64_t PTS = (int64_t)ZT * S;
     ks::GemmGroup g2{};
-    g2.count = 4;
+    g2.count = 3;
     g2.p[0] = mk(S, S, S, cnt, Operand{Yb, S, XS, nullptr}, Operand{Xb, S, XS, nullptr}, OperandW{Sb, T, TT, nullptr},
                  -1.0, 0.0);
     g2.p[0].addI = 1;
     g2.p[1] = mk(S, S, S, cnt, Operand{Yb, S, XS, nullptr}, Operand{nb.PT, S, PTS, nullptr},
                  OperandW{Eb, T, TT, nullptr}, -1.0, 1.0);
     g2.p[1].Cin = Operand{nb.PT + SS, S, PTS, nullptr};  // P_r^T
-    g2.p[2] = mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{Xb, S, XS, nullptr},
-                 OperandW{Fb, T, TT, nullptr}, 1.0, 1.0);
-    g2.p[3] = mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{nb.PT, S, PTS, nullptr},
+    g2.p[2] = mk(S, S, S, cnt, Operand{nb.PHl, S, SS, nullptr}, Operand{nb.PT, S, PTS, nullptr},
                  OperandW{Cb, T, TT, nullptr}, 1.0, 0.0);
-    g2.p[3].tri = 2;  // C = P_l H_l P_l^T is symmetric: tiles on and below the diagonal, mirrored
+    g2.p[2].tri = 2;  // C = P_l H_l P_l^T is symmetric: tiles on and below the diagonal, mirrored
     ++L.count[0];
     if (abl & 64) {
     } else if (cudaError_t e = ks::gemm_group(g2, st)) return fail(KS_ERR_CUDA, "assembly stage 2: %s", cudaGetErrorString(e));
     if ((rc = L.check("assembly2"))) return rc;
+    if (!(abl & 64)) {
+      if ((rc = L.gemm(mk(S, S, S, cnt, Operand{Eb, T, TT, nullptr}, Operand{f->hbuf.p, S, SS, nb.right},
+                          OperandW{Fb, T, TT, nullptr}, -1.0, 0.0), true, false, "assembly3")))
+        return rc;
+    }
   }
   ks::launch_znorm1(nb, st);  // ||Z||_1 for the condition estimate (linalg.py:176)
   ++L.count[0];
